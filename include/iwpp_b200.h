@@ -1,0 +1,158 @@
+/*
+ * iwpp_b200.h -- C ABI of the B200-native IWPP library (libiwpp_b200.so).
+ *
+ * Drop-in boundary for the hot path of the reference package "gridwave"
+ * (/root/reference/pkg/src/gridwave).  The reference has no C ABI: its
+ * "native" layer is numba-JIT kernels called from Python
+ * (_kernels.py, cited K.<line>).  Each entry point below replaces one
+ * reference call (file:line given per function); the Python package
+ * paper_1209_3314_b200 binds these with ctypes exactly where the
+ * reference's operators call their kernels.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Image buffers are row-major (H, W),
+ *    C-contiguous, DEVICE pointers unless the function name ends in _host.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  All work is enqueued on it; a function synchronizes the
+ *    stream only when it must return a host-visible result (stats != NULL,
+ *    *_host variants, error flags).
+ *  - Scratch memory is caller-owned: query *_workspace_bytes(), allocate
+ *    that many bytes of device memory (256-byte aligned), pass it in.
+ *    The library never allocates device memory itself.
+ *  - Return value: IWPP_OK (0) or a negative IWPP_E* status;
+ *    iwpp_last_error() returns a thread-local message for the last failure.
+ *    The Python layer maps statuses onto the reference's exceptions
+ *    (errors.py:4-25): CONTRACT -> ContractViolation,
+ *    NO_BACKGROUND -> NoBackgroundError, ENGINE_LIMIT -> EngineError.
+ */
+#ifndef IWPP_B200_H
+#define IWPP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element kinds (grid.py:22-27 plus int32) */
+enum iwpp_dtype {
+  IWPP_U8 = 0,  /* "u8" and "binary" */
+  IWPP_U16 = 1, /* "u16" */
+  IWPP_I32 = 2, /* "i32" (not an Image2D kind in the reference; its kernels accept it) */
+};
+
+enum iwpp_status {
+  IWPP_OK = 0,
+  IWPP_E_CONTRACT = -1,      /* precondition violated (marker > mask, bad dims/kind/conn) */
+  IWPP_E_NO_BACKGROUND = -2, /* EDT finalize saw an unassigned cell (edt.py:275-276) */
+  IWPP_E_ENGINE_LIMIT = -3,  /* max_rounds exceeded (engine.py:311-317) */
+  IWPP_E_CUDA = -4,          /* CUDA runtime error */
+  IWPP_E_WORKSPACE = -5,     /* workspace too small */
+  IWPP_E_OVERFLOW = -6,      /* queue overflow not resolved by rescans */
+};
+
+/* Counters mirrored from RunStats (engine.py:46-59) plus device-engine
+ * counters.  Filled only when a non-NULL pointer is passed (forces a sync). */
+typedef struct iwpp_stats {
+  int64_t rounds;          /* EDT: two-phase rounds; recon: 0 (asynchronous engine) */
+  int64_t executions;      /* engine executions (overflow re-runs included) */
+  int64_t overflow_count;  /* block-queue overflows resolved by an in-tile rescan */
+  int64_t queued_total;    /* queue insertions (pixels) */
+  int64_t seeds;           /* initial wavefront size (pixels) */
+  int64_t tiles_processed; /* recon: tile activations (incl. re-runs) */
+  int64_t tile_reruns;     /* recon: activations caused by a neighbour's border change */
+  int64_t contract_violations; /* recon: cells with marker > mask seen by the engine */
+  int64_t n_inf;           /* EDT: cells left without a source */
+} iwpp_stats;
+
+/* ---- library -------------------------------------------------------- */
+const char *iwpp_last_error(void);
+const char *iwpp_version(void);
+/* Device properties the engines size themselves by (SM count etc.). */
+int iwpp_device_info(int device, int *sm_count, int *cc_major, int *cc_minor);
+
+/* ---- morphological reconstruction by dilation -----------------------
+ * Replaces recon_fh / recon_sr / recon_qb / recon_parallel / recon_tiled
+ * (recon.py:164-342): their common fixed point is unique, so every entry
+ * routes to one device engine.  J (marker in, result out, in place) and I
+ * (mask) are device buffers of `dtype`.  conn is 4 or 8.
+ * The engine = row/column clamp-scan sweeps (K.115-190 semantics) +
+ * persistent tile engine (in-tile seed detection K.193-217, warp-aggregated
+ * shared-memory queue propagation K.220-270 semantics, global tile queue).
+ */
+typedef struct iwpp_recon_opts {
+  int sweeps;        /* full-image row/col sweep pairs before the tile engine (-1 = auto) */
+  int max_blocks;    /* persistent grid size cap (0 = auto) */
+  int check_contract;/* 1: count cells with marker > mask (stats->contract_violations) */
+  int queue_capacity;/* block-queue capacity (0 = default 4608); smaller values force the
+                        overflow -> rescan path (QueueConfig.gbq_capacity, wqueue.py:58-60) */
+} iwpp_recon_opts;
+
+size_t iwpp_recon_workspace_bytes(int64_t W, int64_t H, int dtype, int conn);
+int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn,
+               void *workspace, size_t workspace_bytes, const iwpp_recon_opts *opts,
+               iwpp_stats *stats, void *stream);
+
+/* Host-buffer variant (the e2e path of the reference-facing call):
+ * copies marker/mask host->device (into the workspace), runs iwpp_recon,
+ * copies the result device->host into `out`, synchronizes.  Host buffers
+ * may be pageable or pinned.  Returns IWPP_E_CONTRACT if marker > mask
+ * anywhere (ReconInput.__post_init__, recon.py:60-61). */
+size_t iwpp_recon_host_workspace_bytes(int64_t W, int64_t H, int dtype, int conn);
+int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W,
+                    int64_t H, int dtype, int conn, void *workspace,
+                    size_t workspace_bytes, const iwpp_recon_opts *opts,
+                    iwpp_stats *stats, void *stream);
+
+/* marker <= mask check (recon.py:60): *n_violations_host = count. Syncs. */
+int iwpp_check_le(const void *J, const void *I, int64_t n, int dtype,
+                  void *workspace, int64_t *n_violations_host, void *stream);
+
+/* Individual stages (for the stage-level parity tests and the tiled /
+ * multi-GPU drivers). */
+/* Row sweeps forward+backward (K.115-139, exact clamp-composition scan). */
+int iwpp_recon_sweep_rows(void *J, const void *I, int64_t W, int64_t H, int dtype,
+                          void *stream);
+/* Column sweeps forward+backward (K.142-190, vertical part exact). */
+int iwpp_recon_sweep_cols(void *J, const void *I, int64_t W, int64_t H, int dtype,
+                          void *stream);
+/* Full-neighbourhood seed scan (K.193-217): writes active pixels (packed
+ * y*W+x, int64, raster order NOT guaranteed) to out; *n_host = count. */
+int iwpp_recon_seed_scan(const void *J, const void *I, int64_t W, int64_t H,
+                         int dtype, int conn, int64_t *out, int64_t *n_host,
+                         void *workspace, void *stream);
+
+/* ---- Euclidean distance transform ----------------------------------
+ * Replaces edt() / edt_propagate() / finalize_distance_map()
+ * (edt.py:248-294).  Level-synchronous two-phase rounds (K.403-433,
+ * edt.py:217-226) with the (d^2, packed index) total order (K.320-336):
+ * bit-identical to the reference's canonical schedule. */
+size_t iwpp_edt_workspace_bytes(int64_t W, int64_t H, int conn);
+/* mask: device u8 (0 = background).  vr: device int64 (H,W) out (packed
+ * source, -1 = INF).  dist: device f32 (H,W) out, or NULL.
+ * Returns IWPP_E_NO_BACKGROUND when some cell has no source (vr is still
+ * written, dist is not meaningful). */
+int iwpp_edt(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *vr,
+             float *dist, void *workspace, size_t workspace_bytes,
+             int64_t max_rounds, iwpp_stats *stats, void *stream);
+/* edt_propagate (edt.py:248-269): vr in/out (device int64), seeds device
+ * int64 packed (duplicates allowed). */
+int iwpp_edt_propagate(int64_t *vr, int64_t W, int64_t H, int conn,
+                       const int64_t *seeds, int64_t n_seeds, void *workspace,
+                       size_t workspace_bytes, int64_t max_rounds,
+                       iwpp_stats *stats, void *stream);
+/* finalize_distance_map (edt.py:272-281): dist = f32(sqrt(f64(d2))).
+ * Returns IWPP_E_NO_BACKGROUND if any vr == -1.  d2 may be NULL. */
+int iwpp_edt_finalize(const int64_t *vr, int64_t W, int64_t H, float *dist,
+                      int64_t *d2, void *workspace, void *stream);
+/* Host-buffer variant: mask host -> device, edt, vr/dist device -> host. */
+size_t iwpp_edt_host_workspace_bytes(int64_t W, int64_t H, int conn);
+int iwpp_edt_host(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *vr,
+                  float *dist, void *workspace, size_t workspace_bytes,
+                  int64_t max_rounds, iwpp_stats *stats, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IWPP_B200_H */

@@ -1,0 +1,150 @@
+"""ctypes binding of libiwpp_b200.so (the C ABI in include/iwpp_b200.h).
+
+There is no CPU fallback: if the shared object is missing or no CUDA
+device is visible, every operator raises ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import ContractViolation, EngineError, NoBackgroundError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libiwpp_b200.so")
+
+IWPP_OK = 0
+IWPP_E_CONTRACT = -1
+IWPP_E_NO_BACKGROUND = -2
+IWPP_E_ENGINE_LIMIT = -3
+IWPP_E_CUDA = -4
+IWPP_E_WORKSPACE = -5
+IWPP_E_OVERFLOW = -6
+
+# every symbol the header declares (checked by tests/test_capi.py)
+EXPORTS = (
+    "iwpp_last_error", "iwpp_version", "iwpp_device_info",
+    "iwpp_recon_workspace_bytes", "iwpp_recon", "iwpp_recon_host_workspace_bytes",
+    "iwpp_recon_host", "iwpp_check_le", "iwpp_recon_sweep_rows", "iwpp_recon_sweep_cols",
+    "iwpp_recon_seed_scan", "iwpp_edt_workspace_bytes", "iwpp_edt", "iwpp_edt_propagate",
+    "iwpp_edt_finalize", "iwpp_edt_host_workspace_bytes", "iwpp_edt_host",
+)
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in (
+        "rounds", "executions", "overflow_count", "queued_total", "seeds",
+        "tiles_processed", "tile_reruns", "contract_violations", "n_inf")]
+
+    def as_dict(self) -> dict:
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class ReconOpts(ctypes.Structure):
+    _fields_ = [("sweeps", ctypes.c_int), ("max_blocks", ctypes.c_int),
+                ("check_contract", ctypes.c_int), ("queue_capacity", ctypes.c_int)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load and prototype the library without touching the GPU."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise RuntimeError(
+                f"libiwpp_b200.so not built ({path}); run __graft_entry__.build() "
+                "or python -m paper_1209_3314_b200.build")
+        L = ctypes.CDLL(path)
+        P, I64, I, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+        SP = ctypes.POINTER(Stats)
+        OP = ctypes.POINTER(ReconOpts)
+        proto = {
+            "iwpp_last_error": ([], ctypes.c_char_p),
+            "iwpp_version": ([], ctypes.c_char_p),
+            "iwpp_device_info": ([I, ctypes.POINTER(I), ctypes.POINTER(I), ctypes.POINTER(I)], I),
+            "iwpp_recon_workspace_bytes": ([I64, I64, I, I], SZ),
+            "iwpp_recon": ([P, P, I64, I64, I, I, P, SZ, OP, SP, P], I),
+            "iwpp_recon_host_workspace_bytes": ([I64, I64, I, I], SZ),
+            "iwpp_recon_host": ([P, P, P, I64, I64, I, I, P, SZ, OP, SP, P], I),
+            "iwpp_check_le": ([P, P, I64, I, P, ctypes.POINTER(I64), P], I),
+            "iwpp_recon_sweep_rows": ([P, P, I64, I64, I, P], I),
+            "iwpp_recon_sweep_cols": ([P, P, I64, I64, I, P], I),
+            "iwpp_recon_seed_scan": ([P, P, I64, I64, I, I, P, ctypes.POINTER(I64), P, P], I),
+            "iwpp_edt_workspace_bytes": ([I64, I64, I], SZ),
+            "iwpp_edt": ([P, I64, I64, I, P, P, P, SZ, I64, SP, P], I),
+            "iwpp_edt_propagate": ([P, I64, I64, I, P, I64, P, SZ, I64, SP, P], I),
+            "iwpp_edt_finalize": ([P, I64, I64, P, P, P, P], I),
+            "iwpp_edt_host_workspace_bytes": ([I64, I64, I], SZ),
+            "iwpp_edt_host": ([P, I64, I64, I, P, P, P, SZ, I64, SP, P], I),
+        }
+        for name, (args, res) in proto.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+        return L
+
+
+def lib():
+    """The library, with a CUDA device required (fails loudly otherwise)."""
+    L = load_library()
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1209_3314_b200 needs a CUDA device (B200, sm_100a); none visible")
+    return L
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def check(rc: int, what: str = ""):
+    if rc == IWPP_OK:
+        return
+    msg = _lib.iwpp_last_error().decode(errors="replace") if _lib else ""
+    msg = f"{what}: {msg}" if what else msg
+    if rc == IWPP_E_CONTRACT:
+        raise ContractViolation(msg)
+    if rc == IWPP_E_NO_BACKGROUND:
+        raise NoBackgroundError(msg)
+    if rc == IWPP_E_ENGINE_LIMIT:
+        raise EngineError(msg)
+    raise RuntimeError(f"iwpp error {rc}: {msg}")
+
+
+# -- workspace cache (one growable device buffer per device) ---------------
+_ws = {}
+
+
+def workspace(nbytes: int):
+    """A device byte buffer of at least nbytes on the current device.  The
+    buffer is reused by later calls on the same stream order; callers that
+    run concurrently on several streams must pass their own."""
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    buf = _ws.get(dev)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=f"cuda:{dev}")
+        _ws[dev] = buf
+    return buf
+
+
+def stream_ptr():
+    return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(a):
+    """Raw pointer of a numpy array or torch tensor."""
+    if isinstance(a, np.ndarray):
+        return ctypes.c_void_p(a.ctypes.data)
+    return ctypes.c_void_p(a.data_ptr())

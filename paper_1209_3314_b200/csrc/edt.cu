@@ -1,0 +1,433 @@
+// edt.cu -- level-synchronous wavefront EDT for sm_100a.
+//
+// Reference: edt.py:187-294 and the kernels K.309-433.  The reference pins
+// ONE canonical schedule: two-phase rounds where every offer in
+// round r uses the source its sender held at the start of round r, and a
+// target adopts a candidate iff it is closer, or equally close with a
+// smaller packed index (closer_source, K.320-336).  The end-of-round state is
+// then the per-cell minimum of {start value, offers} under that total order,
+// which is what this engine computes -- bit-identical to the reference.
+//
+// Design (B200):
+//  * state: source per cell as a 32-bit (sy << 16 | sx) code.  Lexicographic
+//    (y, x) order equals packed-index order, so the index tie-break is a
+//    plain unsigned compare and no divisions are needed.  INF = 0xFFFFFFFF.
+//  * double-buffered state (RD = start of round, WR = being built): one grid
+//    barrier per round instead of two.  WR lags RD exactly on the current
+//    frontier, which each frontier item re-syncs before offering.
+//  * offers: read RD[q] (plain load); only an offer that beats the
+//    round-start value does a CAS-min on WR[q] and claims q for the next
+//    frontier through a per-cell round stamp (dedupe), pushed with
+//    warp-aggregated reservations into the global frontier queue.
+//  * one persistent cooperative kernel runs all rounds with a device-side
+//    grid barrier (no host round trips); the frontier-size counters are
+//    triple-buffered so no block can reset a counter another still reads.
+//  * finalize fused: packed int64 vr and float32(sqrt(float64(d2)))
+//    (edt.py:278-280 -- __dsqrt_rn then RN to float), INF count for
+//    NoBackgroundError.
+
+#include "edt.cuh"
+
+namespace iwpp {
+namespace edt {
+
+__device__ __forceinline__ long long sqd_yx(int qx, int qy, uint32_t s) {
+  int sy = (int)(s >> 16), sx = (int)(s & 0xffffu);
+  long long dx = qx - sx, dy = qy - sy;
+  return dx * dx + dy * dy;
+}
+
+// K.320-336 closer_source on yx codes
+__device__ __forceinline__ bool closer(int qx, int qy, uint32_t cand, uint32_t held) {
+  if (held == INF32) return cand != INF32;
+  if (cand == INF32) return false;
+  long long dc = sqd_yx(qx, qy, cand), dh = sqd_yx(qx, qy, held);
+  if (dc != dh) return dc < dh;
+  return cand < held;
+}
+
+// WR[q] <- min(WR[q], cand) in the order at q
+__device__ __forceinline__ void cas_min(uint32_t *WR, size_t q, int qx, int qy, uint32_t cand) {
+  uint32_t old = __ldcg(WR + q);
+  while (closer(qx, qy, cand, old)) {
+    uint32_t prev = atomicCAS(WR + q, old, cand);
+    if (prev == old) return;
+    old = prev;
+  }
+}
+
+__device__ void grid_barrier(unsigned *count, unsigned *gen, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned g = ld_acquire(gen);
+    __threadfence();
+    unsigned arrived = atomicAdd(count, 1u);
+    if (arrived == nblocks - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (ld_acquire(gen) == g) __nanosleep(16);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ---- init: fused assign (K.339-348) + contour seeds (K.351-373) -----------
+template <int CONN>
+__global__ void edt_init_kernel(const uint8_t *__restrict__ mask, int W, int H, EdtState s) {
+  const unsigned FULL = 0xffffffffu;
+  size_t n = (size_t)W * H;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t base = (size_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n;
+       base += stride) {
+    size_t p = base + (threadIdx.x & 31u);
+    bool push = false;
+    uint32_t yx = 0;
+    if (p < n) {
+      int py = (int)(p / (unsigned)W), px = (int)(p - (size_t)py * W);
+      yx = ((uint32_t)py << 16) | (uint32_t)px;
+      bool bg = mask[p] == 0;
+      uint32_t v = bg ? yx : INF32;
+      s.buf[0][p] = v;
+      s.buf[1][p] = v;
+      s.stamp[p] = 0;
+      if (bg) {
+#pragma unroll
+        for (int k = 0; k < Nbr<CONN>::N; k++) {
+          int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+          if (qx >= 0 && qx < W && qy >= 0 && qy < H && mask[(size_t)qy * W + qx] != 0) push = true;
+        }
+      }
+    }
+    unsigned pos = warp_reserve(&s.cnt[0], push ? 1u : 0u, FULL);
+    if (push) s.F[0][pos] = yx;
+  }
+}
+
+// ---- import a user source map + seeds (edt_propagate) ----------------------
+__global__ void edt_import_kernel(const int64_t *__restrict__ vr, int W, int H, EdtState s) {
+  size_t n = (size_t)W * H;
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (size_t)gridDim.x * blockDim.x) {
+    int64_t v = vr[p];
+    uint32_t c;
+    if (v < 0) {
+      c = INF32;
+    } else if (v >= (int64_t)n) {
+      c = INF32;
+      atomicAdd(&s.counters[EC_BAD], 1ull);
+    } else {
+      int sy = (int)(v / W), sx = (int)(v - (int64_t)sy * W);
+      c = ((uint32_t)sy << 16) | (uint32_t)sx;
+    }
+    s.buf[0][p] = c;
+    s.buf[1][p] = c;
+    s.stamp[p] = 0;
+  }
+}
+
+__global__ void edt_seed_kernel(const int64_t *__restrict__ seeds, int64_t n_seeds, int W, int H,
+                                EdtState s) {
+  const unsigned FULL = 0xffffffffu;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n_seeds;
+       base += stride) {
+    int64_t i = base + (threadIdx.x & 31u);
+    bool push = false;
+    uint32_t yx = 0;
+    if (i < n_seeds) {
+      int64_t p = seeds[i];
+      if (p < 0 || p >= (int64_t)W * H) {
+        atomicAdd(&s.counters[EC_BAD], 1ull);
+      } else {
+        int py = (int)(p / W), px = (int)(p - (int64_t)py * W);
+        yx = ((uint32_t)py << 16) | (uint32_t)px;
+        push = atomicExch(&s.stamp[p], SEED_STAMP) != SEED_STAMP;
+      }
+    }
+    unsigned pos = warp_reserve(&s.cnt[0], push ? 1u : 0u, FULL);
+    if (push) s.F[0][pos] = yx;
+  }
+}
+
+// ---- the round engine ------------------------------------------------------
+template <int CONN>
+__global__ void __launch_bounds__(kRoundThreads) edt_rounds_kernel(int W, int H, EdtState s,
+                                                                   long long max_rounds) {
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned long long visits = 0;
+  int r = 0;
+  for (;; r++) {
+    unsigned n = ld_acquire(&s.cnt[r % 3]);
+    if (n == 0) break;
+    if (max_rounds >= 0 && r >= max_rounds) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) s.counters[EC_LIMIT] = 1;
+      break;
+    }
+    const uint32_t *RD = s.buf[r & 1];
+    uint32_t *WR = s.buf[(r + 1) & 1];
+    const uint32_t *cur = s.F[r & 1];
+    uint32_t *nxt = s.F[(r + 1) & 1];
+    unsigned *ncnt = &s.cnt[(r + 1) % 3];
+    const uint32_t stamp_r = (uint32_t)r + 1u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      s.cnt[(r + 2) % 3] = 0;
+      visits += n;
+    }
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+      unsigned i = base + lane;
+      unsigned mask = 0;
+      int px = 0, py = 0;
+      if (i < n) {
+        uint32_t pyx = __ldcg(cur + i);
+        py = (int)(pyx >> 16);
+        px = (int)(pyx & 0xffffu);
+        size_t p = (size_t)py * W + px;
+        uint32_t src = __ldcg(RD + p);
+        cas_min(WR, p, px, py, src);  // WR lags RD on the frontier
+        if (src != INF32) {
+#pragma unroll
+          for (int k = 0; k < Nbr<CONN>::N; k++) {
+            int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+            if (qx >= 0 && qx < W && qy >= 0 && qy < H) {
+              size_t q = (size_t)qy * W + qx;
+              uint32_t held = __ldcg(RD + q);
+              if (closer(qx, qy, src, held)) {
+                cas_min(WR, q, qx, qy, src);
+                if (__ldcg(s.stamp + q) != stamp_r && atomicExch(s.stamp + q, stamp_r) != stamp_r)
+                  mask |= 1u << k;
+              }
+            }
+          }
+        }
+      }
+      unsigned c = __popc(mask);
+      unsigned pos = warp_reserve(ncnt, c, FULL);
+      while (mask) {
+        int k = __ffs(mask) - 1;
+        mask &= mask - 1;
+        int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+        nxt[pos++] = ((uint32_t)qy << 16) | (uint32_t)qx;
+      }
+    }
+    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s.counters[EC_ROUNDS] = (unsigned long long)r;
+    s.counters[EC_VISITS] = visits;
+    s.counters[EC_FINAL] = (unsigned long long)(r & 1);
+  }
+}
+
+// ---- finalize (edt.py:272-281) --------------------------------------------
+__global__ void edt_finalize_kernel(const uint32_t *__restrict__ st, int W, int H,
+                                    int64_t *__restrict__ vr, float *__restrict__ dist,
+                                    int64_t *__restrict__ d2out, unsigned long long *counters) {
+  size_t n = (size_t)W * H;
+  unsigned long long ninf = 0;
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (size_t)gridDim.x * blockDim.x) {
+    uint32_t s = st[p];
+    if (s == INF32) {
+      ninf++;
+      if (vr) vr[p] = -1;
+      if (dist) dist[p] = 0.f;
+      if (d2out) d2out[p] = (int64_t)1 << 62;
+      continue;
+    }
+    int py = (int)(p / (unsigned)W), px = (int)(p - (size_t)py * W);
+    int sy = (int)(s >> 16), sx = (int)(s & 0xffffu);
+    long long dx = px - sx, dy = py - sy, d2 = dx * dx + dy * dy;
+    if (vr) vr[p] = (int64_t)sy * W + sx;
+    if (dist) dist[p] = __double2float_rn(__dsqrt_rn((double)d2));
+    if (d2out) d2out[p] = d2;
+  }
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 16);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 8);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 4);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 2);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 1);
+  if ((threadIdx.x & 31) == 0 && ninf) atomicAdd(&counters[EC_NINF], ninf);
+}
+
+// finalize directly from an int64 source map (iwpp_edt_finalize)
+__global__ void edt_finalize_vr_kernel(const int64_t *__restrict__ vr, int W, int H,
+                                       float *__restrict__ dist, int64_t *__restrict__ d2out,
+                                       unsigned long long *counters) {
+  size_t n = (size_t)W * H;
+  unsigned long long ninf = 0;
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (size_t)gridDim.x * blockDim.x) {
+    int64_t s = vr[p];
+    if (s < 0) {
+      ninf++;
+      if (dist) dist[p] = 0.f;
+      if (d2out) d2out[p] = (int64_t)1 << 62;
+      continue;
+    }
+    int64_t py = (int64_t)(p / (unsigned)W), px = (int64_t)p - py * W;
+    int64_t sy = s / W, sx = s - sy * W;
+    long long dx = px - sx, dy = py - sy, d2 = dx * dx + dy * dy;
+    if (dist) dist[p] = __double2float_rn(__dsqrt_rn((double)d2));
+    if (d2out) d2out[p] = d2;
+  }
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 16);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 8);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 4);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 2);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 1);
+  if ((threadIdx.x & 31) == 0 && ninf) atomicAdd(&counters[EC_NINF], ninf);
+}
+
+// ---- host side -------------------------------------------------------------
+
+size_t state_bytes(int64_t W, int64_t H) {
+  size_t n = (size_t)W * H;
+  Carver c(nullptr);
+  c.take<uint32_t>(n);
+  c.take<uint32_t>(n);
+  c.take<uint32_t>(n);
+  c.take<uint32_t>(n);
+  c.take<uint32_t>(n);
+  c.take<unsigned>(8);
+  c.take<unsigned long long>(EC_N);
+  return c.off + 256;
+}
+
+EdtState carve_state(Carver &c, int64_t W, int64_t H) {
+  size_t n = (size_t)W * H;
+  EdtState s;
+  s.buf[0] = c.take<uint32_t>(n);
+  s.buf[1] = c.take<uint32_t>(n);
+  s.stamp = c.take<uint32_t>(n);
+  s.F[0] = c.take<uint32_t>(n);
+  s.F[1] = c.take<uint32_t>(n);
+  unsigned *ctl = c.take<unsigned>(8);
+  s.cnt = ctl;      // [0..2]
+  s.bar = ctl + 4;  // [4..5]
+  s.counters = c.take<unsigned long long>(EC_N);
+  return s;
+}
+
+static int grid_for(size_t n, int threads) {
+  size_t b = (n + threads - 1) / threads;
+  size_t cap = (size_t)device_sm_count() * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+int reset_control(const EdtState &s, cudaStream_t st) {
+  IWPP_CUDA_TRY(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * 8, st));
+  IWPP_CUDA_TRY(cudaMemsetAsync(s.counters, 0, sizeof(unsigned long long) * EC_N, st));
+  return IWPP_OK;
+}
+
+int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, cudaStream_t st) {
+  size_t n = (size_t)W * H;
+  int g = grid_for(n, 256);
+  if (conn == 8)
+    edt_init_kernel<8><<<g, 256, 0, st>>>(mask, W, H, s);
+  else
+    edt_init_kernel<4><<<g, 256, 0, st>>>(mask, W, H, s);
+  IWPP_CUDA_TRY(cudaGetLastError());
+  return IWPP_OK;
+}
+
+int launch_import(const int64_t *vr, const int64_t *seeds, int64_t n_seeds, int W, int H,
+                  const EdtState &s, cudaStream_t st) {
+  size_t n = (size_t)W * H;
+  edt_import_kernel<<<grid_for(n, 256), 256, 0, st>>>(vr, W, H, s);
+  IWPP_CUDA_TRY(cudaGetLastError());
+  if (n_seeds > 0) {
+    edt_seed_kernel<<<grid_for((size_t)n_seeds, 256), 256, 0, st>>>(seeds, n_seeds, W, H, s);
+    IWPP_CUDA_TRY(cudaGetLastError());
+  }
+  return IWPP_OK;
+}
+
+int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_rounds,
+                  cudaStream_t st) {
+  void *kern = conn == 8 ? (void *)edt_rounds_kernel<8> : (void *)edt_rounds_kernel<4>;
+  static int blocks_cache[2] = {0, 0};
+  int &blocks = blocks_cache[conn == 8];
+  if (blocks == 0) {
+    int per_sm = 0;
+    IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRoundThreads, 0));
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > kRoundBlocksPerSm) per_sm = kRoundBlocksPerSm;
+    blocks = device_sm_count() * per_sm;
+  }
+  int w = W, h = H;
+  EdtState ss = s;
+  void *args[] = {&w, &h, &ss, &max_rounds};
+  IWPP_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(kRoundThreads), args, 0, st));
+  return IWPP_OK;
+}
+
+int launch_finalize(const EdtState &s, int final_buf, int W, int H, int64_t *vr, float *dist,
+                    int64_t *d2, cudaStream_t st) {
+  size_t n = (size_t)W * H;
+  edt_finalize_kernel<<<grid_for(n, 256), 256, 0, st>>>(s.buf[final_buf], W, H, vr, dist, d2,
+                                                         s.counters);
+  IWPP_CUDA_TRY(cudaGetLastError());
+  return IWPP_OK;
+}
+
+int launch_finalize_vr(const int64_t *vr, int W, int H, float *dist, int64_t *d2,
+                       unsigned long long *counters, cudaStream_t st) {
+  size_t n = (size_t)W * H;
+  edt_finalize_vr_kernel<<<grid_for(n, 256), 256, 0, st>>>(vr, W, H, dist, d2, counters);
+  IWPP_CUDA_TRY(cudaGetLastError());
+  return IWPP_OK;
+}
+
+// The final state lives in buf[rounds & 1]; the rounds kernel records it in
+// counters[EC_FINAL].  A tiny copy kernel selects it on the device so the
+// whole pipeline stays asynchronous.
+__global__ void edt_select_final_kernel(EdtState s, int W, int H, int64_t *vr, float *dist,
+                                        int64_t *d2) {
+  // launched with the same grid as finalize; reads the flag once per thread
+  int fb = (int)s.counters[EC_FINAL];
+  const uint32_t *st = s.buf[fb];
+  size_t n = (size_t)W * H;
+  unsigned long long ninf = 0;
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (size_t)gridDim.x * blockDim.x) {
+    uint32_t c = st[p];
+    if (c == INF32) {
+      ninf++;
+      if (vr) vr[p] = -1;
+      if (dist) dist[p] = 0.f;
+      if (d2) d2[p] = (int64_t)1 << 62;
+      continue;
+    }
+    int py = (int)(p / (unsigned)W), px = (int)(p - (size_t)py * W);
+    int sy = (int)(c >> 16), sx = (int)(c & 0xffffu);
+    long long dx = px - sx, dy = py - sy, dd = dx * dx + dy * dy;
+    if (vr) vr[p] = (int64_t)sy * W + sx;
+    if (dist) dist[p] = __double2float_rn(__dsqrt_rn((double)dd));
+    if (d2) d2[p] = dd;
+  }
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 16);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 8);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 4);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 2);
+  ninf += __shfl_xor_sync(0xffffffffu, ninf, 1);
+  if ((threadIdx.x & 31) == 0 && ninf) atomicAdd(&s.counters[EC_NINF], ninf);
+}
+
+int launch_finalize_auto(const EdtState &s, int W, int H, int64_t *vr, float *dist, int64_t *d2,
+                         cudaStream_t st) {
+  size_t n = (size_t)W * H;
+  edt_select_final_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, W, H, vr, dist, d2);
+  IWPP_CUDA_TRY(cudaGetLastError());
+  return IWPP_OK;
+}
+
+}  // namespace edt
+}  // namespace iwpp

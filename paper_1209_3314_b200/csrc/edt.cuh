@@ -1,0 +1,43 @@
+// edt.cuh -- level-synchronous EDT engine interface (see edt.cu).
+#pragma once
+#include "iwpp_common.cuh"
+
+namespace iwpp {
+namespace edt {
+
+constexpr uint32_t INF32 = 0xFFFFFFFFu;
+constexpr uint32_t SEED_STAMP = 0xFFFFFFFEu;
+constexpr int kRoundThreads = 512;
+constexpr int kRoundBlocksPerSm = 2;
+
+enum { EC_ROUNDS = 0, EC_VISITS, EC_NINF, EC_LIMIT, EC_FINAL, EC_BAD, EC_N = 8 };
+
+struct EdtState {
+  uint32_t *buf[2];  // source per cell, (sy << 16 | sx), double-buffered
+  uint32_t *stamp;   // round stamp per cell (frontier dedupe)
+  uint32_t *F[2];    // frontier queues (yx codes)
+  unsigned *cnt;     // [3] frontier sizes (triple-buffered)
+  unsigned *bar;     // [2] grid barrier count / generation
+  unsigned long long *counters;
+};
+
+// Images the 32-bit (y,x) code can address (INF must stay unused).
+inline bool size_supported(int64_t W, int64_t H) {
+  return W >= 1 && H >= 1 && W <= 65536 && H <= 65536 && !(W == 65536 && H == 65536);
+}
+
+size_t state_bytes(int64_t W, int64_t H);
+EdtState carve_state(Carver &c, int64_t W, int64_t H);
+int reset_control(const EdtState &s, cudaStream_t st);
+int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, cudaStream_t st);
+int launch_import(const int64_t *vr, const int64_t *seeds, int64_t n_seeds, int W, int H,
+                  const EdtState &s, cudaStream_t st);
+int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_rounds,
+                  cudaStream_t st);
+int launch_finalize_auto(const EdtState &s, int W, int H, int64_t *vr, float *dist, int64_t *d2,
+                         cudaStream_t st);
+int launch_finalize_vr(const int64_t *vr, int W, int H, float *dist, int64_t *d2,
+                       unsigned long long *counters, cudaStream_t st);
+
+}  // namespace edt
+}  // namespace iwpp

@@ -1,0 +1,16 @@
+// recon_sweeps.cuh -- scan sweeps / seed scan / contract check (recon_sweeps.cu).
+#pragma once
+#include "iwpp_common.cuh"
+
+namespace iwpp {
+namespace recon {
+
+int sweep_rows(void *J, const void *I, int W, int H, int dtype, cudaStream_t st);
+int sweep_cols(void *J, const void *I, int W, int H, int dtype, cudaStream_t st);
+int seed_scan(const void *J, const void *I, int W, int H, int dtype, int conn, int64_t *out,
+              unsigned long long *n_out, cudaStream_t st);
+int check_le(const void *J, const void *I, size_t n, int dtype, unsigned long long *viol,
+             cudaStream_t st);
+
+}  // namespace recon
+}  // namespace iwpp

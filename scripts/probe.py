@@ -1,0 +1,45 @@
+"""Quick device timings for development (not the bench contract)."""
+import sys, os, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import oracle
+import paper_1209_3314_b200 as gw
+
+def timeit(fn, reps=10, warm=3):
+    for _ in range(warm): fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(); fn(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+    return np.median(ts), min(ts)
+
+for n, conn in [(4096, 8), (4096, 4)]:
+    J, I = oracle.gray_pair(n, 0, h=40)
+    dJ, dI = torch.from_numpy(J).cuda(), torch.from_numpy(I).cuda()
+    for sw in (0, 1):
+        st = {}
+        gw.reconstruct(dJ, dI, conn, sweeps=sw, stats=st)
+        med, mn = timeit(lambda: gw.reconstruct(dJ, dI, conn, sweeps=sw))
+        print(f"recon u8 {n}^2 c{conn} sweeps={sw}: median {med:.3f} ms min {mn:.3f} ms  {n*n/med/1e3:.0f} Mpx/s  stats={st}", flush=True)
+
+bw = oracle.gen_synthetic_mask(4096, 4096, 50, 7)
+bw16 = np.tile(bw, (4, 4))
+mk, ms = oracle.imfill_pair(bw16)
+dJ, dI = torch.from_numpy(mk).cuda(), torch.from_numpy(ms).cuda()
+for conn in (4, 8):
+    for sw in (0, 1):
+        st = {}
+        gw.reconstruct(dJ, dI, conn, sweeps=sw, stats=st)
+        med, mn = timeit(lambda: gw.reconstruct(dJ, dI, conn, sweeps=sw), reps=3, warm=1)
+        n = 16384
+        print(f"imfill 16K^2 c{conn} sweeps={sw}: median {med:.3f} ms  {n*n/med/1e3:.0f} Mpx/s stats={st}", flush=True)
+
+for name, m in [("nuclei4k", oracle.gen_nuclei_mask(4096, 4096, 30.0, 7)), ("blob4k", bw)]:
+    dm = torch.from_numpy(m).cuda()
+    img = gw.Image2D(4096, 4096, "binary", dm)
+    cfg = gw.EngineConfig()
+    gw.edt(img, gw.SE8, mode="parallel", cfg=cfg)
+    med, mn = timeit(lambda: gw.edt(img, gw.SE8), reps=5, warm=2)
+    print(f"edt {name} c8: median {med:.3f} ms  {4096*4096/med/1e3:.0f} Mpx/s rounds={cfg.stats.rounds} visits={cfg.stats.queued_total}", flush=True)

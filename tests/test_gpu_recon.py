@@ -1,0 +1,210 @@
+"""Reconstruction parity on the B200: the CUDA engine through the public
+(drop-in) API and the C ABI, against the reference's golden vectors and
+the CPU oracle.  Bit-exact everywhere (integer work, zero tolerance).
+
+Mirrors the reference's own recon tests (pkg/tests/test_recon.py,
+test_acceptance.py C1-C4, C7)."""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def gw():
+    import torch
+    import paper_1209_3314_b200 as gw
+    torch.cuda.set_device(0)
+    return gw
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _kind(a, name=""):
+    if name.startswith(("bin", "imfill")):
+        return "binary"
+    return {np.uint8: "u8", np.uint16: "u16", np.int32: "i32"}[a.dtype.type]
+
+
+def _pair(gw, J, I, conn, kind, device):
+    h, w = J.shape
+    if device:
+        t = _torch()
+        J, I = t.from_numpy(J.copy()).cuda(), t.from_numpy(I.copy()).cuda()
+    return gw.ReconInput(gw.Image2D(w, h, kind, J), gw.Image2D(w, h, kind, I),
+                         gw.StructuringElement(conn))
+
+
+def _np(a):
+    return a.cpu().numpy() if hasattr(a, "cpu") else a
+
+
+RZ = np.load(os.path.join(GOLD, "recon_golden.npz"))
+RNAMES = sorted({k.split("__")[0] for k in RZ.files if k.endswith("__out")})
+
+
+@pytest.mark.parametrize("device", [False, True])
+@pytest.mark.parametrize("name", RNAMES)
+def test_golden_vectors(gw, name, device):
+    J, I, R = RZ[name + "__marker"], RZ[name + "__mask"], RZ[name + "__out"]
+    conn = 8 if name.endswith("c8") else 4
+    inp = _pair(gw, J, I, conn, _kind(J, name), device)
+    out = gw.recon_fh(inp)
+    assert out.elem_kind == inp.marker.elem_kind
+    assert np.array_equal(_np(out.data), R)
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+@pytest.mark.parametrize("dtype", [np.uint8, np.uint16, np.int32])
+def test_random_sizes_vs_oracle(gw, conn, dtype):
+    rng = np.random.default_rng(100 + conn)
+    for shape in [(1, 1), (1, 300), (300, 1), (63, 65), (64, 64), (65, 129), (200, 333), (513, 257)]:
+        seed = int(rng.integers(0, 1 << 30))
+        h = {np.uint8: 40, np.uint16: 9000, np.int32: 1 << 27}[dtype]
+        J, I = oracle.gray_pair(shape, seed, h=h, dtype=dtype)
+        want = oracle.recon_fh(J, I, conn)
+        got = gw.reconstruct(_torch().from_numpy(J).cuda(), _torch().from_numpy(I).cuda(), conn)
+        assert np.array_equal(got.cpu().numpy(), want), (shape, seed)
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_4k_u8_vs_oracle(gw, conn):
+    """BASELINE configs[1] at full size (4096^2 u8), seed 0."""
+    J, I = oracle.gray_pair(4096, 0, h=40)
+    want = oracle.recon_fh(J, I, conn)
+    got = gw.reconstruct(_torch().from_numpy(J).cuda(), _torch().from_numpy(I).cuda(), conn)
+    assert np.array_equal(got.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_4k_int32_vs_oracle(gw, conn):
+    J, I = oracle.gray_pair(2048, 3, h=1 << 28, dtype=np.int32)
+    want = oracle.recon_fh(J, I, conn)
+    got = gw.reconstruct(_torch().from_numpy(J).cuda(), _torch().from_numpy(I).cuda(), conn)
+    assert np.array_equal(got.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_imfill_vs_oracle(gw, conn):
+    bw = oracle.gen_synthetic_mask(1024, 1024, 50, 7)
+    marker, mask = oracle.imfill_pair(bw)
+    want = oracle.recon_fh(marker, mask, conn)
+    inp = _pair(gw, marker, mask, conn, "binary", True)
+    assert np.array_equal(_np(gw.recon_fh(inp).data), want)
+
+
+def test_all_entry_points_agree_and_inputs_untouched(gw):
+    J, I = oracle.gray_pair(96, 7, h=50)
+    want = oracle.recon_fh(J, I, 8)
+    for device in (False, True):
+        inp = _pair(gw, J, I, 8, "u8", device)
+        J0, I0 = _np(inp.marker.data).copy(), _np(inp.mask.data).copy()
+        outs = [gw.recon_sr(inp), gw.recon_qb(inp), gw.recon_fh(inp),
+                gw.recon_parallel(inp, gw.EngineConfig(n_workers=4)),
+                gw.recon_tiled(inp, (32, 32), gw.PipelineConfig(n_workers=2))]
+        for o in outs:
+            assert np.array_equal(_np(o.data), want)
+        assert np.array_equal(_np(inp.marker.data), J0)
+        assert np.array_equal(_np(inp.mask.data), I0)
+
+
+def test_forced_overflow_recovers_exactly(gw):
+    """C7 analog: a tiny block queue forces drop -> rescan -> re-execute."""
+    J, I = oracle.gray_pair(256, 1007, h=40)
+    want = oracle.recon_fh(J, I, 8)
+    cfg = gw.EngineConfig(n_workers=2, queue=gw.QueueConfig(gbq_capacity=16))
+    inp = _pair(gw, J, I, 8, "u8", True)
+    got = gw.recon_parallel(inp, cfg)
+    assert np.array_equal(_np(got.data), want)
+    assert cfg.stats.overflow_count >= 2
+
+
+def test_contract_violation_raises(gw):
+    J = np.array([[5, 0]], np.uint8)
+    I = np.array([[4, 9]], np.uint8)
+    with pytest.raises(gw.ContractViolation):
+        _pair(gw, J, I, 8, "u8", True)
+    with pytest.raises(gw.ContractViolation):
+        _pair(gw, J, I, 8, "u8", False)
+
+
+def test_marker_equal_mask_identity_and_zero_marker(gw):
+    rng = np.random.default_rng(1)
+    I = rng.integers(0, 256, (77, 91)).astype(np.uint8)
+    out = gw.recon_fh(_pair(gw, I.copy(), I, 8, "u8", True))
+    assert np.array_equal(_np(out.data), I)
+    Z = np.zeros_like(I)
+    out = gw.recon_fh(_pair(gw, Z, np.maximum(I, 1), 4, "u8", True))
+    assert not _np(out.data).any()
+
+
+def test_fixed_point_equation_and_idempotence(gw):
+    J, I = oracle.gray_pair(128, 23, h=40)
+    out = _np(gw.recon_fh(_pair(gw, J, I, 8, "u8", True)).data)
+    assert np.all(J <= out) and np.all(out <= I)
+    P = np.pad(out, 1, mode="constant")
+    neigh = np.stack([P[1 + dy:129 + dy, 1 + dx:129 + dx]
+                      for dx, dy in [(a, b) for b in (-1, 0, 1) for a in (-1, 0, 1)]])
+    assert np.array_equal(out, np.minimum(neigh.max(0), I))
+    again = _np(gw.recon_fh(_pair(gw, out, I, 8, "u8", True)).data)
+    assert np.array_equal(again, out)
+
+
+def test_binary_components(gw):
+    rng = np.random.default_rng(1004)
+    for i in range(10):
+        conn = 8 if i % 2 == 0 else 4
+        mask = (rng.random((64, 64)) < 0.45).astype(np.uint8) * 255
+        marker = np.where((rng.random((64, 64)) < 0.06) & (mask == 255), 255, 0).astype(np.uint8)
+        want = oracle.recon_fh(marker, mask, conn)
+        got = gw.recon_fh(_pair(gw, marker, mask, conn, "binary", True))
+        assert np.array_equal(_np(got.data), want)
+
+
+def test_row_sweep_stage_is_exact_row_recurrence(gw):
+    """iwpp_recon_sweep_rows = K.115-139 forward then backward, exactly."""
+    from paper_1209_3314_b200 import _lib
+    t = _torch()
+    L = _lib.lib()
+    for dtype, W in [(np.uint8, 4096), (np.uint8, 1001), (np.int32, 777), (np.uint16, 64)]:
+        J, I = oracle.gray_pair((37, W), 5, h=30 if dtype == np.uint8 else 1000, dtype=dtype)
+        want = J.astype(np.int64).copy()
+        Ii = I.astype(np.int64)
+        for y in range(J.shape[0]):
+            for x in range(1, W):
+                want[y, x] = max(want[y, x], min(want[y, x - 1], Ii[y, x]))
+            for x in range(W - 2, -1, -1):
+                want[y, x] = max(want[y, x], min(want[y, x + 1], Ii[y, x]))
+        dJ, dI = t.from_numpy(J).cuda(), t.from_numpy(I).cuda()
+        code = {np.uint8: 0, np.uint16: 1, np.int32: 2}[dtype]
+        _lib.check(L.iwpp_recon_sweep_rows(_lib.ptr(dJ), _lib.ptr(dI), W, J.shape[0], code,
+                                           _lib.stream_ptr()))
+        assert np.array_equal(dJ.cpu().numpy().astype(np.int64), want), (dtype, W)
+
+
+def test_seed_scan_matches_oracle(gw):
+    J, I = oracle.gray_pair((130, 97), 9, h=60)
+    for conn in (4, 8):
+        want = oracle.recon_seed_scan(J, I, conn)
+        got = gw.recon.seed_scan(J, I, conn)
+        assert np.array_equal(got, want)
+
+
+def test_sweeps_option_same_result(gw):
+    """The full-image sweep pre-pass (any count) never changes the result."""
+    J, I = oracle.gray_pair(300, 11, h=40)
+    want = oracle.recon_fh(J, I, 8)
+    for sweeps in (1, 2):
+        got = gw.reconstruct(_torch().from_numpy(J).cuda(), _torch().from_numpy(I).cuda(), 8,
+                             sweeps=sweeps)
+        assert np.array_equal(got.cpu().numpy(), want)
