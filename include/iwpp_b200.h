@@ -87,6 +87,8 @@ typedef struct iwpp_recon_opts {
   int check_contract;/* 1: count cells with marker > mask (stats->contract_violations) */
   int queue_capacity;/* block-queue capacity (0 = default 4608); smaller values force the
                         overflow -> rescan path (QueueConfig.gbq_capacity, wqueue.py:58-60) */
+  int tile_sweeps;   /* in-tile row/column sweep passes on a tile's first visit (-1 = auto) */
+  int halo_sweep_threshold; /* re-visit: sweep when more halo pixels than this are active (-1 = auto) */
 } iwpp_recon_opts;
 
 size_t iwpp_recon_workspace_bytes(int64_t W, int64_t H, int dtype, int conn);
@@ -104,6 +106,13 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W,
                     int64_t H, int dtype, int conn, void *workspace,
                     size_t workspace_bytes, const iwpp_recon_opts *opts,
                     iwpp_stats *stats, void *stream);
+
+/* Diagnostics: copy the engine's device counters of the last iwpp_recon on
+ * this workspace (tile activations, re-runs, pushes, overflows, seeds,
+ * violations, then per-phase SM cycles: pop, load, sweep, detect, queue,
+ * store).  Returns the number of counters written.  Syncs. */
+int iwpp_recon_engine_counters(const void *workspace, int64_t W, int64_t H, uint64_t *out,
+                               int n, void *stream);
 
 /* marker <= mask check (recon.py:60): *n_violations_host = count. Syncs. */
 int iwpp_check_le(const void *J, const void *I, int64_t n, int dtype,

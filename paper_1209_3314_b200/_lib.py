@@ -29,7 +29,8 @@ IWPP_E_OVERFLOW = -6
 EXPORTS = (
     "iwpp_last_error", "iwpp_version", "iwpp_device_info",
     "iwpp_recon_workspace_bytes", "iwpp_recon", "iwpp_recon_host_workspace_bytes",
-    "iwpp_recon_host", "iwpp_check_le", "iwpp_recon_sweep_rows", "iwpp_recon_sweep_cols",
+    "iwpp_recon_host", "iwpp_recon_engine_counters", "iwpp_check_le",
+    "iwpp_recon_sweep_rows", "iwpp_recon_sweep_cols",
     "iwpp_recon_seed_scan", "iwpp_edt_workspace_bytes", "iwpp_edt", "iwpp_edt_propagate",
     "iwpp_edt_finalize", "iwpp_edt_host_workspace_bytes", "iwpp_edt_host",
 )
@@ -46,7 +47,8 @@ class Stats(ctypes.Structure):
 
 class ReconOpts(ctypes.Structure):
     _fields_ = [("sweeps", ctypes.c_int), ("max_blocks", ctypes.c_int),
-                ("check_contract", ctypes.c_int), ("queue_capacity", ctypes.c_int)]
+                ("check_contract", ctypes.c_int), ("queue_capacity", ctypes.c_int),
+                ("tile_sweeps", ctypes.c_int), ("halo_sweep_threshold", ctypes.c_int)]
 
 
 _lib = None
@@ -75,6 +77,7 @@ def load_library(path: str = LIB_PATH):
             "iwpp_recon": ([P, P, I64, I64, I, I, P, SZ, OP, SP, P], I),
             "iwpp_recon_host_workspace_bytes": ([I64, I64, I, I], SZ),
             "iwpp_recon_host": ([P, P, P, I64, I64, I, I, P, SZ, OP, SP, P], I),
+            "iwpp_recon_engine_counters": ([P, I64, I64, ctypes.POINTER(ctypes.c_uint64), I, P], I),
             "iwpp_check_le": ([P, P, I64, I, P, ctypes.POINTER(I64), P], I),
             "iwpp_recon_sweep_rows": ([P, P, I64, I64, I, P], I),
             "iwpp_recon_sweep_cols": ([P, P, I64, I64, I, P], I),

@@ -135,10 +135,14 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
     if ((rc = recon::sweep_rows(J, I, (int)W, (int)H, dtype, st))) return rc;
     if ((rc = recon::sweep_cols(J, I, (int)W, (int)H, dtype, st))) return rc;
   }
-  int max_blocks = opts ? opts->max_blocks : 0;
-  int qcap = opts ? opts->queue_capacity : 0;
-  if ((rc = recon::run_tile_engine(J, I, (int)W, (int)H, dtype, conn, w.q, w.counters, max_blocks,
-                                   qcap, st)))
+  recon::EngineOpts eo;
+  if (opts) {
+    eo.max_blocks = opts->max_blocks;
+    eo.qcap = opts->queue_capacity;
+    if (opts->tile_sweeps >= 0) eo.sweeps = opts->tile_sweeps;
+    eo.halo_thresh = opts->halo_sweep_threshold;
+  }
+  if ((rc = recon::run_tile_engine(J, I, (int)W, (int)H, dtype, conn, w.q, w.counters, eo, st)))
     return rc;
   if (opts && opts->check_contract) {
     if ((rc = recon::check_le(J, I, (size_t)W * H, dtype, &w.counters[recon::CNT_VIOL], st)))
@@ -179,7 +183,7 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   unsigned long long viol = 0;
   IWPP_CUDA_TRY(cudaMemcpyAsync(&viol, &w.counters[recon::CNT_VIOL], sizeof viol,
                                 cudaMemcpyDeviceToHost, st));
-  iwpp_recon_opts o = opts ? *opts : iwpp_recon_opts{-1, 0, 0, 0};
+  iwpp_recon_opts o = opts ? *opts : iwpp_recon_opts{-1, 0, 0, 0, -1, -1};
   o.check_contract = 0;
   if ((rc = iwpp_recon(dJ, dI, W, H, dtype, conn, rest, rest_bytes, &o, nullptr, stream))) return rc;
   IWPP_CUDA_TRY(cudaMemcpyAsync(out, dJ, nb, cudaMemcpyDeviceToHost, st));
@@ -187,6 +191,17 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   if (viol) return set_error(IWPP_E_CONTRACT, "marker exceeds mask somewhere (%llu cells)", viol);
   if (stats) return fill_recon_stats(w, stats, st);
   return IWPP_OK;
+}
+
+int iwpp_recon_engine_counters(const void *workspace, int64_t W, int64_t H, uint64_t *out,
+                               int n, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Carver c((void *)workspace);
+  ReconWs w = carve_recon(c, W, H);
+  if (n > recon::CNT_N) n = recon::CNT_N;
+  IWPP_CUDA_TRY(cudaMemcpyAsync(out, w.counters, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, st));
+  IWPP_CUDA_TRY(cudaStreamSynchronize(st));
+  return n;
 }
 
 int iwpp_check_le(const void *J, const void *I, int64_t n, int dtype, void *workspace,

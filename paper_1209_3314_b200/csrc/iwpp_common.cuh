@@ -97,6 +97,30 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
   return v;
 }
 
+// Predicated shared-memory atomics (no branch around the atomic, so a run of
+// them issues back to back).  A predicated-off call returns INT_MAX (max) /
+// all-ones (or), which callers treat as "no effect".
+__device__ __forceinline__ int smem_atomic_max_if(int *p, int v, unsigned pred) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  int old = 0x7fffffff;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q atom.shared.max.s32 %0, [%1], %2;\n\t}"
+      : "+r"(old)
+      : "r"(a), "r"(v), "r"(pred)
+      : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned smem_atomic_or_if(unsigned *p, unsigned v, unsigned pred) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(p);
+  unsigned old = 0xffffffffu;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q atom.shared.or.b32 %0, [%1], %2;\n\t}"
+      : "+r"(old)
+      : "r"(a), "r"(v), "r"(pred)
+      : "memory");
+  return old;
+}
+
 // Element traits: the engines keep values as int32 in shared memory so the
 // hardware atomicMax covers every element kind (u8/u16 widen losslessly).
 template <typename T>
@@ -104,14 +128,17 @@ struct Elem;
 template <>
 struct Elem<uint8_t> {
   static constexpr int code = IWPP_U8;
+  static constexpr uint8_t lo = 0;  // smallest value (the "outside" sentinel mask)
 };
 template <>
 struct Elem<uint16_t> {
   static constexpr int code = IWPP_U16;
+  static constexpr uint16_t lo = 0;
 };
 template <>
 struct Elem<int32_t> {
   static constexpr int code = IWPP_I32;
+  static constexpr int32_t lo = INT32_MIN;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

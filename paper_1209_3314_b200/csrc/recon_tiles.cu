@@ -1,26 +1,42 @@
-// recon_tiles.cu -- persistent tile engine for morphological reconstruction.
+// recon_tiles.cu -- persistent warp-per-tile engine for morphological
+// reconstruction by dilation.
 //
-// Replaces the reference's wavefront phase (recon_wavefront K.220-270,
-// run_parallel/round shares engine.py:251-364, K.273-303) and its seed
-// detection (recon_seed_scan K.193-217) with one persistent sm_100a kernel.
+// Replaces the reference's scan + wavefront phases (recon_raster_pass /
+// recon_antiraster_pass K.38-112, recon_rows/cols K.115-190, recon_seed_scan
+// K.193-217, recon_wavefront K.220-270, the round engine engine.py:251-364)
+// with one persistent sm_100a kernel.  Every warp is an independent worker
+// that owns one 32x32 tile (+ 1-pixel halo) at a time in its own slice of
+// shared memory -- no CTA barriers anywhere, ~20 tiles in flight per SM.
+// Per tile activation:
 //
-// Queue hierarchy (the paper's TQ/BQ/GBQ, re-designed):
-//   TQ  : per-thread register bitmask of raised neighbours (<= 8 bits)
-//   BQ  : per-CTA shared-memory pixel queue (two level buffers); pushes are
-//         warp-aggregated (shfl scan + one shared atomicAdd per warp)
-//   GBQ : global MPMC ring of *tile* ids.  A tile enters it when one of its
-//         halo pixels is raised by a neighbouring tile (border exchange,
-//         the BP step of tiles.py:342-359 done asynchronously).
-// Persistent blocks pop tiles, load tile+halo into shared memory, detect
-// the tile's active pixels (full-neighbourhood predicate, K.193-217), run
-// the BQ propagation to the tile's local fixed point with shared-memory
-// atomicMax (the update rule J(q) <- min(J(p), I(q)) under the condition
-// J(q) < J(p) and J(q) != I(q), recon.py:92-101), write the tile back and
-// activate neighbour tiles whose pixels the changed border can still raise.
-// BQ overflow drops work, raises a flag and re-seeds the tile by a full
-// rescan (the drop/rescan/re-execute contract of engine.py:274-303).
-// Termination: a global count of tiles that are queued or running; the
-// engine is done when the ring is empty and that count is 0.
+//   1. load tile + halo (16-byte vector loads of the rows, L2-coherent)
+//   2. sweeps (first visit, or a wide front entering): lane = line, each
+//      lane walks its row W->E / E->W, then its column N->S / S->N with
+//      v <- clamp(v, J, I) -- the paper's raster / anti-raster scan phase in
+//      its axis-decomposed form (Alg. 5), halo cells as fixed sources
+//   3. initial-wavefront detection: every cell (interior or halo) that can
+//      still raise an interior neighbour (J(q) < J(p), J(q) < I(q)),
+//      computed as a 3x3 (8-conn) / cross (4-conn) min filter over the
+//      "raisable" values, lane = column, sliding row window in registers;
+//      ballot-compacted into the warp's pixel queue
+//   4. propagation to the tile's fixed point: the warp drains its pixel
+//      queue 32 items per step with shared atomicMax merges
+//      (J(q) <- min(J(p), I(q)) iff J(q) < J(p) and J(q) != I(q),
+//      recon.py:92-101); pushes are placed by bit-plane ballots (no
+//      atomics), an in-queue bitmap dedupes them
+//   5. write the interior back and activate the neighbour tiles whose
+//      cells the changed border can still raise.
+//
+// Queue hierarchy (the paper's TQ/BQ/GBQ):
+//   TQ  : per-lane register bitmask of raised neighbours (<= 8 bits)
+//   BQ  : per-warp shared-memory pixel ring, ballot/popc placement
+//   GBQ : global MPMC ring of tile ids (ticket pop, per-tile state bits);
+//         a tile whose halo a neighbour raised re-enters it -- the BP border
+//         exchange of tiles.py:342-359, asynchronous, no wave barriers.
+// BQ overflow (only reachable with a user-forced small capacity,
+// QueueConfig.gbq_capacity) drops work and re-seeds the tile by a full
+// rescan -- the drop / rescan / re-execute contract of engine.py:274-303.
+// Termination: a global count of queued+running tiles reaches 0.
 //
 // The fixed point is unique (engine.py:9-18), so this asynchronous schedule
 // is bit-exact with recon_fh.
@@ -33,403 +49,717 @@
 namespace iwpp {
 namespace recon {
 
-// tile states
-constexpr unsigned ST_IDLE = 0, ST_QUEUED = 1, ST_RUNNING = 2, ST_DIRTY = 3;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr unsigned ST_Q = 1, ST_R = 2, ST_V = 4;
+constexpr int RING = 4 * TS + 4;  // halo cells
 
-struct SmemLayout {
-  int *J;          // PN  (int32 working values; INT_MIN = outside image)
-  int *I;          // PN
-  uint16_t *q[2];  // QCAP each
-  int *ring0;      // 4*TW border-ring values as written back last time
+// One warp's shared memory.  J is int32 so the hardware atomicMax covers
+// every element kind; I keeps the element type.  Cells outside the image
+// hold J = INT_MIN, I = min(T): never a source, and a clamp through them can
+// never raise an in-image cell; interior cells past the image edge are also
+// excluded from detection and propagation by the tile's in-image extent.
+template <typename T>
+struct alignas(16) WarpSmem {
+  int J[PNS];
+  alignas(16) T I[PNS];
+  alignas(16) uint16_t ring[RQ];  // pixel queue (absolute positions mod RQ)
+  alignas(16) unsigned bits[BITW];
+  int ring0[4 * TS];  // border ring as last published
 };
-
-__host__ __device__ constexpr size_t smem_bytes() {
-  return sizeof(int) * PN * 2 + sizeof(uint16_t) * QCAP * 2 + sizeof(int) * 4 * TW + 64;
-}
-
-__device__ __forceinline__ int ring_index(int lx, int ly) {
-  // interior border ring position of an interior cell on the tile edge,
-  // -1 when the cell is not on the ring
-  if (ly == 1) return lx - 1;
-  if (ly == TH) return TW + lx - 1;
-  if (lx == 1) return 2 * TW + ly - 1;
-  if (lx == TW) return 3 * TW + ly - 1;
-  return -1;
-}
-
-__device__ __forceinline__ bool interior(int lx, int ly) {
-  return lx >= 1 && lx <= TW && ly >= 1 && ly <= TH;
-}
 
 struct EngineArgs {
   void *J;
   const void *I;
   int W, H;
   int ntx, nty;
-  unsigned ntiles;
-  unsigned qlimit;  // block-queue capacity actually used (<= QCAP)
+  unsigned qlimit;       // pixel-queue capacity actually used (<= RQ)
+  unsigned halo_thresh;  // re-activation halo front above which to sweep first
+  int sweeps;            // sweep passes on a tile's first visit
+  int vec;               // rows are 16-byte aligned
   TileQueue q;
 };
 
-// --- global tile queue ---------------------------------------------------
+struct Lim {  // in-image interior extent of the current tile: 1..x, 1..y
+  int x, y;
+};
+
+__device__ __forceinline__ int sidx(int lx, int ly) { return ly * PS + lx; }
+__device__ __forceinline__ bool interior(Lim l, int lx, int ly) {
+  return lx >= 1 && lx <= l.x && ly >= 1 && ly <= l.y;
+}
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(hi, max(lo, v)); }
+
+// halo cell h in [0, RING) -> (lx, ly): top row, bottom row, left, right
+__device__ __forceinline__ void halo_cell(int h, int &lx, int &ly) {
+  if (h < PW) {
+    lx = h;
+    ly = 0;
+  } else if (h < 2 * PW) {
+    lx = h - PW;
+    ly = TS + 1;
+  } else if (h < 2 * PW + TS) {
+    lx = 0;
+    ly = h - 2 * PW + 1;
+  } else {
+    lx = TS + 1;
+    ly = h - 2 * PW - TS + 1;
+  }
+}
+
+// border-ring slot of an interior edge cell (corners map to the rows)
+__device__ __forceinline__ int ring_index(int lx, int ly) {
+  if (ly == 1) return lx - 1;
+  if (ly == TS) return TS + lx - 1;
+  if (lx == 1) return 2 * TS + ly - 1;
+  return 3 * TS + ly - 1;  // lx == TS
+}
+__device__ __forceinline__ void ring_cell(int r, int &lx, int &ly) {
+  int side = r / TS, k = r - side * TS;
+  lx = side < 2 ? k + 1 : (side == 2 ? 1 : TS);
+  ly = side < 2 ? (side == 0 ? 1 : TS) : k + 1;
+}
+
+// --- global tile queue (GBQ) -------------------------------------------------
 
 __device__ __forceinline__ void ring_push(const TileQueue &q, unsigned t) {
   unsigned pos = atomicAdd(q.tail, 1u);
   st_release64(&q.ring[pos & q.mask], ((unsigned long long)pos << 32) | t);
 }
 
-// returns tile id or -1 when the ring is momentarily empty
+// Ticket pop: one fetch-and-add per pop (no CAS retry storms on the head),
+// then wait until the slot carries the ticket's tag.  Returns -1 once the
+// engine has terminated (no tile queued or running: nothing can be pushed
+// any more, and a filled slot would imply a queued tile).
 __device__ __forceinline__ int ring_pop(const TileQueue &q) {
-  for (;;) {
-    unsigned h = ld_relaxed(q.head);
-    unsigned t = ld_relaxed(q.tail);
-    if ((int)(t - h) <= 0) return -1;
-    if (atomicCAS(q.head, h, h + 1) != h) continue;
-    unsigned long long *slot = &q.ring[h & q.mask];
-    unsigned long long v;
-    while (((v = ld_acquire64(slot)) >> 32) != h) __nanosleep(20);
-    return (int)(v & 0xffffffffu);
+  unsigned ticket = atomicAdd(q.head, 1u);
+  unsigned long long *slot = &q.ring[ticket & q.mask];
+  for (unsigned ns = 32;; ns = ns < 256 ? ns * 2 : 256) {
+    unsigned long long v = ld_acquire64(slot);
+    if ((unsigned)(v >> 32) == ticket) return (int)(v & 0xffffffffu);
+    if (ld_acquire(q.pending) == 0) return -1;
+    __nanosleep(ns);
   }
 }
 
+// Tile state bits: Q = queued, or re-run requested while running; R =
+// running; V = never processed (set only by the initial fill).
+//   activate : old = atomicOr(Q); old == 0 (idle) -> we own the push
+//   pop      : old = atomicExch(R) + fence (acquire: sees every border write
+//              made before a request that found Q already set)
+//   finish   : CAS(R -> 0); failure means Q was set meanwhile -> re-run
 __device__ __forceinline__ void activate(const TileQueue &q, unsigned t) {
-  unsigned s = ld_relaxed(&q.state[t]);
-  for (;;) {
-    if (s == ST_QUEUED || s == ST_DIRTY) return;
-    if (s == ST_IDLE) {
-      unsigned old = atomicCAS(&q.state[t], ST_IDLE, ST_QUEUED);
-      if (old == ST_IDLE) {
-        atomicAdd(q.pending, 1u);
-        ring_push(q, t);
-        return;
-      }
-      s = old;
-    } else {  // RUNNING
-      unsigned old = atomicCAS(&q.state[t], ST_RUNNING, ST_DIRTY);
-      if (old == ST_RUNNING) return;
-      s = old;
-    }
+  unsigned old = atomicOr(&q.state[t], ST_Q);
+  if (old == 0) {
+    atomicAdd(q.pending, 1u);
+    ring_push(q, t);
   }
 }
 
-// --- tile processing -----------------------------------------------------
+// --- loads / stores (warp) -----------------------------------------------------
 
 template <typename T>
-__device__ __forceinline__ void load_cell(const EngineArgs &a, SmemLayout &s, int i, int x0,
-                                          int y0) {
-  int ly = i / PW, lx = i - ly * PW;
+__device__ __forceinline__ void load_scalar(const EngineArgs &a, WarpSmem<T> &s, int lx, int ly,
+                                            int x0, int y0) {
   int gx = x0 + lx - 1, gy = y0 + ly - 1;
+  int i = sidx(lx, ly);
   if (gx >= 0 && gx < a.W && gy >= 0 && gy < a.H) {
     size_t g = (size_t)gy * a.W + gx;
     s.J[i] = (int)ld_cg((const T *)a.J + g);
-    s.I[i] = (int)__ldg((const T *)a.I + g);
+    s.I[i] = __ldg((const T *)a.I + g);
   } else {
     s.J[i] = INT_MIN;
-    s.I[i] = INT_MIN;
+    s.I[i] = Elem<T>::lo;
   }
 }
 
-// Detect active pixels (p can raise an interior neighbour) into q[0]
-// (K.193-217 restricted to the tile, halo cells act as sources only).
-// Returns the number queued (clipped to qlimit; *s_over set if clipped).
-template <int CONN>
-__device__ unsigned detect_seeds(SmemLayout &s, unsigned *s_n, unsigned *s_over, unsigned qlimit) {
-  const unsigned FULL = 0xffffffffu;
-  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int base = warp * 32; base < PN; base += blockDim.x) {
-    int p = base + lane;
+template <typename T>
+__device__ void load_halo(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, int lane) {
+  for (int h = lane; h < RING; h += 32) {
+    int lx, ly;
+    halo_cell(h, lx, ly);
+    load_scalar<T>(a, s, lx, ly, x0, y0);
+  }
+}
+
+// lane = row; full-width aligned rows go by 16-byte vectors
+template <typename T>
+__device__ void load_tile(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, int lane) {
+  constexpr int E = 16 / sizeof(T), CPR = TS / E;
+  const int ly = lane + 1, gy = y0 + lane;
+  if (a.vec && x0 + TS <= a.W && gy < a.H) {
+    const T *pj = (const T *)a.J + (size_t)gy * a.W + x0;
+    const T *pi = (const T *)a.I + (size_t)gy * a.W + x0;
+#pragma unroll
+    for (int c = 0; c < CPR; c++) {
+      uint4 vj = __ldcg(reinterpret_cast<const uint4 *>(pj) + c);
+      uint4 vi = __ldg(reinterpret_cast<const uint4 *>(pi) + c);
+      const T *ej = reinterpret_cast<const T *>(&vj);
+      const T *ei = reinterpret_cast<const T *>(&vi);
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        s.J[sidx(1 + c * E + e, ly)] = (int)ej[e];
+        s.I[sidx(1 + c * E + e, ly)] = ei[e];
+      }
+    }
+  } else {
+    for (int lx = 1; lx <= TS; lx++) load_scalar<T>(a, s, lx, ly, x0, y0);
+  }
+  load_halo<T>(a, s, x0, y0, lane);
+}
+
+template <typename T>
+__device__ void store_tile(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, Lim lim,
+                           int lane) {
+  constexpr int E = 16 / sizeof(T), CPR = TS / E;
+  const int ly = lane + 1, gy = y0 + lane;
+  if (ly > lim.y) return;
+  T *pj = (T *)a.J + (size_t)gy * a.W + x0;
+  if (a.vec && x0 + TS <= a.W) {
+#pragma unroll
+    for (int c = 0; c < CPR; c++) {
+      uint4 v;
+      T *ev = reinterpret_cast<T *>(&v);
+#pragma unroll
+      for (int e = 0; e < E; e++) ev[e] = (T)s.J[sidx(1 + c * E + e, ly)];
+      reinterpret_cast<uint4 *>(pj)[c] = v;
+    }
+  } else {
+    for (int lx = 1; lx <= lim.x; lx++) pj[lx - 1] = (T)s.J[sidx(lx, ly)];
+  }
+}
+
+// --- sweeps (the paper's scan phase, Alg. 5 axis decomposition) ---------------
+//
+// lane = line; the lane walks its 32 cells with v <- clamp(v, J, I) from the
+// cell before the line: rows W->E then E->W (K.115-139), then columns N->S
+// then S->N (K.142-190, vertical neighbour).  Straight-line code: compile-
+// time stride, a chunk's loads issued together, unconditional stores.
+// Partial tiles walk all 32 cells: cells past the image edge hold the
+// sentinel (J = INT_MIN, I = min(T)), and clamp(v, INT_MIN, min(T)) <= min(T)
+// can never raise an in-image cell.
+template <int STEP, typename T>
+__device__ __forceinline__ bool walk_line(WarpSmem<T> &s, int first, int carry_idx) {
+  constexpr int C = 8;
+  int v = s.J[carry_idx];
+  bool chg = false;
+#pragma unroll
+  for (int k0 = 0; k0 < TS; k0 += C) {
+    int j[C], m[C];
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+      j[c] = s.J[first + (k0 + c) * STEP];
+      m[c] = (int)s.I[first + (k0 + c) * STEP];
+    }
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+      int nv = clampi(v, j[c], m[c]);
+      chg |= nv != j[c];
+      s.J[first + (k0 + c) * STEP] = nv;
+      v = nv;
+    }
+  }
+  return chg;
+}
+
+template <typename T>
+__device__ bool sweep_pass(WarpSmem<T> &s, int lane) {
+  const int k = lane + 1;
+  bool chg = walk_line<1>(s, sidx(1, k), sidx(0, k));
+  chg |= walk_line<-1>(s, sidx(TS, k), sidx(TS + 1, k));
+  __syncwarp();
+  chg |= walk_line<PS>(s, sidx(k, 1), sidx(k, 0));
+  chg |= walk_line<-PS>(s, sidx(k, TS), sidx(k, TS + 1));
+  __syncwarp();
+  return __any_sync(FULL, chg);
+}
+
+// --- detection -----------------------------------------------------------------
+
+// "raisable" value: J if the cell is an in-image interior cell below its
+// mask, else +inf.  p is active iff J(p) > min over N(p) of m.
+template <typename T>
+__device__ __forceinline__ int mval(const WarpSmem<T> &s, Lim lim, int lx, int ly) {
+  if (!interior(lim, lx, ly)) return INT_MAX;
+  int i = sidx(lx, ly);
+  int j = s.J[i];
+  return j < (int)s.I[i] ? j : INT_MAX;
+}
+
+template <int CONN, typename T>
+__device__ __forceinline__ bool can_raise(const WarpSmem<T> &s, Lim lim, int lx, int ly) {
+  int v = s.J[sidx(lx, ly)];
+  bool want = false;
+#pragma unroll
+  for (int k = 0; k < Nbr<CONN>::N; k++) {
+    int qx = lx + Nbr<CONN>::dx(k), qy = ly + Nbr<CONN>::dy(k);
+    if (interior(lim, qx, qy)) {
+      int qq = sidx(qx, qy);
+      int vq = s.J[qq];
+      if (vq < v && vq < (int)s.I[qq]) want = true;
+    }
+  }
+  return want;
+}
+
+// queue a ballot of cells (one per lane) at the warp tail; returns the new tail
+__device__ __forceinline__ unsigned push_ballot(uint16_t *ring, unsigned t, bool want, int p,
+                                                unsigned qlimit, unsigned h, int lane) {
+  unsigned k = __ballot_sync(FULL, want);
+  unsigned pos = t + __popc(k & lanemask_lt());
+  if (want && pos - h < qlimit) ring[pos & (RQ - 1)] = (uint16_t)p;
+  (void)lane;
+  return t + __popc(k);
+}
+
+// Full detection (K.193-217 restricted to the tile; halo cells are sources
+// only).  lane = column x; rows -1..34 stream through a 3-row window of
+// m (own column) and lr = min(m left, m right) (shuffles; the halo columns'
+// m is +inf).  Row 0 / 33 centres are the top / bottom halo cells; lanes 0
+// and 31 additionally test the left / right halo columns from their own m.
+// Writes the queue at [0, n) and returns n (may exceed qlimit: truncated).
+template <int CONN, typename T>
+__device__ unsigned detect_full(WarpSmem<T> &s, Lim lim, unsigned qlimit, int lane) {
+  const int x = lane + 1;
+  auto row = [&](int y, int &m, int &lr, int &j) {
+    if (y < 0 || y > TS + 1) {
+      m = INT_MAX;
+      lr = INT_MAX;
+      j = INT_MIN;
+      return;
+    }
+    int i = sidx(x, y);
+    j = s.J[i];
+    m = (interior(lim, x, y) && j < (int)s.I[i]) ? j : INT_MAX;
+    int l = __shfl_up_sync(FULL, m, 1), r = __shfl_down_sync(FULL, m, 1);
+    if (lane == 0) l = INT_MAX;   // column 0 is halo
+    if (lane == 31) r = INT_MAX;  // column 33 is halo
+    lr = min(l, r);
+  };
+  unsigned t = 0;
+  int m_p, lr_p, jd, m_c, lr_c, j_c;
+  row(-1, m_p, lr_p, jd);
+  row(0, m_c, lr_c, j_c);
+  for (int y = 0; y <= TS + 1; y++) {
+    int m_n, lr_n, j_n;
+    row(y + 1, m_n, lr_n, j_n);
+    int lo = CONN == 8 ? min(min(min(m_p, lr_p), min(m_c, lr_c)), min(m_n, lr_n))
+                       : min(min(lr_c, m_p), m_n);
+    // halo rows (y = 0, TS+1) are sources even though not interior
+    bool ok = (y == 0 || y == TS + 1) ? true : interior(lim, x, y);
+    t = push_ballot(s.ring, t, ok && j_c > lo, sidx(x, y), qlimit, 0, lane);
+    // left / right halo columns, rows 0..TS+1 (corners included)
+    bool side = false;
+    int ps = 0;
+    if (lane == 0 || lane == 31) {
+      int hx = lane == 0 ? 0 : TS + 1;
+      int lo2 = CONN == 8 ? min(min(m_p, m_c), m_n) : m_c;
+      side = s.J[sidx(hx, y)] > lo2;
+      ps = sidx(hx, y);
+    }
+    t = push_ballot(s.ring, t, side, ps, qlimit, 0, lane);
+    m_p = m_c;
+    lr_p = lr_c;
+    m_c = m_n;
+    lr_c = lr_n;
+    j_c = j_n;
+  }
+  return t;
+}
+
+// One sweep pass whose last walk (columns S->N, lane = column) also does the
+// full detection: after the walk finalises row y, rows y..y+2 are final, so
+// the centre row y+1 is evaluated one step behind the walk (same 3-row
+// window as detect_full, no second pass over the tile).  Returns whether
+// the sweep changed anything; *n = cells queued (may exceed qlimit).
+template <int CONN, typename T>
+__device__ bool sweep_detect(WarpSmem<T> &s, Lim lim, unsigned qlimit, int lane, unsigned &n) {
+  const int k = lane + 1, x = k;
+  bool chg = walk_line<1>(s, sidx(1, k), sidx(0, k));
+  chg |= walk_line<-1>(s, sidx(TS, k), sidx(TS + 1, k));
+  __syncwarp();
+  chg |= walk_line<PS>(s, sidx(k, 1), sidx(k, 0));
+  __syncwarp();
+  // S -> N with the detection window: rows (y, y+1, y+2) = (n_, c_, p_)
+  unsigned t = 0;
+  int v = s.J[sidx(x, TS + 1)];
+  int m_c = INT_MAX, lr_c = INT_MAX, j_c = v;              // row TS+1 (bottom halo)
+  int m_p = INT_MAX, lr_p = INT_MAX;                       // row TS+2 (beyond)
+  auto centre = [&](int c, int m_n, int lr_n) {
+    // evaluate centre row c with rows c-1 (n), c (c), c+1 (p)
+    int lo = CONN == 8 ? min(min(min(m_p, lr_p), min(m_c, lr_c)), min(m_n, lr_n))
+                       : min(min(lr_c, m_p), m_n);
+    bool ok = (c == 0 || c == TS + 1) ? true : interior(lim, x, c);
+    t = push_ballot(s.ring, t, ok && j_c > lo, sidx(x, c), qlimit, 0, lane);
+    bool side = false;
+    int ps = 0;
+    if (lane == 0 || lane == 31) {
+      int hx = lane == 0 ? 0 : TS + 1;
+      int lo2 = CONN == 8 ? min(min(m_p, m_c), m_n) : m_c;
+      side = s.J[sidx(hx, c)] > lo2;
+      ps = sidx(hx, c);
+    }
+    t = push_ballot(s.ring, t, side, ps, qlimit, 0, lane);
+  };
+  auto lr_of = [&](int m) {
+    int l = __shfl_up_sync(FULL, m, 1), r = __shfl_down_sync(FULL, m, 1);
+    if (lane == 0) l = INT_MAX;
+    if (lane == 31) r = INT_MAX;
+    return min(l, r);
+  };
+  constexpr int C = 8;
+#pragma unroll
+  for (int k0 = 0; k0 < TS; k0 += C) {
+    int j[C], mm[C];
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+      j[c] = s.J[sidx(x, TS - k0 - c)];
+      mm[c] = (int)s.I[sidx(x, TS - k0 - c)];
+    }
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+      const int y = TS - k0 - c;
+      int nv = clampi(v, j[c], mm[c]);
+      chg |= nv != j[c];
+      s.J[sidx(x, y)] = nv;
+      v = nv;
+      int m_n = (interior(lim, x, y) && nv < mm[c]) ? nv : INT_MAX;
+      int lr_n = lr_of(m_n);
+      centre(y + 1, m_n, lr_n);  // rows y..y+2 are final now
+      m_p = m_c;
+      lr_p = lr_c;
+      m_c = m_n;
+      lr_c = lr_n;
+      j_c = nv;
+    }
+  }
+  // centre row 1: rows 0 (top halo, m = +inf), 1, 2
+  centre(1, INT_MAX, INT_MAX);
+  // centre row 0 (top halo): rows -1 (beyond), 0, 1
+  m_p = m_c;
+  lr_p = lr_c;
+  m_c = INT_MAX;
+  lr_c = INT_MAX;
+  j_c = s.J[sidx(x, 0)];
+  centre(0, INT_MAX, INT_MAX);
+  n = t;
+  return __any_sync(FULL, chg);
+}
+
+// Halo-only detection for a re-visit: the interior is already stable with
+// respect to itself, so only halo cells can be new sources.
+template <int CONN, typename T>
+__device__ unsigned detect_halo(WarpSmem<T> &s, Lim lim, unsigned qlimit, int lane) {
+  unsigned t = 0;
+  for (int h0 = 0; h0 < RING; h0 += 32) {
+    int h = h0 + lane;
     bool want = false;
-    if (p < PN) {
-      int v = s.J[p];
-      int py = p / PW, px = p - py * PW;
+    int p = 0;
+    if (h < RING) {
+      int lx, ly;
+      halo_cell(h, lx, ly);
+      p = sidx(lx, ly);
+      want = can_raise<CONN>(s, lim, lx, ly);
+    }
+    t = push_ballot(s.ring, t, want, p, qlimit, 0, lane);
+  }
+  return t;
+}
+
+// --- propagation to the tile's fixed point ---------------------------------------
+//
+// The warp drains its ring 32 items per step.  Items are popped (their
+// in-queue bit cleared), __syncwarp, then each lane offers its cell's
+// value to its in-tile neighbours with shared atomicMax; a neighbour it
+// raised and whose bit was clear is pushed (bit set).  __syncwarp orders
+// one step's merges before the next step's reads.
+template <int CONN, typename T>
+__device__ void tile_fixpoint(WarpSmem<T> &s, Lim lim, unsigned qlimit, bool full, int sweeps,
+                              unsigned halo_thresh, int lane, bool &changed,
+                              unsigned long long &pushes, unsigned long long &overflows,
+                              unsigned long long &seeds, unsigned long long *ph) {
+  const bool l0 = lane == 0;
+  unsigned h = 0, t = 0;
+  bool rescan = true, pending = false, swept = false;
+  for (;;) {
+    if (rescan) {
+      long long d0 = l0 ? clock64() : 0;
+      for (int w = lane; w < BITW; w += 32) s.bits[w] = 0;
+      unsigned n;
+      if (full && !swept && sweeps > 0) {
+        // sweeps, the last one with the detection fused into its final walk
+        swept = true;
+        for (int sp = 1; sp < sweeps; sp++) changed |= sweep_pass(s, lane);
+        changed |= sweep_detect<CONN>(s, lim, qlimit, lane, n);
+        __syncwarp();
+        if (l0) ph[2] += clock64() - d0;
+      } else {
+        swept = swept || full;
+        __syncwarp();
+        n = full ? detect_full<CONN>(s, lim, qlimit, lane) : detect_halo<CONN>(s, lim, qlimit, lane);
+        __syncwarp();
+        if (l0) ph[3] += clock64() - d0;
+      }
+      if (!full && sweeps > 0 && n > halo_thresh) {
+        full = true;  // a wide front entered: sweep it in, then detect everywhere
+        continue;
+      }
+      full = true;  // later rescans (overflow recovery) are always full
+      rescan = false;
+      pending = n > qlimit;
+      if (pending) n = qlimit;
+      if (l0) {
+        seeds += n;
+        if (pending) overflows++;
+      }
+      // mark the queued seeds
+      for (unsigned i = lane; i < n; i += 32) {
+        int p = s.ring[i];
+        atomicOr(&s.bits[p >> 5], 1u << (p & 31));
+      }
+      __syncwarp();
+      h = 0;
+      t = n;
+      if (n == 0) break;
+    }
+    // one step: up to 32 items
+    unsigned b = min(t - h, 32u);
+    int p = 0, px = 0, py = 0;
+    if ((unsigned)lane < b) {
+      p = s.ring[(h + lane) & (RQ - 1)];
+      atomicAnd(&s.bits[p >> 5], ~(1u << (p & 31)));
+    }
+    __syncwarp();
+    // Branch-free neighbour offers: all loads, then all (predicated)
+    // atomics back to back, so their latencies overlap.
+    unsigned mask = 0;
+    bool raised = false;
+    {
+      const bool act = (unsigned)lane < b;
+      py = p / PS;
+      px = p - py * PS;
+      const int v = act ? s.J[p] : INT_MIN;
+      int nv[Nbr<CONN>::N];
+      unsigned cand = 0;
 #pragma unroll
       for (int k = 0; k < Nbr<CONN>::N; k++) {
         int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
-        if (interior(qx, qy)) {
-          int qq = qy * PW + qx;
-          int vq = s.J[qq];
-          if (vq < v && vq < s.I[qq]) want = true;
-        }
+        bool in = act && interior(lim, qx, qy);
+        int qq = in ? sidx(qx, qy) : 0;
+        int vq = s.J[qq];
+        int iq = (int)s.I[qq];
+        nv[k] = v < iq ? v : iq;
+        if (in && vq < v && vq < iq) cand |= 1u << k;
+      }
+      unsigned up = 0;
+#pragma unroll
+      for (int k = 0; k < Nbr<CONN>::N; k++) {
+        int qq = sidx(px + Nbr<CONN>::dx(k), py + Nbr<CONN>::dy(k));
+        int old = smem_atomic_max_if(&s.J[qq], nv[k], (cand >> k) & 1u);
+        if (old < nv[k]) up |= 1u << k;  // predicated-off lanes return INT_MAX
+      }
+      raised = up != 0;
+#pragma unroll
+      for (int k = 0; k < Nbr<CONN>::N; k++) {
+        int qq = sidx(px + Nbr<CONN>::dx(k), py + Nbr<CONN>::dy(k));
+        unsigned bb = 1u << (qq & 31);
+        unsigned old = smem_atomic_or_if(&s.bits[qq >> 5], bb, (up >> k) & 1u);
+        if (((up >> k) & 1u) && !(old & bb)) mask |= 1u << k;  // not yet queued
       }
     }
-    unsigned pos = warp_reserve(s_n, want ? 1u : 0u, FULL);
-    if (want) {
-      if (pos < qlimit)
-        s.q[0][pos] = (uint16_t)p;
-      else
-        *s_over = 1;
+    changed |= __any_sync(FULL, raised);
+    // placement: exclusive prefix of the per-lane counts from bit-plane ballots
+    unsigned c = __popc(mask);
+    unsigned b0 = __ballot_sync(FULL, c & 1u), b1 = __ballot_sync(FULL, c & 2u);
+    unsigned b2 = __ballot_sync(FULL, c & 4u), b3 = __ballot_sync(FULL, c & 8u);
+    unsigned lt = lanemask_lt();
+    unsigned pre = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt) + 8 * __popc(b3 & lt);
+    unsigned tot = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2) + 8 * __popc(b3);
+    unsigned hb = h + b, pos = t + pre;
+    while (mask) {
+      int k = __ffs(mask) - 1;
+      mask &= mask - 1;
+      if (pos - hb < qlimit)
+        s.ring[pos & (RQ - 1)] = (uint16_t)sidx(px + Nbr<CONN>::dx(k), py + Nbr<CONN>::dy(k));
+      pos++;
+    }
+    if (l0) pushes += tot;
+    h = hb;
+    t += tot;
+    __syncwarp();
+    if (t - h > qlimit) {  // dropped pushes: discard and rescan the tile
+      if (l0) overflows++;
+      rescan = true;
+      continue;
+    }
+    if (h == t) {
+      if (!pending) break;
+      rescan = true;
     }
   }
-  __syncthreads();
-  unsigned n = *s_n;
-  return n < qlimit ? n : qlimit;
 }
 
-// BQ propagation to the tile-local fixed point (level-synchronous inside
-// the CTA; K.220-270 semantics with atomicMax merges, recon.py:92-101).
-// Dropped work (BQ overflow) is recovered by a full rescan of the tile.
-template <int CONN>
-__device__ void tile_fixpoint(SmemLayout &s, unsigned *s_n, unsigned *s_over, unsigned *s_changed,
-                              unsigned qlimit, unsigned long long &pushes,
-                              unsigned long long &overflows, unsigned long long &seeds) {
-  const unsigned FULL = 0xffffffffu;
-  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int cur = 0;
-  unsigned n = 0;
-  bool rescan = true;
-  for (;;) {
-    if (n == 0) {
-      if (!rescan) break;
-      if (threadIdx.x == 0) {
-        s_n[0] = 0;
-        *s_over = 0;
-      }
-      __syncthreads();
-      n = detect_seeds<CONN>(s, &s_n[0], s_over, qlimit);
-      rescan = *s_over != 0;
-      if (threadIdx.x == 0) {
-        seeds += n;
-        if (rescan) overflows++;
-      }
-      cur = 0;
-      __syncthreads();
-      if (n == 0) break;
-    }
-    if (threadIdx.x == 0) {
-      s_n[1 - cur] = 0;
-      *s_over = 0;
-    }
-    __syncthreads();
-    const uint16_t *in = s.q[cur];
-    uint16_t *out = s.q[1 - cur];
-    for (unsigned base = warp * 32; base < n; base += blockDim.x) {
-      unsigned i = base + lane;
-      unsigned mask = 0;
-      int p = 0;
-      if (i < n) {
-        p = in[i];
-        int v = s.J[p];
-        int py = p / PW, px = p - py * PW;
-#pragma unroll
-        for (int k = 0; k < Nbr<CONN>::N; k++) {
-          int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
-          if (interior(qx, qy)) {
-            int qq = qy * PW + qx;
-            int vq = s.J[qq];
-            int iq = s.I[qq];
-            if (vq < v && vq < iq) {
-              int nv = v < iq ? v : iq;
-              int old = atomicMax(&s.J[qq], nv);
-              if (old < nv) mask |= 1u << k;
-            }
-          }
-        }
-      }
-      unsigned cnt = __popc(mask);
-      unsigned pos = warp_reserve(&s_n[1 - cur], cnt, FULL);
-      if (cnt) {
-        *s_changed = 1;
-        int py = p / PW, px = p - py * PW;
-        while (mask) {
-          int k = __ffs(mask) - 1;
-          mask &= mask - 1;
-          if (pos < qlimit)
-            out[pos] = (uint16_t)((py + Nbr<CONN>::dy(k)) * PW + px + Nbr<CONN>::dx(k));
-          else
-            *s_over = 1;
-          pos++;
-        }
-      }
-    }
-    __syncthreads();
-    unsigned nn = s_n[1 - cur];
-    if (*s_over) {
-      rescan = true;
-      if (threadIdx.x == 0) overflows++;
-      nn = qlimit;
-    }
-    if (threadIdx.x == 0) pushes += nn;
-    cur = 1 - cur;
-    n = nn;
-    __syncthreads();
-  }
-}
+// --- the persistent kernel ------------------------------------------------------
 
 template <typename T, int CONN>
-__global__ void __launch_bounds__(kTileThreads) tile_engine_kernel(EngineArgs a,
-                                                                   unsigned long long *counters) {
+__global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) tile_engine_kernel(EngineArgs a,
+                                                                  unsigned long long *counters) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SmemLayout s;
-  s.J = (int *)smem_raw;
-  s.I = s.J + PN;
-  s.q[0] = (uint16_t *)(s.I + PN);
-  s.q[1] = s.q[0] + QCAP;
-  s.ring0 = (int *)(s.q[1] + QCAP);
-  __shared__ int s_tile;
-  __shared__ unsigned s_n[2], s_over, s_changed, s_dirs;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpSmem<T> &s = reinterpret_cast<WarpSmem<T> *>(smem_raw)[warp];
+  const bool l0 = lane == 0;
 
   unsigned long long n_tiles = 0, n_reruns = 0, n_push = 0, n_over = 0, n_seeds = 0;
+  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
 
   for (;;) {
-    if (threadIdx.x == 0) {
-      int t;
-      for (;;) {
-        t = ring_pop(a.q);
-        if (t >= 0) {
-          atomicExch(&a.q.state[t], ST_RUNNING);
-          __threadfence();
-          break;
-        }
-        if (ld_acquire(a.q.pending) == 0) break;
-        __nanosleep(64);
-      }
-      s_tile = t;
-    }
-    __syncthreads();
-    const int t = s_tile;
-    if (t < 0) break;
-    const int tx = t % a.ntx, ty = t / a.ntx;
-    const int x0 = tx * TW, y0 = ty * TH;
-
-    // full load of tile + halo
-    for (int i = threadIdx.x; i < PN; i += blockDim.x) load_cell<T>(a, s, i, x0, y0);
-    __syncthreads();
-    for (int r = threadIdx.x; r < 4 * TW; r += blockDim.x) {
-      int side = r / TW, k = r - side * TW;
-      int lx = side < 2 ? k + 1 : (side == 2 ? 1 : TW);
-      int ly = side < 2 ? (side == 0 ? 1 : TH) : k + 1;
-      s.ring0[r] = s.J[ly * PW + lx];
-    }
-    bool first = true;
-    for (;;) {  // re-run loop while neighbours dirtied this tile
-      if (threadIdx.x == 0) {
-        s_n[0] = 0;
-        s_n[1] = 0;
-        s_changed = 0;
-        s_dirs = 0;
-        n_tiles++;
-        if (!first) n_reruns++;
-      }
-      __syncthreads();
-      tile_fixpoint<CONN>(s, s_n, &s_over, &s_changed, a.qlimit, n_push, n_over, n_seeds);
-      __syncthreads();
-      if (s_changed) {
-        // write back the interior
-        for (int i = threadIdx.x; i < TW * TH; i += blockDim.x) {
-          int ly = i / TW + 1, lx = i % TW + 1;
-          int gx = x0 + lx - 1, gy = y0 + ly - 1;
-          if (gx < a.W && gy < a.H) ((T *)a.J)[(size_t)gy * a.W + gx] = (T)s.J[ly * PW + lx];
-        }
+    long long c_pop = l0 ? clock64() : 0;
+    int t = -1;
+    unsigned first = 0;
+    if (l0) {
+      t = ring_pop(a.q);
+      if (t >= 0) {
+        unsigned old = atomicExch(&a.q.state[t], ST_R);
         __threadfence();
+        first = old & ST_V;
+      }
+    }
+    t = __shfl_sync(FULL, t, 0);
+    if (t < 0) break;
+    bool full = __shfl_sync(FULL, first, 0) != 0;
+    const int tx = t % a.ntx, ty = t / a.ntx;
+    const int x0 = tx * TS, y0 = ty * TS;
+    const Lim lim{min(TS, a.W - x0), min(TS, a.H - y0)};
+    long long c_load = l0 ? clock64() : 0;
+    if (l0) ph[0] += c_load - c_pop;
+
+    load_tile<T>(a, s, x0, y0, lane);
+    __syncwarp();
+    for (int r = lane; r < 4 * TS; r += 32) {
+      int lx, ly;
+      ring_cell(r, lx, ly);
+      s.ring0[r] = s.J[sidx(lx, ly)];
+    }
+    if (l0) ph[1] += clock64() - c_load;
+    bool rerun = false;
+    for (;;) {  // re-run while neighbours request it
+      n_tiles += l0;
+      n_reruns += l0 && rerun;
+      long long c_fix = l0 ? clock64() : 0;
+      unsigned long long sd0 = ph[2] + ph[3];
+      bool changed = false;
+      tile_fixpoint<CONN>(s, lim, a.qlimit, full, a.sweeps, a.halo_thresh, lane, changed, n_push,
+                          n_over, n_seeds, ph);
+      full = false;
+      changed = __any_sync(FULL, changed);
+      long long c_st = l0 ? clock64() : 0;
+      if (l0) ph[4] += (c_st - c_fix) - (ph[2] + ph[3] - sd0);
+      if (changed) {
+        __syncwarp();
+        store_tile<T>(a, s, x0, y0, lim, lane);
         // which neighbour tiles can the changed border still raise?
-        for (int h = threadIdx.x; h < 2 * PW + 2 * TH; h += blockDim.x) {
+        // Per side, lane = position along it: cv = the border cell's value
+        // if it changed since last published (else -inf); a halo cell needs
+        // its tile re-run iff it can still be raised (J < I) by the max cv
+        // of its interior neighbours (lanes l-1..l+1 for 8-conn).
+        const int k = lane + 1;
+        auto cv_of = [&](int bx, int by) -> int {
+          if (!interior(lim, bx, by)) return INT_MIN;
+          int vb = s.J[sidx(bx, by)];
+          return vb != s.ring0[ring_index(bx, by)] ? vb : INT_MIN;
+        };
+        auto nb3 = [&](int c) -> int {
+          if (CONN == 4) return c;
+          int u = __shfl_up_sync(FULL, c, 1), d = __shfl_down_sync(FULL, c, 1);
+          if (lane == 0) u = INT_MIN;
+          if (lane == 31) d = INT_MIN;
+          return max(c, max(u, d));
+        };
+        auto need_h = [&](int hx, int hy, int c) -> bool {
+          int gx = x0 + hx - 1, gy = y0 + hy - 1;
+          if (gx < 0 || gx >= a.W || gy < 0 || gy >= a.H) return false;  // outside the image
+          int vh = s.J[sidx(hx, hy)];
+          return vh < (int)s.I[sidx(hx, hy)] && vh < c;
+        };
+        const int ct = cv_of(k, 1), cb = cv_of(k, TS), cl = cv_of(1, k), cr = cv_of(TS, k);
+        const int nt = nb3(ct), nbm = nb3(cb), nl = nb3(cl), nr = nb3(cr);
+        unsigned dirs = 0;
+        if (__any_sync(FULL, need_h(k, 0, nt))) dirs |= 1u << 1;        // N
+        if (__any_sync(FULL, need_h(k, TS + 1, nbm))) dirs |= 1u << 7;  // S
+        if (__any_sync(FULL, need_h(0, k, nl))) dirs |= 1u << 3;        // W
+        if (__any_sync(FULL, need_h(TS + 1, k, nr))) dirs |= 1u << 5;   // E
+        if (CONN == 8) {  // corners touch one interior cell each
+          bool c0 = lane == 0 && need_h(0, 0, ct), c2 = lane == 31 && need_h(TS + 1, 0, ct);
+          bool c6 = lane == 0 && need_h(0, TS + 1, cb), c8 = lane == 31 && need_h(TS + 1, TS + 1, cb);
+          if (__any_sync(FULL, c0)) dirs |= 1u << 0;
+          if (__any_sync(FULL, c2)) dirs |= 1u << 2;
+          if (__any_sync(FULL, c6)) dirs |= 1u << 6;
+          if (__any_sync(FULL, c8)) dirs |= 1u << 8;
+        }
+        __threadfence();  // publish the interior before any neighbour is (re)queued
+        __syncwarp();
+        if (lane < 9 && ((dirs >> lane) & 1u)) {  // one lane per direction
+          int ntxi = tx + (lane % 3) - 1, ntyi = ty + (lane / 3) - 1;
+          if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty)
+            activate(a.q, (unsigned)(ntyi * a.ntx + ntxi));
+        }
+        for (int r = lane; r < 4 * TS; r += 32) {
           int lx, ly;
-          if (h < PW) {
-            lx = h;
-            ly = 0;
-          } else if (h < 2 * PW) {
-            lx = h - PW;
-            ly = TH + 1;
-          } else if (h < 2 * PW + TH) {
-            lx = 0;
-            ly = h - 2 * PW + 1;
-          } else {
-            lx = TW + 1;
-            ly = h - 2 * PW - TH + 1;
-          }
-          int hi = ly * PW + lx;
-          int vh = s.J[hi];
-          if (vh == INT_MIN && s.I[hi] == INT_MIN) continue;  // outside the image
-          if (!(vh < s.I[hi])) continue;
-          bool need = false;
-#pragma unroll
-          for (int k = 0; k < Nbr<CONN>::N; k++) {
-            int bx = lx + Nbr<CONN>::dx(k), by = ly + Nbr<CONN>::dy(k);
-            if (interior(bx, by)) {
-              int ri = ring_index(bx, by);
-              int vb = s.J[by * PW + bx];
-              if (vb != s.ring0[ri] && vh < vb) need = true;
-            }
-          }
-          if (need) {
-            int dxi = lx == 0 ? 0 : (lx == TW + 1 ? 2 : 1);
-            int dyi = ly == 0 ? 0 : (ly == TH + 1 ? 2 : 1);
-            atomicOr(&s_dirs, 1u << (dyi * 3 + dxi));
-          }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0 && s_dirs) {
-          unsigned d = s_dirs;
-          while (d) {
-            int b = __ffs(d) - 1;
-            d &= d - 1;
-            int ntxi = tx + (b % 3) - 1, ntyi = ty + (b / 3) - 1;
-            if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty)
-              activate(a.q, (unsigned)(ntyi * a.ntx + ntxi));
-          }
-        }
-        // the ring as now published
-        for (int r = threadIdx.x; r < 4 * TW; r += blockDim.x) {
-          int side = r / TW, k = r - side * TW;
-          int lx = side < 2 ? k + 1 : (side == 2 ? 1 : TW);
-          int ly = side < 2 ? (side == 0 ? 1 : TH) : k + 1;
-          s.ring0[r] = s.J[ly * PW + lx];
+          ring_cell(r, lx, ly);
+          s.ring0[r] = s.J[sidx(lx, ly)];
         }
       }
-      __syncthreads();
-      // finish: RUNNING -> IDLE, or re-run if a neighbour dirtied us
-      if (threadIdx.x == 0) {
-        unsigned old = atomicCAS(&a.q.state[t], ST_RUNNING, ST_IDLE);
-        if (old == ST_RUNNING) {
+      // finish: R -> idle, or re-run if a neighbour requested it meanwhile
+      int done = 0;
+      if (l0) {
+        unsigned old = atomicCAS(&a.q.state[t], ST_R, 0u);
+        if (old == ST_R) {
           __threadfence();
           atomicSub(a.q.pending, 1u);
-          s_tile = -1;
+          done = 1;
         } else {
-          atomicExch(&a.q.state[t], ST_RUNNING);
+          atomicExch(&a.q.state[t], ST_R);  // consume the request (acquire)
           __threadfence();
         }
       }
-      __syncthreads();
-      if (s_tile < 0) break;
-      // re-run: refresh the halo only (the interior is ours and current)
-      for (int h = threadIdx.x; h < 2 * PW + 2 * TH; h += blockDim.x) {
-        int lx, ly;
-        if (h < PW) {
-          lx = h;
-          ly = 0;
-        } else if (h < 2 * PW) {
-          lx = h - PW;
-          ly = TH + 1;
-        } else if (h < 2 * PW + TH) {
-          lx = 0;
-          ly = h - 2 * PW + 1;
-        } else {
-          lx = TW + 1;
-          ly = h - 2 * PW - TH + 1;
-        }
-        load_cell<T>(a, s, ly * PW + lx, x0, y0);
-      }
-      first = false;
-      __syncthreads();
+      done = __shfl_sync(FULL, done, 0);
+      if (l0) ph[5] += clock64() - c_st;
+      if (done) break;
+      __syncwarp();
+      load_halo<T>(a, s, x0, y0, lane);  // the interior is ours and current
+      __syncwarp();
+      rerun = true;
     }
-    __syncthreads();
   }
-  if (threadIdx.x == 0) {
+  if (l0) {
     atomicAdd(&counters[CNT_TILES], n_tiles);
     atomicAdd(&counters[CNT_RERUNS], n_reruns);
     atomicAdd(&counters[CNT_PUSHES], n_push);
     atomicAdd(&counters[CNT_OVERFLOW], n_over);
     atomicAdd(&counters[CNT_SEEDS], n_seeds);
+    for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
   }
 }
 
-__global__ void tile_queue_init_kernel(TileQueue q, unsigned ntiles, unsigned long long *counters) {
+// Initial GBQ: every tile, ordered by 2x2 colour class (then raster) so the
+// first wave of concurrently running tiles are never neighbours.
+__global__ void tile_queue_init_kernel(TileQueue q, int ntx, int nty, unsigned long long *counters) {
+  unsigned ntiles = (unsigned)ntx * nty;
+  unsigned stride = gridDim.x * blockDim.x;
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  for (unsigned t = i; t < ntiles; t += gridDim.x * blockDim.x) {
-    q.state[t] = ST_QUEUED;
-    q.ring[t] = ((unsigned long long)t << 32) | t;
+  unsigned cx[4], cy[4], base[4];
+  for (int c = 0; c < 4; c++) {
+    cx[c] = (ntx - (c & 1) + 1) / 2;
+    cy[c] = (nty - (c >> 1) + 1) / 2;
+    base[c] = c == 0 ? 0 : base[c - 1] + cx[c - 1] * cy[c - 1];
   }
-  for (unsigned t = ntiles + i; t <= q.mask; t += gridDim.x * blockDim.x) q.ring[t] = ~0ull;
+  for (unsigned t = i; t < ntiles; t += stride) {
+    unsigned tx = t % ntx, ty = t / ntx;
+    unsigned c = (tx & 1) | ((ty & 1) << 1);
+    unsigned slot = base[c] + (ty >> 1) * cx[c] + (tx >> 1);
+    q.state[t] = ST_Q | ST_V;
+    q.ring[slot] = ((unsigned long long)slot << 32) | t;
+  }
+  for (unsigned t = ntiles + i; t <= q.mask; t += stride) q.ring[t] = ~0ull;
   if (i == 0) {
     *q.head = 0;
     *q.tail = ntiles;
@@ -439,15 +769,16 @@ __global__ void tile_queue_init_kernel(TileQueue q, unsigned ntiles, unsigned lo
 }
 
 size_t tile_queue_bytes(unsigned ntiles) {
-  unsigned cap = 1;
-  while (cap < 2 * ntiles + 2) cap <<= 1;
-  return align_up(sizeof(unsigned) * ntiles, 256) + align_up(sizeof(unsigned long long) * cap, 256) +
-         256 * 2;
+  Carver c(nullptr);
+  carve_tile_queue(c, ntiles);
+  return c.off + 256;
 }
 
 TileQueue carve_tile_queue(Carver &c, unsigned ntiles) {
   unsigned cap = 1;
-  while (cap < 2 * ntiles + 2) cap <<= 1;
+  // >= 2x the tiles plus the tickets waiting workers can hold, so a slot is
+  // never refilled before its ticket holder has read it
+  while (cap < 2 * ntiles + 65536) cap <<= 1;
   TileQueue q;
   q.state = c.take<unsigned>(ntiles);
   q.ring = c.take<unsigned long long>(cap);
@@ -461,33 +792,40 @@ TileQueue carve_tile_queue(Carver &c, unsigned ntiles) {
 
 template <typename T, int CONN>
 static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
-                         unsigned long long *counters, int max_blocks, int qcap, cudaStream_t st) {
-  int ntx = (W + TW - 1) / TW, nty = (H + TH - 1) / TH;
+                         unsigned long long *counters, const EngineOpts &o, cudaStream_t st) {
+  int ntx = (W + TS - 1) / TS, nty = (H + TS - 1) / TS;
   unsigned ntiles = (unsigned)ntx * nty;
-  size_t smem = smem_bytes();
+  size_t smem = sizeof(WarpSmem<T>) * kWarpsPerCta;
   auto kern = tile_engine_kernel<T, CONN>;
-  IWPP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTileThreads, smem));
-  if (per_sm < 1) per_sm = 1;
-  int blocks = device_sm_count() * per_sm;
-  if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
-  if ((unsigned)blocks > ntiles) blocks = (int)ntiles;
-  tile_queue_init_kernel<<<(ntiles + 255) / 256 > 1024 ? 1024 : (ntiles + 255) / 256 + 1, 256, 0, st>>>(
-      q, ntiles, counters);
+  static int per_sm_cache = 0;
+  if (per_sm_cache == 0) {
+    IWPP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCtaThreads, smem));
+    per_sm_cache = per_sm < 1 ? 1 : per_sm;
+  }
+  int blocks = device_sm_count() * per_sm_cache;
+  if (o.max_blocks > 0 && blocks > o.max_blocks) blocks = o.max_blocks;
+  unsigned max_b = (ntiles + kWarpsPerCta - 1) / kWarpsPerCta;
+  if ((unsigned)blocks > max_b) blocks = (int)max_b;
+  unsigned ib = (q.mask + 1 + 255) / 256;
+  if (ib > 1024) ib = 1024;
+  tile_queue_init_kernel<<<ib, 256, 0, st>>>(q, ntx, nty, counters);
   IWPP_CUDA_TRY(cudaGetLastError());
-  unsigned qlimit = (qcap > 0 && qcap < QCAP) ? (unsigned)qcap : (unsigned)QCAP;
-  EngineArgs a{J, I, W, H, ntx, nty, ntiles, qlimit, q};
-  kern<<<blocks, kTileThreads, smem, st>>>(a, counters);
+  unsigned qlimit = (o.qcap > 0 && o.qcap < RQ) ? (unsigned)o.qcap : (unsigned)RQ;
+  unsigned hth = o.halo_thresh >= 0 ? (unsigned)o.halo_thresh : kHaloSweepThreshold;
+  bool vec = ((size_t)W * sizeof(T)) % 16 == 0 && (uintptr_t)J % 16 == 0 && (uintptr_t)I % 16 == 0;
+  EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, q};
+  kern<<<blocks, kCtaThreads, smem, st>>>(a, counters);
   IWPP_CUDA_TRY(cudaGetLastError());
   return IWPP_OK;
 }
 
 int run_tile_engine(void *J, const void *I, int W, int H, int dtype, int conn, TileQueue q,
-                    unsigned long long *counters, int max_blocks, int qcap, cudaStream_t st) {
-#define DISPATCH(T)                                                                           \
-  return conn == 8 ? launch_engine<T, 8>(J, I, W, H, q, counters, max_blocks, qcap, st)      \
-                   : launch_engine<T, 4>(J, I, W, H, q, counters, max_blocks, qcap, st)
+                    unsigned long long *counters, const EngineOpts &o, cudaStream_t st) {
+#define DISPATCH(T)                                                        \
+  return conn == 8 ? launch_engine<T, 8>(J, I, W, H, q, counters, o, st) \
+                   : launch_engine<T, 4>(J, I, W, H, q, counters, o, st)
   switch (dtype) {
     case IWPP_U8:
       DISPATCH(uint8_t);

@@ -5,31 +5,52 @@
 namespace iwpp {
 namespace recon {
 
-constexpr int TW = 64, TH = 64;         // tile interior
-constexpr int PW = TW + 2, PH = TH + 2; // with a 1-pixel halo
-constexpr int PN = PW * PH;
-constexpr int QCAP = 4608;              // >= PN so a full rescan always fits
-constexpr int kTileThreads = 256;
-static_assert(TW == TH, "border ring indexing assumes square tiles");
-static_assert(QCAP >= PN, "rescan must fit the block queue");
+// One warp owns one TS x TS tile at a time (plus a 1-pixel halo).
+constexpr int TS = 32;                   // tile side
+constexpr int PW = TS + 2;               // logical tile side with the halo
+constexpr int PS = PW + 1;               // shared-memory row stride (odd: conflict-free)
+constexpr int PN = PW * PW;              // logical cells
+constexpr int PNS = PW * PS;             // shared-memory cells
+constexpr int RQ = 2048;                 // per-warp pixel ring (>= PN: a full rescan fits)
+constexpr int BITW = (PNS + 31) / 32;    // in-queue bitmap words
+constexpr int kWarpsPerCta = 4;
+constexpr int kCtaThreads = 32 * kWarpsPerCta;
+constexpr int kCtaMinBlocks = 5;  // resident CTAs per SM (shared memory allows 5 for u8)
+static_assert(RQ >= PN && (RQ & (RQ - 1)) == 0, "ring must hold a full rescan");
+static_assert(PNS < 65536, "queue entries are 16-bit");
+
+// re-activations whose halo front is wider than this sweep before queueing
+constexpr unsigned kHaloSweepThreshold = 16;
 
 // device counters (workspace)
-enum { CNT_TILES = 0, CNT_RERUNS, CNT_PUSHES, CNT_OVERFLOW, CNT_SEEDS, CNT_VIOL, CNT_N = 8 };
+enum {
+  CNT_TILES = 0, CNT_RERUNS, CNT_PUSHES, CNT_OVERFLOW, CNT_SEEDS, CNT_VIOL,
+  // per-phase SM cycles summed over warps (lane 0's clock; diagnostics)
+  CNT_PH_POP = 8, CNT_PH_LOAD, CNT_PH_SWEEP, CNT_PH_DETECT, CNT_PH_BFS, CNT_PH_STORE,
+  CNT_N = 16
+};
 
 struct TileQueue {
-  unsigned *state;          // per-tile state
-  unsigned long long *ring; // (pos << 32) | tile
-  unsigned mask;            // ring capacity - 1
+  unsigned *state;           // per-tile state bits (recon_tiles.cu: Q, R, V)
+  unsigned long long *ring;  // (pos << 32) | tile
+  unsigned mask;             // ring capacity - 1
   unsigned *head, *tail, *pending;
+};
+
+struct EngineOpts {
+  int max_blocks = 0;    // persistent grid cap in CTAs (0 = all resident)
+  int qcap = 0;          // per-warp pixel-queue capacity (0 = RQ)
+  int sweeps = 1;        // in-tile sweep passes on a tile's first visit
+  int halo_thresh = -1;  // re-activation front that triggers sweeps (-1 = default)
 };
 
 size_t tile_queue_bytes(unsigned ntiles);
 TileQueue carve_tile_queue(Carver &c, unsigned ntiles);
 int run_tile_engine(void *J, const void *I, int W, int H, int dtype, int conn, TileQueue q,
-                    unsigned long long *counters, int max_blocks, int qcap, cudaStream_t st);
+                    unsigned long long *counters, const EngineOpts &o, cudaStream_t st);
 
 inline unsigned num_tiles(int64_t W, int64_t H) {
-  return (unsigned)(((W + TW - 1) / TW) * ((H + TH - 1) / TH));
+  return (unsigned)(((W + TS - 1) / TS) * ((H + TS - 1) / TS));
 }
 
 }  // namespace recon

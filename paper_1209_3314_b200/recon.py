@@ -74,11 +74,14 @@ def _count_violations(m: Image2D, i: Image2D) -> int:
 # ---------------------------------------------------------------------------
 # the device engine
 
-def _opts(cfg: EngineConfig | None, sweeps: int = -1) -> _lib.ReconOpts:
+def _opts(cfg: EngineConfig | None, sweeps: int = -1, tile_sweeps: int = -1,
+          halo_sweep_threshold: int = -1, max_blocks: int = 0) -> _lib.ReconOpts:
     o = _lib.ReconOpts()
     o.sweeps = sweeps
-    o.max_blocks = 0
+    o.max_blocks = max_blocks
     o.check_contract = 0
+    o.tile_sweeps = tile_sweeps
+    o.halo_sweep_threshold = halo_sweep_threshold
     if cfg is not None and cfg.queue.gbq_capacity is not None:
         o.queue_capacity = int(cfg.queue.gbq_capacity)
     else:
@@ -87,11 +90,13 @@ def _opts(cfg: EngineConfig | None, sweeps: int = -1) -> _lib.ReconOpts:
 
 
 def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
-                sweeps: int = -1, stats: dict | None = None):
+                sweeps: int = -1, stats: dict | None = None, tile_sweeps: int = -1,
+                halo_sweep_threshold: int = -1, max_blocks: int = 0):
     """Reconstruction of raw arrays (numpy -> numpy, CUDA tensor -> tensor).
 
     The marker is not modified.  ``stats`` (a dict) receives the device
-    counters when given (this synchronizes the stream).
+    counters when given (this synchronizes the stream).  The remaining
+    keywords are engine tuning knobs (results never depend on them).
     """
     L = _lib.lib()
     from .grid import np_dtype_of, is_device_array
@@ -102,7 +107,7 @@ def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
     H, W = marker.shape
     st = _lib.Stats()
     sp = _lib.ctypes.byref(st) if stats is not None else None
-    opts = _opts(cfg, sweeps)
+    opts = _opts(cfg, sweeps, tile_sweeps, halo_sweep_threshold, max_blocks)
     if is_device_array(marker):
         torch = _lib._torch()
         J = marker.clone()
