@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""Benchmark: megapixels/s of grayscale morphological reconstruction on B200.
+
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W`` prints
+ONE JSON line on rank 0.  N > 1 runs under torchrun, one rank per GPU.
+
+Workload (BASELINE.json configs[1]): reconstruction by dilation of a
+4096x4096 uint8 random marker/mask pair (mask ~ U[0,256), marker =
+max(mask - 40, 0); the generator of the reference's bench/verify/acceptance
+tests), 8-connectivity.  One step = one reference ``recon_fh`` call on the
+device: copy the marker (the reference works on a copy, recon.py:63-64) and
+run the engine to the fixed point.  Inputs are resident in HBM; the L2
+(126 MB > the 48 MB of state) is flushed between timed steps by writing a
+256 MB buffer outside the timed events.  With N GPUs every rank processes
+its own tile (independent tiles, no data-path collective): weak scaling,
+value = all ranks' pixels / max-over-ranks device time.
+
+Extra keys: ``e2e`` (the same metric through the host-buffer C-ABI call,
+H2D + D2H inside the timed region), ``roofline`` (the tile-engine kernel vs
+the measured HBM copy bandwidth), ``cpu_baseline`` (the CPU restatement of
+the reference algorithm, timed on this host's cores), ``extras`` (4-conn,
+int32, EDT and imfill configs of BASELINE.json, single GPU).
+
+``--impl reference`` times the reference's CPU algorithm (the C restatement
+in oracle/: the reference is Python+numba, not compilable
+here) on all host cores, on the same workload and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_PX = 4096
+H_MARKER = 40
+METRIC = "Megapixels/sec: gray morph reconstruction + EDT, 1/2/4/8 B200 vs CPU ref"
+WORKLOAD = "recon_by_dilation 4096x4096 u8 random marker/mask (h=40), 8-connectivity"
+ALG_BYTES_PER_PX = 3  # read marker + read mask + write result
+
+
+def gray_pair(n: int, seed: int, h: int = H_MARKER):
+    """The reference's marker/mask generator (test_acceptance.py:54-57)."""
+    rng = np.random.default_rng(seed)
+    I = rng.integers(0, 256, (n, n)).astype(np.uint8)
+    J = np.maximum(I.astype(np.int32) - h, 0).astype(np.uint8)
+    return J, I
+
+
+def measured_peak_gbs():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel_key: str):
+    """DRAM bytes per launch of a kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d[kernel_key]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = the CPU restatement of the reference algorithm)
+
+def cpu_fh_throughput(J, I, conn, threads: int, rounds: int):
+    """`threads` concurrent recon_fh runs (ctypes drops the GIL) x rounds.
+    Returns (Mpx/s, wall seconds, runs)."""
+    import oracle
+
+    oracle.lib()
+    runs = threads * rounds
+    errs = []
+
+    def work():
+        try:
+            for _ in range(rounds):
+                oracle.recon_fh(J, I, conn)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=work) for _ in range(threads)]
+    t0 = time.perf_counter()
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    wall = time.perf_counter() - t0
+    if errs:
+        raise errs[0]
+    return runs * J.size / wall / 1e6, wall, runs
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return 0
+    J, I = gray_pair(N_PX, 0)
+    cores = host_cores()
+    for _ in range(args.warmup):
+        cpu_fh_throughput(J, I, 8, cores, 1)
+    t_steps = []
+    px = 0
+    for _ in range(args.steps):
+        _, wall, runs = cpu_fh_throughput(J, I, 8, cores, 1)
+        t_steps.append(wall)
+        px += runs * J.size
+    total = sum(t_steps)
+    value = px / total / 1e6
+    sample = (f"{cores} concurrent recon_fh runs of the 4096^2 u8 8-conn workload per step "
+              f"(C restatement of the reference, oracle/iwpp_oracle.c)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "Mpx/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "shape": [N_PX, N_PX], "conn": 8, "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": round(value, 3), "unit": "Mpx/s", "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "Mpx/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# device legs
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    from paper_1209_3314_b200 import _lib
+    from paper_1209_3314_b200.build import LIB
+
+    L = _lib.lib()
+    dev = torch.device(f"cuda:{local}")
+    Jh, Ih = gray_pair(N_PX, rank)
+    dJ = torch.from_numpy(Jh).to(dev)
+    dI = torch.from_numpy(Ih).to(dev)
+    out = torch.empty_like(dJ)
+    W = H = N_PX
+    ws = _lib.workspace(L.iwpp_recon_workspace_bytes(W, H, 0, 8))
+    ev0, ev1 = _lib.Event(), _lib.Event()
+    opts = _lib.ReconOpts()
+    opts.sweeps, opts.max_blocks, opts.check_contract, opts.queue_capacity = -1, 0, 0, 0
+    opts.tile_sweeps, opts.halo_sweep_threshold = -1, -1
+    opts.ev_begin, opts.ev_end = ev0.handle, ev1.handle
+    stream = _lib.stream_ptr()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
+
+    def step():
+        out.copy_(dJ)  # the operator works on a copy of the marker
+        _lib.check(L.iwpp_recon(_lib.ptr(out), _lib.ptr(dI), W, H, 0, 8, _lib.ptr(ws),
+                                ws.numel(), _lib.ctypes.byref(opts), None, stream), "recon")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    step_ms, kern_ms = [], []
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xff)  # evict the inputs from L2 (outside the timed events)
+            s0.record()
+            step()
+            s1.record()
+            s1.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            kern_ms.append(ev0.elapsed_ms(ev1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+
+    # parity spot check of the benchmarked output (bit-exact oracle on rank 0)
+    ok = None
+    if rank == 0 and not args.no_cpu:
+        import oracle
+        ok = bool(np.array_equal(out.cpu().numpy(), oracle.recon_fh(Jh, Ih, 8)))
+
+    # e2e: host buffers through the C ABI (H2D + D2H inside the timed region)
+    pin_J = torch.from_numpy(Jh).pin_memory()
+    pin_I = torch.from_numpy(Ih).pin_memory()
+    pin_O = torch.empty_like(pin_J).pin_memory()
+    wsh = _lib.workspace(L.iwpp_recon_host_workspace_bytes(W, H, 0, 8))
+    e2e_opts = _lib.ReconOpts()
+    e2e_opts.sweeps, e2e_opts.max_blocks, e2e_opts.check_contract = -1, 0, 0
+    e2e_opts.queue_capacity, e2e_opts.tile_sweeps, e2e_opts.halo_sweep_threshold = 0, -1, -1
+
+    def e2e_step():
+        _lib.check(L.iwpp_recon_host(_lib.ptr(pin_O.numpy()), _lib.ptr(pin_J.numpy()),
+                                     _lib.ptr(pin_I.numpy()), W, H, 0, 8, _lib.ptr(wsh),
+                                     wsh.numel(), _lib.ctypes.byref(e2e_opts), None, stream),
+                   "recon_host")
+
+    for _ in range(2):
+        e2e_step()
+    e2e_t = []
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_step()  # synchronous: returns after the D2H copy
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_total = sum(e2e_t)
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_val = world * args.steps * W * H / e2e_total / 1e6
+
+    value = world * args.steps * W * H / (total_ms / 1e3) / 1e6
+    peak, peak_kind = measured_peak_gbs()
+    kavg = statistics.mean(kern_ms)
+    achieved = ALG_BYTES_PER_PX * W * H / (kavg / 1e3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "Mpx/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (reference generator: mask ~ U[0,256), marker = max(mask-40, 0))",
+        "config": {"workload": WORKLOAD, "shape": [H, W], "conn": 8,
+                   "per_rank_tiles": 1, "parallelism": f"independent tiles x{world}",
+                   "l2": "flushed between timed steps (256 MB write outside the events)"},
+        "clocks": clk.summary(),
+        "e2e": {"value": round(e2e_val, 2), "unit": "Mpx/s",
+                "h2d_bytes_per_step": 2 * W * H, "d2h_bytes_per_step": W * H,
+                "path": "iwpp_recon_host (pinned host buffers, C ABI)"},
+        "gpu_launches": 2 * args.steps,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": ncu_traffic("recon_tile_engine_u8_c8"),
+                     "kernel": "tile_engine_kernel<uint8,8>",
+                     "kernel_ms": round(kavg, 4), "alg_bytes_per_px": ALG_BYTES_PER_PX,
+                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
+        "library": os.path.relpath(LIB, ROOT),
+        "parity_vs_oracle": ok,
+    }
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        J, I = Jh, Ih
+        cores = host_cores()
+        rounds = 1
+        v, wall, runs = cpu_fh_throughput(J, I, 8, cores, rounds)
+        line["cpu_baseline"] = {
+            "value": round(v, 3), "unit": "Mpx/s", "cores": cores, "kind": "port",
+            "sample": f"{runs} recon_fh runs of the 4096^2 u8 8-conn workload on {cores} "
+                      f"threads ({wall:.1f} s wall; oracle/iwpp_oracle.c)"}
+
+    if rank == 0 and world == 1 and not args.no_extras:
+        line["extras"] = extras(L, _lib, dev, flush)
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def extras(L, _lib, dev, flush):
+    """Secondary BASELINE.json configs (single GPU): each timed over a few
+    device-resident calls with the L2 flushed in between."""
+    import torch
+    import paper_1209_3314_b200 as gw
+
+    out = {}
+
+    def timed(fn, reps=5, warm=2):
+        for _ in range(warm):
+            fn()
+        ts = []
+        for i in range(reps):
+            flush.fill_(i & 0xff)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    J, I = gray_pair(N_PX, 0)
+    dJ, dI = torch.from_numpy(J).to(dev), torch.from_numpy(I).to(dev)
+    ms = timed(lambda: gw.reconstruct(dJ, dI, 4))
+    out["recon_4k_u8_c4"] = {"ms": round(ms, 4), "mpx_s": round(N_PX * N_PX / ms / 1e3, 1)}
+
+    rng = np.random.default_rng(0)
+    I32 = rng.integers(0, 2**31 - 1, (N_PX, N_PX), dtype=np.int32)
+    J32 = np.maximum(I32.astype(np.int64) - (1 << 28), 0).astype(np.int32)
+    dJ32, dI32 = torch.from_numpy(J32).to(dev), torch.from_numpy(I32).to(dev)
+    ms = timed(lambda: gw.reconstruct(dJ32, dI32, 8))
+    out["recon_4k_i32_c8"] = {"ms": round(ms, 4), "mpx_s": round(N_PX * N_PX / ms / 1e3, 1)}
+
+    import oracle  # input generators only (restated imgio generators)
+
+    for name, m in (("edt_4k_nuclei_c8", oracle.gen_nuclei_mask(N_PX, N_PX, 30.0, 7)),
+                    ("edt_4k_blob_c8", oracle.gen_synthetic_mask(N_PX, N_PX, 50, 7))):
+        img = gw.Image2D(N_PX, N_PX, "binary", torch.from_numpy(m).to(dev))
+        cfg = gw.EngineConfig()
+        gw.edt(img, gw.SE8, mode="parallel", cfg=cfg)
+        ms = timed(lambda: gw.edt(img, gw.SE8), reps=3)
+        out[name] = {"ms": round(ms, 4), "mpx_s": round(N_PX * N_PX / ms / 1e3, 1),
+                     "rounds": cfg.stats.rounds}
+
+    bw = np.tile(oracle.gen_synthetic_mask(N_PX, N_PX, 50, 7), (4, 4))
+    mk, msk = oracle.imfill_pair(bw)
+    dM, dK = torch.from_numpy(mk).to(dev), torch.from_numpy(msk).to(dev)
+    n16 = bw.size
+    for conn in (4, 8):
+        ms = timed(lambda: gw.reconstruct(dM, dK, conn), reps=3, warm=1)
+        out[f"imfill_16k_c{conn}"] = {"ms": round(ms, 3), "mpx_s": round(n16 / ms / 1e3, 1)}
+    return out
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -89,7 +89,16 @@ typedef struct iwpp_recon_opts {
                         overflow -> rescan path (QueueConfig.gbq_capacity, wqueue.py:58-60) */
   int tile_sweeps;   /* in-tile row/column sweep passes on a tile's first visit (-1 = auto) */
   int halo_sweep_threshold; /* re-visit: sweep when more halo pixels than this are active (-1 = auto) */
+  void *ev_begin;    /* optional events (iwpp_event_create) recorded on the stream */
+  void *ev_end;      /* right before / after the tile-engine kernel (roofline timing) */
 } iwpp_recon_opts;
+
+/* Timing helpers (events live in this library's CUDA runtime). */
+int iwpp_event_create(void **ev);
+int iwpp_event_destroy(void *ev);
+int iwpp_event_record(void *ev, void *stream);
+/* milliseconds between two recorded events (synchronizes on `end`) */
+int iwpp_event_elapsed_ms(void *begin, void *end, float *ms);
 
 size_t iwpp_recon_workspace_bytes(int64_t W, int64_t H, int dtype, int conn);
 int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn,

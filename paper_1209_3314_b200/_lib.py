@@ -33,6 +33,7 @@ EXPORTS = (
     "iwpp_recon_sweep_rows", "iwpp_recon_sweep_cols",
     "iwpp_recon_seed_scan", "iwpp_edt_workspace_bytes", "iwpp_edt", "iwpp_edt_propagate",
     "iwpp_edt_finalize", "iwpp_edt_host_workspace_bytes", "iwpp_edt_host",
+    "iwpp_event_create", "iwpp_event_destroy", "iwpp_event_record", "iwpp_event_elapsed_ms",
 )
 
 
@@ -48,7 +49,8 @@ class Stats(ctypes.Structure):
 class ReconOpts(ctypes.Structure):
     _fields_ = [("sweeps", ctypes.c_int), ("max_blocks", ctypes.c_int),
                 ("check_contract", ctypes.c_int), ("queue_capacity", ctypes.c_int),
-                ("tile_sweeps", ctypes.c_int), ("halo_sweep_threshold", ctypes.c_int)]
+                ("tile_sweeps", ctypes.c_int), ("halo_sweep_threshold", ctypes.c_int),
+                ("ev_begin", ctypes.c_void_p), ("ev_end", ctypes.c_void_p)]
 
 
 _lib = None
@@ -88,6 +90,10 @@ def load_library(path: str = LIB_PATH):
             "iwpp_edt_finalize": ([P, I64, I64, P, P, P, P], I),
             "iwpp_edt_host_workspace_bytes": ([I64, I64, I], SZ),
             "iwpp_edt_host": ([P, I64, I64, I, P, P, P, SZ, I64, SP, P], I),
+            "iwpp_event_create": ([ctypes.POINTER(P)], I),
+            "iwpp_event_destroy": ([P], I),
+            "iwpp_event_record": ([P, P], I),
+            "iwpp_event_elapsed_ms": ([P, P, ctypes.POINTER(ctypes.c_float)], I),
         }
         for name, (args, res) in proto.items():
             fn = getattr(L, name)
@@ -144,6 +150,31 @@ def workspace(nbytes: int):
 
 def stream_ptr():
     return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+class Event:
+    """A CUDA event owned by libiwpp_b200 (same runtime as its kernels)."""
+
+    def __init__(self):
+        L = lib()
+        h = ctypes.c_void_p()
+        check(L.iwpp_event_create(ctypes.byref(h)), "event_create")
+        self.handle = h
+
+    def record(self, stream=None):
+        check(lib().iwpp_event_record(self.handle, stream if stream is not None else stream_ptr()))
+
+    def elapsed_ms(self, end: "Event") -> float:
+        ms = ctypes.c_float()
+        check(lib().iwpp_event_elapsed_ms(self.handle, end.handle, ctypes.byref(ms)))
+        return float(ms.value)
+
+    def __del__(self):
+        try:
+            if _lib is not None and self.handle:
+                _lib.iwpp_event_destroy(self.handle)
+        except Exception:
+            pass
 
 
 def ptr(a):

@@ -141,6 +141,8 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
     eo.qcap = opts->queue_capacity;
     if (opts->tile_sweeps >= 0) eo.sweeps = opts->tile_sweeps;
     eo.halo_thresh = opts->halo_sweep_threshold;
+    eo.ev_begin = opts->ev_begin;
+    eo.ev_end = opts->ev_end;
   }
   if ((rc = recon::run_tile_engine(J, I, (int)W, (int)H, dtype, conn, w.q, w.counters, eo, st)))
     return rc;
@@ -183,13 +185,33 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   unsigned long long viol = 0;
   IWPP_CUDA_TRY(cudaMemcpyAsync(&viol, &w.counters[recon::CNT_VIOL], sizeof viol,
                                 cudaMemcpyDeviceToHost, st));
-  iwpp_recon_opts o = opts ? *opts : iwpp_recon_opts{-1, 0, 0, 0, -1, -1};
+  iwpp_recon_opts o = opts ? *opts : iwpp_recon_opts{-1, 0, 0, 0, -1, -1, nullptr, nullptr};
   o.check_contract = 0;
   if ((rc = iwpp_recon(dJ, dI, W, H, dtype, conn, rest, rest_bytes, &o, nullptr, stream))) return rc;
   IWPP_CUDA_TRY(cudaMemcpyAsync(out, dJ, nb, cudaMemcpyDeviceToHost, st));
   IWPP_CUDA_TRY(cudaStreamSynchronize(st));
   if (viol) return set_error(IWPP_E_CONTRACT, "marker exceeds mask somewhere (%llu cells)", viol);
   if (stats) return fill_recon_stats(w, stats, st);
+  return IWPP_OK;
+}
+
+int iwpp_event_create(void **ev) {
+  cudaEvent_t e;
+  IWPP_CUDA_TRY(cudaEventCreate(&e));
+  *ev = (void *)e;
+  return IWPP_OK;
+}
+int iwpp_event_destroy(void *ev) {
+  IWPP_CUDA_TRY(cudaEventDestroy((cudaEvent_t)ev));
+  return IWPP_OK;
+}
+int iwpp_event_record(void *ev, void *stream) {
+  IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)stream));
+  return IWPP_OK;
+}
+int iwpp_event_elapsed_ms(void *begin, void *end, float *ms) {
+  IWPP_CUDA_TRY(cudaEventSynchronize((cudaEvent_t)end));
+  IWPP_CUDA_TRY(cudaEventElapsedTime(ms, (cudaEvent_t)begin, (cudaEvent_t)end));
   return IWPP_OK;
 }
 

@@ -816,8 +816,10 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   unsigned hth = o.halo_thresh >= 0 ? (unsigned)o.halo_thresh : kHaloSweepThreshold;
   bool vec = ((size_t)W * sizeof(T)) % 16 == 0 && (uintptr_t)J % 16 == 0 && (uintptr_t)I % 16 == 0;
   EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, q};
+  if (o.ev_begin) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_begin, st));
   kern<<<blocks, kCtaThreads, smem, st>>>(a, counters);
   IWPP_CUDA_TRY(cudaGetLastError());
+  if (o.ev_end) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_end, st));
   return IWPP_OK;
 }
 

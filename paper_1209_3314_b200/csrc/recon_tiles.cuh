@@ -42,6 +42,7 @@ struct EngineOpts {
   int qcap = 0;          // per-warp pixel-queue capacity (0 = RQ)
   int sweeps = 1;        // in-tile sweep passes on a tile's first visit
   int halo_thresh = -1;  // re-activation front that triggers sweeps (-1 = default)
+  void *ev_begin = nullptr, *ev_end = nullptr;  // cudaEvent_t around the engine kernel
 };
 
 size_t tile_queue_bytes(unsigned ntiles);
