@@ -10,22 +10,30 @@
 // Per tile activation:
 //
 //   1. load tile + halo (16-byte vector loads of the rows, L2-coherent)
-//   2. sweeps (first visit, or a wide front entering): lane = line, each
+//   2. halo offers: every (halo -> border cell) pair is applied once, so the
+//      halo never has to be queued (values only grow: an applied offer stays
+//      satisfied) and all queue items are interior cells
+//   3. sweeps (first visit, or a wide front entering): lane = line, each
 //      lane walks its row W->E / E->W, then its column N->S / S->N with
 //      v <- clamp(v, J, I) -- the paper's raster / anti-raster scan phase in
-//      its axis-decomposed form (Alg. 5), halo cells as fixed sources
-//   3. initial-wavefront detection: every cell (interior or halo) that can
-//      still raise an interior neighbour (J(q) < J(p), J(q) < I(q)),
-//      computed as a 3x3 (8-conn) / cross (4-conn) min filter over the
-//      "raisable" values, lane = column, sliding row window in registers;
+//      its axis-decomposed form (Alg. 5)
+//   4. initial-wavefront detection fused into the last walk: a cell is
+//      active iff it can raise a neighbour (J(q) < J(p), J(q) < I(q)), i.e.
+//      J(p) > min over N(p) of the "raisable" values -- a 3x3 (8-conn) /
+//      cross (4-conn) min filter, sliding row window in registers,
 //      ballot-compacted into the warp's pixel queue
-//   4. propagation to the tile's fixed point: the warp drains its pixel
-//      queue 32 items per step with shared atomicMax merges
+//   5. propagation to the tile's fixed point: the warp drains its pixel
+//      queue 32 items per step; each lane offers its cell's value to its 8
+//      (4) neighbours with predicated shared atomicMax
 //      (J(q) <- min(J(p), I(q)) iff J(q) < J(p) and J(q) != I(q),
-//      recon.py:92-101); pushes are placed by bit-plane ballots (no
-//      atomics), an in-queue bitmap dedupes them
-//   5. write the interior back and activate the neighbour tiles whose
-//      cells the changed border can still raise.
+//      recon.py:92-101); pushes are placed by bit-plane ballots (no atomics)
+//   6. write the interior back and activate the neighbour tiles whose cells
+//      the changed border can still raise.
+//
+// Sentinels instead of bounds checks: halo cells and cells outside the image
+// carry I = min(T) in the propagation arrays (never raisable); cells outside
+// the image also carry J = min(T) (raise nothing).  The halo's real mask
+// values live apart (Ih) for the activation test.
 //
 // Queue hierarchy (the paper's TQ/BQ/GBQ):
 //   TQ  : per-lane register bitmask of raised neighbours (<= 8 bits)
@@ -33,9 +41,9 @@
 //   GBQ : global MPMC ring of tile ids (ticket pop, per-tile state bits);
 //         a tile whose halo a neighbour raised re-enters it -- the BP border
 //         exchange of tiles.py:342-359, asynchronous, no wave barriers.
-// BQ overflow (only reachable with a user-forced small capacity,
-// QueueConfig.gbq_capacity) drops work and re-seeds the tile by a full
-// rescan -- the drop / rescan / re-execute contract of engine.py:274-303.
+// BQ overflow (user-forced small capacity, QueueConfig.gbq_capacity) drops
+// work and re-seeds the tile by a full rescan -- the drop / rescan /
+// re-execute contract of engine.py:274-303.
 // Termination: a global count of queued+running tiles reaches 0.
 //
 // The fixed point is unique (engine.py:9-18), so this asynchronous schedule
@@ -53,18 +61,13 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr unsigned ST_Q = 1, ST_R = 2, ST_V = 4;
 constexpr int RING = 4 * TS + 4;  // halo cells
 
-// One warp's shared memory.  J is int32 so the hardware atomicMax covers
-// every element kind; I keeps the element type.  Cells outside the image
-// hold J = INT_MIN, I = min(T): never a source, and a clamp through them can
-// never raise an in-image cell; interior cells past the image edge are also
-// excluded from detection and propagation by the tile's in-image extent.
 template <typename T>
 struct alignas(16) WarpSmem {
   int J[PNS];
-  alignas(16) T I[PNS];
+  alignas(16) T I[PNS];    // interior: mask; halo / outside the image: min(T)
+  alignas(16) T Ih[RING];  // the halo's real mask values (activation test)
   alignas(16) uint16_t ring[RQ];  // pixel queue (absolute positions mod RQ)
-  alignas(16) unsigned bits[BITW];
-  int ring0[4 * TS];  // border ring as last published
+  int ring0[4 * TS];              // border ring as last published
 };
 
 struct EngineArgs {
@@ -73,21 +76,18 @@ struct EngineArgs {
   int W, H;
   int ntx, nty;
   unsigned qlimit;       // pixel-queue capacity actually used (<= RQ)
-  unsigned halo_thresh;  // re-activation halo front above which to sweep first
+  unsigned halo_thresh;  // re-activation front above which to sweep first
   int sweeps;            // sweep passes on a tile's first visit
   int vec;               // rows are 16-byte aligned
   TileQueue q;
 };
 
-struct Lim {  // in-image interior extent of the current tile: 1..x, 1..y
-  int x, y;
-};
-
 __device__ __forceinline__ int sidx(int lx, int ly) { return ly * PS + lx; }
-__device__ __forceinline__ bool interior(Lim l, int lx, int ly) {
-  return lx >= 1 && lx <= l.x && ly >= 1 && ly <= l.y;
-}
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(hi, max(lo, v)); }
+template <int CONN>
+__device__ __forceinline__ int noff(int k) {  // neighbour k as a shared-memory index offset
+  return Nbr<CONN>::dy(k) * PS + Nbr<CONN>::dx(k);
+}
 
 // halo cell h in [0, RING) -> (lx, ly): top row, bottom row, left, right
 __device__ __forceinline__ void halo_cell(int h, int &lx, int &ly) {
@@ -129,11 +129,12 @@ __device__ __forceinline__ void ring_push(const TileQueue &q, unsigned t) {
 // Ticket pop: one fetch-and-add per pop (no CAS retry storms on the head),
 // then wait until the slot carries the ticket's tag.  Returns -1 once the
 // engine has terminated (no tile queued or running: nothing can be pushed
-// any more, and a filled slot would imply a queued tile).
+// any more, and a filled slot would imply a queued tile).  Idle workers back
+// off to ~1 us so they do not steal issue slots from busy ones.
 __device__ __forceinline__ int ring_pop(const TileQueue &q) {
   unsigned ticket = atomicAdd(q.head, 1u);
   unsigned long long *slot = &q.ring[ticket & q.mask];
-  for (unsigned ns = 32;; ns = ns < 256 ? ns * 2 : 256) {
+  for (unsigned ns = 64;; ns = ns < 1024 ? ns * 2 : 1024) {
     unsigned long long v = ld_acquire64(slot);
     if ((unsigned)(v >> 32) == ticket) return (int)(v & 0xffffffffu);
     if (ld_acquire(q.pending) == 0) return -1;
@@ -158,26 +159,22 @@ __device__ __forceinline__ void activate(const TileQueue &q, unsigned t) {
 // --- loads / stores (warp) -----------------------------------------------------
 
 template <typename T>
-__device__ __forceinline__ void load_scalar(const EngineArgs &a, WarpSmem<T> &s, int lx, int ly,
-                                            int x0, int y0) {
-  int gx = x0 + lx - 1, gy = y0 + ly - 1;
-  int i = sidx(lx, ly);
-  if (gx >= 0 && gx < a.W && gy >= 0 && gy < a.H) {
-    size_t g = (size_t)gy * a.W + gx;
-    s.J[i] = (int)ld_cg((const T *)a.J + g);
-    s.I[i] = __ldg((const T *)a.I + g);
-  } else {
-    s.J[i] = INT_MIN;
-    s.I[i] = Elem<T>::lo;
-  }
-}
-
-template <typename T>
 __device__ void load_halo(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, int lane) {
+  constexpr int LO = (int)Elem<T>::lo;
   for (int h = lane; h < RING; h += 32) {
     int lx, ly;
     halo_cell(h, lx, ly);
-    load_scalar<T>(a, s, lx, ly, x0, y0);
+    int gx = x0 + lx - 1, gy = y0 + ly - 1;
+    int i = sidx(lx, ly);
+    s.I[i] = Elem<T>::lo;  // never raisable from inside the tile
+    if (gx >= 0 && gx < a.W && gy >= 0 && gy < a.H) {
+      size_t g = (size_t)gy * a.W + gx;
+      s.J[i] = (int)ld_cg((const T *)a.J + g);
+      s.Ih[h] = __ldg((const T *)a.I + g);
+    } else {
+      s.J[i] = LO;
+      s.Ih[h] = Elem<T>::lo;
+    }
   }
 }
 
@@ -185,6 +182,7 @@ __device__ void load_halo(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, i
 template <typename T>
 __device__ void load_tile(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, int lane) {
   constexpr int E = 16 / sizeof(T), CPR = TS / E;
+  constexpr int LO = (int)Elem<T>::lo;
   const int ly = lane + 1, gy = y0 + lane;
   if (a.vec && x0 + TS <= a.W && gy < a.H) {
     const T *pj = (const T *)a.J + (size_t)gy * a.W + x0;
@@ -202,17 +200,27 @@ __device__ void load_tile(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, i
       }
     }
   } else {
-    for (int lx = 1; lx <= TS; lx++) load_scalar<T>(a, s, lx, ly, x0, y0);
+    for (int lx = 1; lx <= TS; lx++) {
+      int gx = x0 + lx - 1, i = sidx(lx, ly);
+      if (gx < a.W && gy < a.H) {
+        size_t g = (size_t)gy * a.W + gx;
+        s.J[i] = (int)ld_cg((const T *)a.J + g);
+        s.I[i] = __ldg((const T *)a.I + g);
+      } else {  // outside the image: raises nothing, never raised
+        s.J[i] = LO;
+        s.I[i] = Elem<T>::lo;
+      }
+    }
   }
   load_halo<T>(a, s, x0, y0, lane);
 }
 
 template <typename T>
-__device__ void store_tile(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, Lim lim,
-                           int lane) {
+__device__ void store_tile(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, int limx,
+                           int limy, int lane) {
   constexpr int E = 16 / sizeof(T), CPR = TS / E;
   const int ly = lane + 1, gy = y0 + lane;
-  if (ly > lim.y) return;
+  if (ly > limy) return;
   T *pj = (T *)a.J + (size_t)gy * a.W + x0;
   if (a.vec && x0 + TS <= a.W) {
 #pragma unroll
@@ -224,8 +232,62 @@ __device__ void store_tile(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, 
       reinterpret_cast<uint4 *>(pj)[c] = v;
     }
   } else {
-    for (int lx = 1; lx <= lim.x; lx++) pj[lx - 1] = (T)s.J[sidx(lx, ly)];
+    for (int lx = 1; lx <= limx; lx++) pj[lx - 1] = (T)s.J[sidx(lx, ly)];
   }
+}
+
+// --- halo offers ---------------------------------------------------------------
+//
+// Apply every (halo h -> border cell q) offer once: J(q) <- max(J(q),
+// min(J(h), I(q))).  Sides run one after the other (a corner cell belongs to
+// two sides), lane = position along the side.  Returns, per lane, a bitmask
+// of the sides whose border cell this lane raised.
+template <int CONN, typename T>
+__device__ unsigned halo_offers(WarpSmem<T> &s, int lane) {
+  const int k = lane + 1;
+  unsigned raised = 0;
+  // (q, halo row/col offset direction): top, bottom, left, right
+#pragma unroll
+  for (int side = 0; side < 4; side++) {
+    int qx, qy, hx, hy, sx, sy;  // q, the facing halo cell, step along the side
+    if (side == 0) { qx = k; qy = 1; hx = k; hy = 0; sx = 1; sy = 0; }
+    else if (side == 1) { qx = k; qy = TS; hx = k; hy = TS + 1; sx = 1; sy = 0; }
+    else if (side == 2) { qx = 1; qy = k; hx = 0; hy = k; sx = 0; sy = 1; }
+    else { qx = TS; qy = k; hx = TS + 1; hy = k; sx = 0; sy = 1; }
+    int q = sidx(qx, qy);
+    int best = s.J[sidx(hx, hy)];
+    if (CONN == 8) {
+      best = max(best, s.J[sidx(hx - sx, hy - sy)]);
+      best = max(best, s.J[sidx(hx + sx, hy + sy)]);
+    }
+    int jq = s.J[q], iq = (int)s.I[q];
+    int nv = min(best, iq);
+    if (nv > jq) {
+      s.J[q] = nv;
+      raised |= 1u << side;
+    }
+    __syncwarp();
+  }
+  return raised;
+}
+
+// queue a ballot of cells (one per lane) at the warp tail; returns the new tail
+__device__ __forceinline__ unsigned push_ballot(uint16_t *ring, unsigned t, bool want, int p,
+                                                unsigned qlimit) {
+  unsigned k = __ballot_sync(FULL, want);
+  unsigned pos = t + __popc(k & lanemask_lt());
+  if (want && pos < qlimit) ring[pos & (RQ - 1)] = (uint16_t)p;
+  return t + __popc(k);
+}
+
+__device__ __forceinline__ unsigned queue_halo_raised(uint16_t *ring, unsigned t, unsigned raised,
+                                                      unsigned qlimit, int lane) {
+  const int k = lane + 1;
+  t = push_ballot(ring, t, raised & 1u, sidx(k, 1), qlimit);
+  t = push_ballot(ring, t, raised & 2u, sidx(k, TS), qlimit);
+  t = push_ballot(ring, t, raised & 4u, sidx(1, k), qlimit);
+  t = push_ballot(ring, t, raised & 8u, sidx(TS, k), qlimit);
+  return t;
 }
 
 // --- sweeps (the paper's scan phase, Alg. 5 axis decomposition) ---------------
@@ -233,10 +295,8 @@ __device__ void store_tile(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, 
 // lane = line; the lane walks its 32 cells with v <- clamp(v, J, I) from the
 // cell before the line: rows W->E then E->W (K.115-139), then columns N->S
 // then S->N (K.142-190, vertical neighbour).  Straight-line code: compile-
-// time stride, a chunk's loads issued together, unconditional stores.
-// Partial tiles walk all 32 cells: cells past the image edge hold the
-// sentinel (J = INT_MIN, I = min(T)), and clamp(v, INT_MIN, min(T)) <= min(T)
-// can never raise an in-image cell.
+// time stride, a chunk's loads issued together, unconditional stores.  A
+// clamp through a sentinel cell (I = min(T)) can never raise an in-image cell.
 template <int STEP, typename T>
 __device__ __forceinline__ bool walk_line(WarpSmem<T> &s, int first, int carry_idx) {
   constexpr int C = 8;
@@ -274,89 +334,47 @@ __device__ bool sweep_pass(WarpSmem<T> &s, int lane) {
 }
 
 // --- detection -----------------------------------------------------------------
+//
+// Raisable value m(q) = J(q) if J(q) < I(q) else +inf (halo and outside cells
+// are never raisable by construction).  p is active iff J(p) > min over N(p)
+// of m.  lane = column; lr = min(m left, m right) by shuffles (the halo
+// columns' m is +inf).
 
-// "raisable" value: J if the cell is an in-image interior cell below its
-// mask, else +inf.  p is active iff J(p) > min over N(p) of m.
-template <typename T>
-__device__ __forceinline__ int mval(const WarpSmem<T> &s, Lim lim, int lx, int ly) {
-  if (!interior(lim, lx, ly)) return INT_MAX;
-  int i = sidx(lx, ly);
-  int j = s.J[i];
-  return j < (int)s.I[i] ? j : INT_MAX;
+__device__ __forceinline__ int lr_of(int m, int lane) {
+  int l = __shfl_up_sync(FULL, m, 1), r = __shfl_down_sync(FULL, m, 1);
+  if (lane == 0) l = INT_MAX;
+  if (lane == 31) r = INT_MAX;
+  return min(l, r);
 }
 
+template <int CONN>
+__device__ __forceinline__ int window_lo(int m_n, int lr_n, int m_c, int lr_c, int m_p, int lr_p) {
+  return CONN == 8 ? min(min(min(m_p, lr_p), min(m_c, lr_c)), min(m_n, lr_n))
+                   : min(min(lr_c, m_p), m_n);
+}
+
+// Full detection over the interior (rows stream through a 3-row window).
 template <int CONN, typename T>
-__device__ __forceinline__ bool can_raise(const WarpSmem<T> &s, Lim lim, int lx, int ly) {
-  int v = s.J[sidx(lx, ly)];
-  bool want = false;
-#pragma unroll
-  for (int k = 0; k < Nbr<CONN>::N; k++) {
-    int qx = lx + Nbr<CONN>::dx(k), qy = ly + Nbr<CONN>::dy(k);
-    if (interior(lim, qx, qy)) {
-      int qq = sidx(qx, qy);
-      int vq = s.J[qq];
-      if (vq < v && vq < (int)s.I[qq]) want = true;
-    }
-  }
-  return want;
-}
-
-// queue a ballot of cells (one per lane) at the warp tail; returns the new tail
-__device__ __forceinline__ unsigned push_ballot(uint16_t *ring, unsigned t, bool want, int p,
-                                                unsigned qlimit, unsigned h, int lane) {
-  unsigned k = __ballot_sync(FULL, want);
-  unsigned pos = t + __popc(k & lanemask_lt());
-  if (want && pos - h < qlimit) ring[pos & (RQ - 1)] = (uint16_t)p;
-  (void)lane;
-  return t + __popc(k);
-}
-
-// Full detection (K.193-217 restricted to the tile; halo cells are sources
-// only).  lane = column x; rows -1..34 stream through a 3-row window of
-// m (own column) and lr = min(m left, m right) (shuffles; the halo columns'
-// m is +inf).  Row 0 / 33 centres are the top / bottom halo cells; lanes 0
-// and 31 additionally test the left / right halo columns from their own m.
-// Writes the queue at [0, n) and returns n (may exceed qlimit: truncated).
-template <int CONN, typename T>
-__device__ unsigned detect_full(WarpSmem<T> &s, Lim lim, unsigned qlimit, int lane) {
+__device__ unsigned detect_full(WarpSmem<T> &s, unsigned t, unsigned qlimit, int lane) {
   const int x = lane + 1;
-  auto row = [&](int y, int &m, int &lr, int &j) {
-    if (y < 0 || y > TS + 1) {
-      m = INT_MAX;
-      lr = INT_MAX;
-      j = INT_MIN;
-      return;
-    }
+  auto mrow = [&](int y, int &m, int &j) {
     int i = sidx(x, y);
     j = s.J[i];
-    m = (interior(lim, x, y) && j < (int)s.I[i]) ? j : INT_MAX;
-    int l = __shfl_up_sync(FULL, m, 1), r = __shfl_down_sync(FULL, m, 1);
-    if (lane == 0) l = INT_MAX;   // column 0 is halo
-    if (lane == 31) r = INT_MAX;  // column 33 is halo
-    lr = min(l, r);
+    m = j < (int)s.I[i] ? j : INT_MAX;
   };
-  unsigned t = 0;
-  int m_p, lr_p, jd, m_c, lr_c, j_c;
-  row(-1, m_p, lr_p, jd);
-  row(0, m_c, lr_c, j_c);
-  for (int y = 0; y <= TS + 1; y++) {
-    int m_n, lr_n, j_n;
-    row(y + 1, m_n, lr_n, j_n);
-    int lo = CONN == 8 ? min(min(min(m_p, lr_p), min(m_c, lr_c)), min(m_n, lr_n))
-                       : min(min(lr_c, m_p), m_n);
-    // halo rows (y = 0, TS+1) are sources even though not interior
-    bool ok = (y == 0 || y == TS + 1) ? true : interior(lim, x, y);
-    t = push_ballot(s.ring, t, ok && j_c > lo, sidx(x, y), qlimit, 0, lane);
-    // left / right halo columns, rows 0..TS+1 (corners included)
-    bool side = false;
-    int ps = 0;
-    if (lane == 0 || lane == 31) {
-      int hx = lane == 0 ? 0 : TS + 1;
-      int lo2 = CONN == 8 ? min(min(m_p, m_c), m_n) : m_c;
-      side = s.J[sidx(hx, y)] > lo2;
-      ps = sidx(hx, y);
-    }
-    t = push_ballot(s.ring, t, side, ps, qlimit, 0, lane);
+  int m_p = INT_MAX, lr_p = INT_MAX, m_c, lr_c, j_c, jd;
+  mrow(0, m_c, jd);  // row 0 is halo: m = +inf
+  lr_c = lr_of(m_c, lane);
+  m_p = m_c;
+  lr_p = lr_c;
+  mrow(1, m_c, j_c);
+  lr_c = lr_of(m_c, lane);
+  for (int y = 1; y <= TS; y++) {
+    int m_n, j_n;
+    mrow(y + 1, m_n, j_n);
+    int lr_n = lr_of(m_n, lane);
+    t = push_ballot(s.ring, t, j_c > window_lo<CONN>(m_n, lr_n, m_c, lr_c, m_p, lr_p),
+                    sidx(x, y), qlimit);
     m_p = m_c;
     lr_p = lr_c;
     m_c = m_n;
@@ -367,45 +385,20 @@ __device__ unsigned detect_full(WarpSmem<T> &s, Lim lim, unsigned qlimit, int la
 }
 
 // One sweep pass whose last walk (columns S->N, lane = column) also does the
-// full detection: after the walk finalises row y, rows y..y+2 are final, so
-// the centre row y+1 is evaluated one step behind the walk (same 3-row
-// window as detect_full, no second pass over the tile).  Returns whether
-// the sweep changed anything; *n = cells queued (may exceed qlimit).
+// detection: once the walk has finalised row y, rows y..y+2 are final, so
+// the centre row y+1 is evaluated one step behind the walk.
 template <int CONN, typename T>
-__device__ bool sweep_detect(WarpSmem<T> &s, Lim lim, unsigned qlimit, int lane, unsigned &n) {
+__device__ bool sweep_detect(WarpSmem<T> &s, unsigned &t, unsigned qlimit, int lane) {
   const int k = lane + 1, x = k;
   bool chg = walk_line<1>(s, sidx(1, k), sidx(0, k));
   chg |= walk_line<-1>(s, sidx(TS, k), sidx(TS + 1, k));
   __syncwarp();
   chg |= walk_line<PS>(s, sidx(k, 1), sidx(k, 0));
   __syncwarp();
-  // S -> N with the detection window: rows (y, y+1, y+2) = (n_, c_, p_)
-  unsigned t = 0;
   int v = s.J[sidx(x, TS + 1)];
-  int m_c = INT_MAX, lr_c = INT_MAX, j_c = v;              // row TS+1 (bottom halo)
-  int m_p = INT_MAX, lr_p = INT_MAX;                       // row TS+2 (beyond)
-  auto centre = [&](int c, int m_n, int lr_n) {
-    // evaluate centre row c with rows c-1 (n), c (c), c+1 (p)
-    int lo = CONN == 8 ? min(min(min(m_p, lr_p), min(m_c, lr_c)), min(m_n, lr_n))
-                       : min(min(lr_c, m_p), m_n);
-    bool ok = (c == 0 || c == TS + 1) ? true : interior(lim, x, c);
-    t = push_ballot(s.ring, t, ok && j_c > lo, sidx(x, c), qlimit, 0, lane);
-    bool side = false;
-    int ps = 0;
-    if (lane == 0 || lane == 31) {
-      int hx = lane == 0 ? 0 : TS + 1;
-      int lo2 = CONN == 8 ? min(min(m_p, m_c), m_n) : m_c;
-      side = s.J[sidx(hx, c)] > lo2;
-      ps = sidx(hx, c);
-    }
-    t = push_ballot(s.ring, t, side, ps, qlimit, 0, lane);
-  };
-  auto lr_of = [&](int m) {
-    int l = __shfl_up_sync(FULL, m, 1), r = __shfl_down_sync(FULL, m, 1);
-    if (lane == 0) l = INT_MAX;
-    if (lane == 31) r = INT_MAX;
-    return min(l, r);
-  };
+  // window (n, c, p) = rows (y, y+1, y+2); start with c = row TS+1 (halo),
+  // p = beyond: both +inf
+  int m_c = INT_MAX, lr_c = INT_MAX, j_c = 0, m_p = INT_MAX, lr_p = INT_MAX;
   constexpr int C = 8;
 #pragma unroll
   for (int k0 = 0; k0 < TS; k0 += C) {
@@ -422,9 +415,11 @@ __device__ bool sweep_detect(WarpSmem<T> &s, Lim lim, unsigned qlimit, int lane,
       chg |= nv != j[c];
       s.J[sidx(x, y)] = nv;
       v = nv;
-      int m_n = (interior(lim, x, y) && nv < mm[c]) ? nv : INT_MAX;
-      int lr_n = lr_of(m_n);
-      centre(y + 1, m_n, lr_n);  // rows y..y+2 are final now
+      int m_n = nv < mm[c] ? nv : INT_MAX;
+      int lr_n = lr_of(m_n, lane);
+      if (y + 1 <= TS)  // centre y+1 (rows y..y+2 final)
+        t = push_ballot(s.ring, t, j_c > window_lo<CONN>(m_n, lr_n, m_c, lr_c, m_p, lr_p),
+                        sidx(x, y + 1), qlimit);
       m_p = m_c;
       lr_p = lr_c;
       m_c = m_n;
@@ -432,77 +427,52 @@ __device__ bool sweep_detect(WarpSmem<T> &s, Lim lim, unsigned qlimit, int lane,
       j_c = nv;
     }
   }
-  // centre row 1: rows 0 (top halo, m = +inf), 1, 2
-  centre(1, INT_MAX, INT_MAX);
-  // centre row 0 (top halo): rows -1 (beyond), 0, 1
-  m_p = m_c;
-  lr_p = lr_c;
-  m_c = INT_MAX;
-  lr_c = INT_MAX;
-  j_c = s.J[sidx(x, 0)];
-  centre(0, INT_MAX, INT_MAX);
-  n = t;
+  // centre row 1: rows 0 (halo: +inf), 1, 2
+  t = push_ballot(s.ring, t, j_c > window_lo<CONN>(INT_MAX, INT_MAX, m_c, lr_c, m_p, lr_p),
+                  sidx(x, 1), qlimit);
   return __any_sync(FULL, chg);
-}
-
-// Halo-only detection for a re-visit: the interior is already stable with
-// respect to itself, so only halo cells can be new sources.
-template <int CONN, typename T>
-__device__ unsigned detect_halo(WarpSmem<T> &s, Lim lim, unsigned qlimit, int lane) {
-  unsigned t = 0;
-  for (int h0 = 0; h0 < RING; h0 += 32) {
-    int h = h0 + lane;
-    bool want = false;
-    int p = 0;
-    if (h < RING) {
-      int lx, ly;
-      halo_cell(h, lx, ly);
-      p = sidx(lx, ly);
-      want = can_raise<CONN>(s, lim, lx, ly);
-    }
-    t = push_ballot(s.ring, t, want, p, qlimit, 0, lane);
-  }
-  return t;
 }
 
 // --- propagation to the tile's fixed point ---------------------------------------
 //
-// The warp drains its ring 32 items per step.  Items are popped (their
-// in-queue bit cleared), __syncwarp, then each lane offers its cell's
-// value to its in-tile neighbours with shared atomicMax; a neighbour it
-// raised and whose bit was clear is pushed (bit set).  __syncwarp orders
-// one step's merges before the next step's reads.
+// The warp drains its ring 32 items per step.  Items are interior cells, so
+// all 8 (4) neighbours lie in the padded tile: no bounds checks.  Each lane
+// loads its neighbours, then issues its predicated atomicMax offers back to
+// back; a neighbour it raised is pushed.  __syncwarp orders one step's
+// merges before the next step's reads.
 template <int CONN, typename T>
-__device__ void tile_fixpoint(WarpSmem<T> &s, Lim lim, unsigned qlimit, bool full, int sweeps,
+__device__ void tile_fixpoint(WarpSmem<T> &s, unsigned qlimit, bool full, int sweeps,
                               unsigned halo_thresh, int lane, bool &changed,
                               unsigned long long &pushes, unsigned long long &overflows,
                               unsigned long long &seeds, unsigned long long *ph) {
   const bool l0 = lane == 0;
   unsigned h = 0, t = 0;
-  bool rescan = true, pending = false, swept = false;
+  bool rescan = true, pending = false, swept = false, offered = false;
   for (;;) {
     if (rescan) {
       long long d0 = l0 ? clock64() : 0;
-      for (int w = lane; w < BITW; w += 32) s.bits[w] = 0;
-      unsigned n;
+      unsigned n = 0;
+      if (!offered) {  // halo -> border offers, once per activation
+        offered = true;
+        unsigned raised = halo_offers<CONN>(s, lane);
+        changed |= __any_sync(FULL, raised != 0);
+        if (!full) {
+          n = queue_halo_raised(s.ring, 0, raised, qlimit, lane);
+          if (sweeps > 0 && n > halo_thresh) full = true;  // a wide front: sweep it in
+        }
+      }
       if (full && !swept && sweeps > 0) {
-        // sweeps, the last one with the detection fused into its final walk
         swept = true;
+        n = 0;
         for (int sp = 1; sp < sweeps; sp++) changed |= sweep_pass(s, lane);
-        changed |= sweep_detect<CONN>(s, lim, qlimit, lane, n);
-        __syncwarp();
+        changed |= sweep_detect<CONN>(s, n, qlimit, lane);
         if (l0) ph[2] += clock64() - d0;
-      } else {
-        swept = swept || full;
-        __syncwarp();
-        n = full ? detect_full<CONN>(s, lim, qlimit, lane) : detect_halo<CONN>(s, lim, qlimit, lane);
-        __syncwarp();
+      } else if (full) {
+        swept = true;
+        n = detect_full<CONN>(s, 0, qlimit, lane);
         if (l0) ph[3] += clock64() - d0;
       }
-      if (!full && sweeps > 0 && n > halo_thresh) {
-        full = true;  // a wide front entered: sweep it in, then detect everywhere
-        continue;
-      }
+      __syncwarp();
       full = true;  // later rescans (overflow recovery) are always full
       rescan = false;
       pending = n > qlimit;
@@ -511,75 +481,45 @@ __device__ void tile_fixpoint(WarpSmem<T> &s, Lim lim, unsigned qlimit, bool ful
         seeds += n;
         if (pending) overflows++;
       }
-      // mark the queued seeds
-      for (unsigned i = lane; i < n; i += 32) {
-        int p = s.ring[i];
-        atomicOr(&s.bits[p >> 5], 1u << (p & 31));
-      }
-      __syncwarp();
       h = 0;
       t = n;
       if (n == 0) break;
     }
     // one step: up to 32 items
-    unsigned b = min(t - h, 32u);
-    int p = 0, px = 0, py = 0;
-    if ((unsigned)lane < b) {
-      p = s.ring[(h + lane) & (RQ - 1)];
-      atomicAnd(&s.bits[p >> 5], ~(1u << (p & 31)));
+    const unsigned b = min(t - h, 32u);
+    const bool act = (unsigned)lane < b;
+    const int p = act ? s.ring[(h + lane) & (RQ - 1)] : sidx(1, 1);
+    const int v = act ? s.J[p] : INT_MIN;
+    int nv[Nbr<CONN>::N];
+    unsigned cand = 0;
+#pragma unroll
+    for (int k = 0; k < Nbr<CONN>::N; k++) {
+      int qq = p + noff<CONN>(k);
+      int vq = s.J[qq], iq = (int)s.I[qq];
+      nv[k] = min(v, iq);
+      if (vq < v && vq < iq) cand |= 1u << k;
     }
-    __syncwarp();
-    // Branch-free neighbour offers: all loads, then all (predicated)
-    // atomics back to back, so their latencies overlap.
     unsigned mask = 0;
-    bool raised = false;
-    {
-      const bool act = (unsigned)lane < b;
-      py = p / PS;
-      px = p - py * PS;
-      const int v = act ? s.J[p] : INT_MIN;
-      int nv[Nbr<CONN>::N];
-      unsigned cand = 0;
 #pragma unroll
-      for (int k = 0; k < Nbr<CONN>::N; k++) {
-        int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
-        bool in = act && interior(lim, qx, qy);
-        int qq = in ? sidx(qx, qy) : 0;
-        int vq = s.J[qq];
-        int iq = (int)s.I[qq];
-        nv[k] = v < iq ? v : iq;
-        if (in && vq < v && vq < iq) cand |= 1u << k;
-      }
-      unsigned up = 0;
-#pragma unroll
-      for (int k = 0; k < Nbr<CONN>::N; k++) {
-        int qq = sidx(px + Nbr<CONN>::dx(k), py + Nbr<CONN>::dy(k));
-        int old = smem_atomic_max_if(&s.J[qq], nv[k], (cand >> k) & 1u);
-        if (old < nv[k]) up |= 1u << k;  // predicated-off lanes return INT_MAX
-      }
-      raised = up != 0;
-#pragma unroll
-      for (int k = 0; k < Nbr<CONN>::N; k++) {
-        int qq = sidx(px + Nbr<CONN>::dx(k), py + Nbr<CONN>::dy(k));
-        unsigned bb = 1u << (qq & 31);
-        unsigned old = smem_atomic_or_if(&s.bits[qq >> 5], bb, (up >> k) & 1u);
-        if (((up >> k) & 1u) && !(old & bb)) mask |= 1u << k;  // not yet queued
-      }
+    for (int k = 0; k < Nbr<CONN>::N; k++) {
+      int old = smem_atomic_max_if(&s.J[p + noff<CONN>(k)], nv[k], (cand >> k) & 1u);
+      if (old < nv[k]) mask |= 1u << k;  // predicated-off lanes return INT_MAX
     }
-    changed |= __any_sync(FULL, raised);
+    changed |= __any_sync(FULL, mask != 0);
     // placement: exclusive prefix of the per-lane counts from bit-plane ballots
-    unsigned c = __popc(mask);
-    unsigned b0 = __ballot_sync(FULL, c & 1u), b1 = __ballot_sync(FULL, c & 2u);
-    unsigned b2 = __ballot_sync(FULL, c & 4u), b3 = __ballot_sync(FULL, c & 8u);
-    unsigned lt = lanemask_lt();
-    unsigned pre = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt) + 8 * __popc(b3 & lt);
-    unsigned tot = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2) + 8 * __popc(b3);
-    unsigned hb = h + b, pos = t + pre;
+    const unsigned c = __popc(mask);
+    const unsigned b0 = __ballot_sync(FULL, c & 1u), b1 = __ballot_sync(FULL, c & 2u);
+    const unsigned b2 = __ballot_sync(FULL, c & 4u), b3 = __ballot_sync(FULL, c & 8u);
+    const unsigned lt = lanemask_lt();
+    const unsigned pre =
+        __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt) + 8 * __popc(b3 & lt);
+    const unsigned tot = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2) + 8 * __popc(b3);
+    const unsigned hb = h + b;
+    unsigned pos = t + pre;
     while (mask) {
       int k = __ffs(mask) - 1;
       mask &= mask - 1;
-      if (pos - hb < qlimit)
-        s.ring[pos & (RQ - 1)] = (uint16_t)sidx(px + Nbr<CONN>::dx(k), py + Nbr<CONN>::dy(k));
+      if (pos - hb < qlimit) s.ring[pos & (RQ - 1)] = (uint16_t)(p + noff<CONN>(k));
       pos++;
     }
     if (l0) pushes += tot;
@@ -601,8 +541,8 @@ __device__ void tile_fixpoint(WarpSmem<T> &s, Lim lim, unsigned qlimit, bool ful
 // --- the persistent kernel ------------------------------------------------------
 
 template <typename T, int CONN>
-__global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) tile_engine_kernel(EngineArgs a,
-                                                                  unsigned long long *counters) {
+__global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
+    tile_engine_kernel(EngineArgs a, unsigned long long *counters) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpSmem<T> &s = reinterpret_cast<WarpSmem<T> *>(smem_raw)[warp];
@@ -628,7 +568,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) tile_engine_kernel
     bool full = __shfl_sync(FULL, first, 0) != 0;
     const int tx = t % a.ntx, ty = t / a.ntx;
     const int x0 = tx * TS, y0 = ty * TS;
-    const Lim lim{min(TS, a.W - x0), min(TS, a.H - y0)};
+    const int limx = min(TS, a.W - x0), limy = min(TS, a.H - y0);
     long long c_load = l0 ? clock64() : 0;
     if (l0) ph[0] += c_load - c_pop;
 
@@ -639,6 +579,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) tile_engine_kernel
       ring_cell(r, lx, ly);
       s.ring0[r] = s.J[sidx(lx, ly)];
     }
+    __syncwarp();
     if (l0) ph[1] += clock64() - c_load;
     bool rerun = false;
     for (;;) {  // re-run while neighbours request it
@@ -647,7 +588,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) tile_engine_kernel
       long long c_fix = l0 ? clock64() : 0;
       unsigned long long sd0 = ph[2] + ph[3];
       bool changed = false;
-      tile_fixpoint<CONN>(s, lim, a.qlimit, full, a.sweeps, a.halo_thresh, lane, changed, n_push,
+      tile_fixpoint<CONN>(s, a.qlimit, full, a.sweeps, a.halo_thresh, lane, changed, n_push,
                           n_over, n_seeds, ph);
       full = false;
       changed = __any_sync(FULL, changed);
@@ -655,15 +596,15 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) tile_engine_kernel
       if (l0) ph[4] += (c_st - c_fix) - (ph[2] + ph[3] - sd0);
       if (changed) {
         __syncwarp();
-        store_tile<T>(a, s, x0, y0, lim, lane);
-        // which neighbour tiles can the changed border still raise?
-        // Per side, lane = position along it: cv = the border cell's value
-        // if it changed since last published (else -inf); a halo cell needs
-        // its tile re-run iff it can still be raised (J < I) by the max cv
-        // of its interior neighbours (lanes l-1..l+1 for 8-conn).
+        store_tile<T>(a, s, x0, y0, limx, limy, lane);
+        // Which neighbour tiles can the changed border still raise?  Per
+        // side, lane = position along it: cv = the border cell's value if it
+        // changed since last published (else -inf); a halo cell needs its
+        // tile re-run iff it can still be raised (J < real I) by the max cv
+        // of its interior neighbours (lanes l-1..l+1 for 8-conn).  Cells
+        // outside the image hold J = I = min(T): never "need".
         const int k = lane + 1;
         auto cv_of = [&](int bx, int by) -> int {
-          if (!interior(lim, bx, by)) return INT_MIN;
           int vb = s.J[sidx(bx, by)];
           return vb != s.ring0[ring_index(bx, by)] ? vb : INT_MIN;
         };
@@ -674,22 +615,22 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks) tile_engine_kernel
           if (lane == 31) d = INT_MIN;
           return max(c, max(u, d));
         };
-        auto need_h = [&](int hx, int hy, int c) -> bool {
-          int gx = x0 + hx - 1, gy = y0 + hy - 1;
-          if (gx < 0 || gx >= a.W || gy < 0 || gy >= a.H) return false;  // outside the image
+        auto need_h = [&](int hx, int hy, int hidx, int c) -> bool {
           int vh = s.J[sidx(hx, hy)];
-          return vh < (int)s.I[sidx(hx, hy)] && vh < c;
+          return vh < (int)s.Ih[hidx] && vh < c;
         };
         const int ct = cv_of(k, 1), cb = cv_of(k, TS), cl = cv_of(1, k), cr = cv_of(TS, k);
         const int nt = nb3(ct), nbm = nb3(cb), nl = nb3(cl), nr = nb3(cr);
         unsigned dirs = 0;
-        if (__any_sync(FULL, need_h(k, 0, nt))) dirs |= 1u << 1;        // N
-        if (__any_sync(FULL, need_h(k, TS + 1, nbm))) dirs |= 1u << 7;  // S
-        if (__any_sync(FULL, need_h(0, k, nl))) dirs |= 1u << 3;        // W
-        if (__any_sync(FULL, need_h(TS + 1, k, nr))) dirs |= 1u << 5;   // E
+        if (__any_sync(FULL, need_h(k, 0, k, nt))) dirs |= 1u << 1;                     // N
+        if (__any_sync(FULL, need_h(k, TS + 1, PW + k, nbm))) dirs |= 1u << 7;          // S
+        if (__any_sync(FULL, need_h(0, k, 2 * PW + k - 1, nl))) dirs |= 1u << 3;        // W
+        if (__any_sync(FULL, need_h(TS + 1, k, 2 * PW + TS + k - 1, nr))) dirs |= 1u << 5;  // E
         if (CONN == 8) {  // corners touch one interior cell each
-          bool c0 = lane == 0 && need_h(0, 0, ct), c2 = lane == 31 && need_h(TS + 1, 0, ct);
-          bool c6 = lane == 0 && need_h(0, TS + 1, cb), c8 = lane == 31 && need_h(TS + 1, TS + 1, cb);
+          bool c0 = lane == 0 && need_h(0, 0, 0, ct);
+          bool c2 = lane == 31 && need_h(TS + 1, 0, TS + 1, ct);
+          bool c6 = lane == 0 && need_h(0, TS + 1, PW, cb);
+          bool c8 = lane == 31 && need_h(TS + 1, TS + 1, PW + TS + 1, cb);
           if (__any_sync(FULL, c0)) dirs |= 1u << 0;
           if (__any_sync(FULL, c2)) dirs |= 1u << 2;
           if (__any_sync(FULL, c6)) dirs |= 1u << 6;
