@@ -132,9 +132,10 @@ int iwpp_check_le(const void *J, const void *I, int64_t n, int dtype,
 /* Row sweeps forward+backward (K.115-139, exact clamp-composition scan). */
 int iwpp_recon_sweep_rows(void *J, const void *I, int64_t W, int64_t H, int dtype,
                           void *stream);
-/* Column sweeps forward+backward (K.142-190, vertical part exact). */
+/* Column sweeps forward+backward (K.142-190, vertical part exact; segment
+ * composites + carry scan + apply).  workspace: iwpp_recon_workspace_bytes. */
 int iwpp_recon_sweep_cols(void *J, const void *I, int64_t W, int64_t H, int dtype,
-                          void *stream);
+                          void *workspace, void *stream);
 /* Full-neighbourhood seed scan (K.193-217): writes active pixels (packed
  * y*W+x, int64, raster order NOT guaranteed) to out; *n_host = count. */
 int iwpp_recon_seed_scan(const void *J, const void *I, int64_t W, int64_t H,

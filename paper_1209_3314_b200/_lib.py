@@ -82,7 +82,7 @@ def load_library(path: str = LIB_PATH):
             "iwpp_recon_engine_counters": ([P, I64, I64, ctypes.POINTER(ctypes.c_uint64), I, P], I),
             "iwpp_check_le": ([P, P, I64, I, P, ctypes.POINTER(I64), P], I),
             "iwpp_recon_sweep_rows": ([P, P, I64, I64, I, P], I),
-            "iwpp_recon_sweep_cols": ([P, P, I64, I64, I, P], I),
+            "iwpp_recon_sweep_cols": ([P, P, I64, I64, I, P, P], I),
             "iwpp_recon_seed_scan": ([P, P, I64, I64, I, I, P, ctypes.POINTER(I64), P, P], I),
             "iwpp_edt_workspace_bytes": ([I64, I64, I], SZ),
             "iwpp_edt": ([P, I64, I64, I, P, P, P, SZ, I64, SP, P], I),

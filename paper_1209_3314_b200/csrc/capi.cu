@@ -57,16 +57,18 @@ static int check_dims(int64_t W, int64_t H) {
   return IWPP_OK;
 }
 
-// recon workspace: tile queue + counters + seed-scan counter
+// recon workspace: tile queue + counters + column-sweep scratch
 struct ReconWs {
   recon::TileQueue q;
   unsigned long long *counters;
+  void *col_scratch;
 };
 
 static ReconWs carve_recon(Carver &c, int64_t W, int64_t H) {
   ReconWs w;
   w.q = recon::carve_tile_queue(c, recon::num_tiles(W, H));
   w.counters = c.take<unsigned long long>(recon::CNT_N);
+  w.col_scratch = c.take<char>(recon::col_scratch_bytes(W, H));
   return w;
 }
 
@@ -133,7 +135,7 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
   if (sweeps < 0) sweeps = 0;  // auto: the tile engine alone (measured best on random inputs)
   for (int s = 0; s < sweeps; s++) {
     if ((rc = recon::sweep_rows(J, I, (int)W, (int)H, dtype, st))) return rc;
-    if ((rc = recon::sweep_cols(J, I, (int)W, (int)H, dtype, st))) return rc;
+    if ((rc = recon::sweep_cols(J, I, (int)W, (int)H, dtype, w.col_scratch, st))) return rc;
   }
   recon::EngineOpts eo;
   if (opts) {
@@ -246,10 +248,13 @@ int iwpp_recon_sweep_rows(void *J, const void *I, int64_t W, int64_t H, int dtyp
   return recon::sweep_rows(J, I, (int)W, (int)H, dtype, (cudaStream_t)stream);
 }
 
-int iwpp_recon_sweep_cols(void *J, const void *I, int64_t W, int64_t H, int dtype, void *stream) {
+int iwpp_recon_sweep_cols(void *J, const void *I, int64_t W, int64_t H, int dtype, void *workspace,
+                          void *stream) {
   int rc = check_dims(W, H);
   if (rc) return rc;
-  return recon::sweep_cols(J, I, (int)W, (int)H, dtype, (cudaStream_t)stream);
+  Carver c(workspace);
+  ReconWs w = carve_recon(c, W, H);
+  return recon::sweep_cols(J, I, (int)W, (int)H, dtype, w.col_scratch, (cudaStream_t)stream);
 }
 
 int iwpp_recon_seed_scan(const void *J, const void *I, int64_t W, int64_t H, int dtype, int conn,

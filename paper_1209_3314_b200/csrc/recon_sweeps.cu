@@ -157,27 +157,88 @@ __global__ void __launch_bounds__(256) row_sweep_kernel(T *__restrict__ J, const
   }
 }
 
-// Column sweeps, vertical neighbour only (K.142-190 with the diagonal terms
-// left to the tile engine): per column the same clamp recurrence.  A warp
-// covers 32 columns; rows are split in chunks chained through a decoupled
-// per-column carry (simple, exact along full columns).
-template <typename T>
-__global__ void __launch_bounds__(256) col_sweep_kernel(T *__restrict__ J, const T *__restrict__ I,
-                                                        int W, int H) {
+// Column sweeps, vertical neighbour (K.142-190; the diagonal terms are left
+// to the tile engine): per column the same clamp recurrence, computed
+// exactly along full columns in three bandwidth-bound passes:
+//   A. per (column, 64-row segment): the composite clamp (l, h) of the segment
+//   B. per column: exclusive scan of the segment composites -> carry-in
+//   C. per (column, segment): re-walk the segment from its carry-in
+// Thread = one column, warp = 32 consecutive columns (coalesced rows).
+constexpr int kColSeg = 64;
+
+template <typename T, bool DOWN>
+__global__ void __launch_bounds__(128) col_composite_kernel(const T *__restrict__ J,
+                                                            const T *__restrict__ I, int W, int H,
+                                                            int2 *__restrict__ comp) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, seg = blockIdx.y;
+  if (x >= W) return;
+  int y0 = seg * kColSeg, y1 = min(H, y0 + kColSeg);
+  int l = INT_MIN, h = INT_MAX;  // identity
+#pragma unroll 8
+  for (int k = 0; k < y1 - y0; k++) {
+    int y = DOWN ? y0 + k : y1 - 1 - k;
+    size_t g = (size_t)y * W + x;
+    int j = (int)__ldcg(J + g), m = (int)__ldg(I + g);
+    l = clampi(l, j, m);  // f_y o (running composite)
+    h = clampi(h, j, m);
+  }
+  comp[(size_t)seg * W + x] = make_int2(l, h);
+}
+
+template <bool DOWN>
+__global__ void __launch_bounds__(128) col_carry_kernel(const int2 *__restrict__ comp, int W,
+                                                        int nseg, int *__restrict__ carry) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= W) return;
   int v = INT_MIN;
-  for (int y = 0; y < H; y++) {
-    size_t g = (size_t)y * W + x;
-    v = clampi(v, (int)J[g], (int)__ldg(I + g));
-    J[g] = (T)v;
+  for (int k = 0; k < nseg; k++) {
+    int seg = DOWN ? k : nseg - 1 - k;
+    carry[(size_t)seg * W + x] = v;
+    int2 c = comp[(size_t)seg * W + x];
+    v = clampi(v, c.x, c.y);
   }
-  v = INT_MIN;
-  for (int y = H - 1; y >= 0; y--) {
+}
+
+template <typename T, bool DOWN>
+__global__ void __launch_bounds__(128) col_apply_kernel(T *__restrict__ J, const T *__restrict__ I,
+                                                        int W, int H,
+                                                        const int *__restrict__ carry) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, seg = blockIdx.y;
+  if (x >= W) return;
+  int y0 = seg * kColSeg, y1 = min(H, y0 + kColSeg);
+  int v = carry[(size_t)seg * W + x];
+#pragma unroll 8
+  for (int k = 0; k < y1 - y0; k++) {
+    int y = DOWN ? y0 + k : y1 - 1 - k;
     size_t g = (size_t)y * W + x;
-    v = clampi(v, (int)J[g], (int)__ldg(I + g));
-    J[g] = (T)v;
+    int j = (int)J[g];
+    v = clampi(v, j, (int)__ldg(I + g));
+    if (v != j) J[g] = (T)v;
   }
+}
+
+size_t col_scratch_bytes(int64_t W, int64_t H) {
+  size_t nseg = (size_t)((H + kColSeg - 1) / kColSeg);
+  return align_up(nseg * W * sizeof(int2), 256) + align_up(nseg * W * sizeof(int), 256);
+}
+
+template <typename T>
+static int cols_impl(void *Jv, const void *Iv, int W, int H, void *scratch, cudaStream_t st) {
+  T *J = (T *)Jv;
+  const T *I = (const T *)Iv;
+  int nseg = (H + kColSeg - 1) / kColSeg;
+  Carver c(scratch);
+  int2 *comp = c.take<int2>((size_t)nseg * W);
+  int *carry = c.take<int>((size_t)nseg * W);
+  dim3 g2((W + 127) / 128, nseg), g1((W + 127) / 128);
+  col_composite_kernel<T, true><<<g2, 128, 0, st>>>(J, I, W, H, comp);
+  col_carry_kernel<true><<<g1, 128, 0, st>>>(comp, W, nseg, carry);
+  col_apply_kernel<T, true><<<g2, 128, 0, st>>>(J, I, W, H, carry);
+  col_composite_kernel<T, false><<<g2, 128, 0, st>>>(J, I, W, H, comp);
+  col_carry_kernel<false><<<g1, 128, 0, st>>>(comp, W, nseg, carry);
+  col_apply_kernel<T, false><<<g2, 128, 0, st>>>(J, I, W, H, carry);
+  IWPP_CUDA_TRY(cudaGetLastError());
+  return IWPP_OK;
 }
 
 template <typename T, int CONN>
@@ -264,16 +325,13 @@ int sweep_rows(void *J, const void *I, int W, int H, int dtype, cudaStream_t st)
   return set_error(IWPP_E_CONTRACT, "unsupported dtype %d", dtype);
 }
 
-int sweep_cols(void *J, const void *I, int W, int H, int dtype, cudaStream_t st) {
-  int blocks = (W + 255) / 256;
+int sweep_cols(void *J, const void *I, int W, int H, int dtype, void *scratch, cudaStream_t st) {
   switch (dtype) {
-    case IWPP_U8: col_sweep_kernel<uint8_t><<<blocks, 256, 0, st>>>((uint8_t *)J, (const uint8_t *)I, W, H); break;
-    case IWPP_U16: col_sweep_kernel<uint16_t><<<blocks, 256, 0, st>>>((uint16_t *)J, (const uint16_t *)I, W, H); break;
-    case IWPP_I32: col_sweep_kernel<int32_t><<<blocks, 256, 0, st>>>((int32_t *)J, (const int32_t *)I, W, H); break;
-    default: return set_error(IWPP_E_CONTRACT, "unsupported dtype %d", dtype);
+    case IWPP_U8: return cols_impl<uint8_t>(J, I, W, H, scratch, st);
+    case IWPP_U16: return cols_impl<uint16_t>(J, I, W, H, scratch, st);
+    case IWPP_I32: return cols_impl<int32_t>(J, I, W, H, scratch, st);
   }
-  IWPP_CUDA_TRY(cudaGetLastError());
-  return IWPP_OK;
+  return set_error(IWPP_E_CONTRACT, "unsupported dtype %d", dtype);
 }
 
 int seed_scan(const void *J, const void *I, int W, int H, int dtype, int conn, int64_t *out,

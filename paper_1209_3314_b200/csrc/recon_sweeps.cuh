@@ -6,7 +6,9 @@ namespace iwpp {
 namespace recon {
 
 int sweep_rows(void *J, const void *I, int W, int H, int dtype, cudaStream_t st);
-int sweep_cols(void *J, const void *I, int W, int H, int dtype, cudaStream_t st);
+// scratch: col_scratch_bytes(W, H) bytes of device memory
+int sweep_cols(void *J, const void *I, int W, int H, int dtype, void *scratch, cudaStream_t st);
+size_t col_scratch_bytes(int64_t W, int64_t H);
 int seed_scan(const void *J, const void *I, int W, int H, int dtype, int conn, int64_t *out,
               unsigned long long *n_out, cudaStream_t st);
 int check_le(const void *J, const void *I, size_t n, int dtype, unsigned long long *viol,

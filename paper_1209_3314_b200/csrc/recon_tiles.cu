@@ -148,12 +148,15 @@ __device__ __forceinline__ int ring_pop(const TileQueue &q) {
 //   pop      : old = atomicExch(R) + fence (acquire: sees every border write
 //              made before a request that found Q already set)
 //   finish   : CAS(R -> 0); failure means Q was set meanwhile -> re-run
-__device__ __forceinline__ void activate(const TileQueue &q, unsigned t) {
+// Returns true when the caller now owns an idle tile's activation (it must
+// either push it or process it itself); pending already counts it.
+__device__ __forceinline__ bool activate_claim(const TileQueue &q, unsigned t) {
   unsigned old = atomicOr(&q.state[t], ST_Q);
   if (old == 0) {
     atomicAdd(q.pending, 1u);
-    ring_push(q, t);
+    return true;
   }
+  return false;
 }
 
 // --- loads / stores (warp) -----------------------------------------------------
@@ -551,12 +554,13 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
   unsigned long long n_tiles = 0, n_reruns = 0, n_push = 0, n_over = 0, n_seeds = 0;
   unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
 
+  int next_tile = -1;  // a claimed neighbour this warp continues with
   for (;;) {
     long long c_pop = l0 ? clock64() : 0;
     int t = -1;
     unsigned first = 0;
     if (l0) {
-      t = ring_pop(a.q);
+      t = next_tile >= 0 ? next_tile : ring_pop(a.q);
       if (t >= 0) {
         unsigned old = atomicExch(&a.q.state[t], ST_R);
         __threadfence();
@@ -564,6 +568,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
       }
     }
     t = __shfl_sync(FULL, t, 0);
+    next_tile = -1;
     if (t < 0) break;
     bool full = __shfl_sync(FULL, first, 0) != 0;
     const int tx = t % a.ntx, ty = t / a.ntx;
@@ -638,11 +643,22 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
         }
         __threadfence();  // publish the interior before any neighbour is (re)queued
         __syncwarp();
-        if (lane < 9 && ((dirs >> lane) & 1u)) {  // one lane per direction
+        // one lane per direction claims the neighbour; the warp keeps one
+        // claimed idle neighbour as its own continuation (no queue round
+        // trip on a wavefront's critical path) and pushes the rest
+        bool own = false;
+        unsigned ntile = 0;
+        if (lane < 9 && ((dirs >> lane) & 1u)) {
           int ntxi = tx + (lane % 3) - 1, ntyi = ty + (lane / 3) - 1;
-          if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty)
-            activate(a.q, (unsigned)(ntyi * a.ntx + ntxi));
+          if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty) {
+            ntile = (unsigned)(ntyi * a.ntx + ntxi);
+            own = activate_claim(a.q, ntile);
+          }
         }
+        unsigned ownmask = __ballot_sync(FULL, own);
+        int keep = (ownmask && next_tile < 0) ? __ffs(ownmask) - 1 : -1;
+        if (own && lane != keep) ring_push(a.q, ntile);
+        if (keep >= 0) next_tile = __shfl_sync(FULL, (int)ntile, keep);
         for (int r = lane; r < 4 * TS; r += 32) {
           int lx, ly;
           ring_cell(r, lx, ly);

@@ -192,6 +192,29 @@ def test_row_sweep_stage_is_exact_row_recurrence(gw):
         assert np.array_equal(dJ.cpu().numpy().astype(np.int64), want), (dtype, W)
 
 
+def test_col_sweep_stage_is_exact_column_recurrence(gw):
+    """iwpp_recon_sweep_cols = K.142-190 (vertical neighbour) forward then
+    backward along full columns, exactly (segment composites + carry scan)."""
+    from paper_1209_3314_b200 import _lib
+    t = _torch()
+    L = _lib.lib()
+    for dtype, (H, W) in [(np.uint8, (1000, 37)), (np.uint8, (64, 128)), (np.int32, (333, 65)),
+                          (np.uint16, (130, 7))]:
+        J, I = oracle.gray_pair((H, W), 6, h=30 if dtype == np.uint8 else 1000, dtype=dtype)
+        want = J.astype(np.int64).copy()
+        Ii = I.astype(np.int64)
+        for y in range(1, H):
+            want[y] = np.maximum(want[y], np.minimum(want[y - 1], Ii[y]))
+        for y in range(H - 2, -1, -1):
+            want[y] = np.maximum(want[y], np.minimum(want[y + 1], Ii[y]))
+        dJ, dI = t.from_numpy(J).cuda(), t.from_numpy(I).cuda()
+        code = {np.uint8: 0, np.uint16: 1, np.int32: 2}[dtype]
+        ws = _lib.workspace(L.iwpp_recon_workspace_bytes(W, H, code, 8))
+        _lib.check(L.iwpp_recon_sweep_cols(_lib.ptr(dJ), _lib.ptr(dI), W, H, code, _lib.ptr(ws),
+                                           _lib.stream_ptr()))
+        assert np.array_equal(dJ.cpu().numpy().astype(np.int64), want), (dtype, H, W)
+
+
 def test_seed_scan_matches_oracle(gw):
     J, I = oracle.gray_pair((130, 97), 9, h=60)
     for conn in (4, 8):
