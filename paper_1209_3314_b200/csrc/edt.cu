@@ -224,35 +224,6 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_kernel(int W, int H,
 }
 
 // ---- finalize (edt.py:272-281) --------------------------------------------
-__global__ void edt_finalize_kernel(const uint32_t *__restrict__ st, int W, int H,
-                                    int64_t *__restrict__ vr, float *__restrict__ dist,
-                                    int64_t *__restrict__ d2out, unsigned long long *counters) {
-  size_t n = (size_t)W * H;
-  unsigned long long ninf = 0;
-  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
-       p += (size_t)gridDim.x * blockDim.x) {
-    uint32_t s = st[p];
-    if (s == INF32) {
-      ninf++;
-      if (vr) vr[p] = -1;
-      if (dist) dist[p] = 0.f;
-      if (d2out) d2out[p] = (int64_t)1 << 62;
-      continue;
-    }
-    int py = (int)(p / (unsigned)W), px = (int)(p - (size_t)py * W);
-    int sy = (int)(s >> 16), sx = (int)(s & 0xffffu);
-    long long dx = px - sx, dy = py - sy, d2 = dx * dx + dy * dy;
-    if (vr) vr[p] = (int64_t)sy * W + sx;
-    if (dist) dist[p] = __double2float_rn(__dsqrt_rn((double)d2));
-    if (d2out) d2out[p] = d2;
-  }
-  ninf += __shfl_xor_sync(0xffffffffu, ninf, 16);
-  ninf += __shfl_xor_sync(0xffffffffu, ninf, 8);
-  ninf += __shfl_xor_sync(0xffffffffu, ninf, 4);
-  ninf += __shfl_xor_sync(0xffffffffu, ninf, 2);
-  ninf += __shfl_xor_sync(0xffffffffu, ninf, 1);
-  if ((threadIdx.x & 31) == 0 && ninf) atomicAdd(&counters[EC_NINF], ninf);
-}
 
 // finalize directly from an int64 source map (iwpp_edt_finalize)
 __global__ void edt_finalize_vr_kernel(const int64_t *__restrict__ vr, int W, int H,
@@ -283,27 +254,231 @@ __global__ void edt_finalize_vr_kernel(const int64_t *__restrict__ vr, int W, in
   if ((threadIdx.x & 31) == 0 && ninf) atomicAdd(&counters[EC_NINF], ninf);
 }
 
-// ---- host side -------------------------------------------------------------
+// ===========================================================================
+// Key engine (default whenever every d^2 fits 32 bits, i.e. up to ~46K^2).
+//
+// Each cell holds key = (d2(cell, src) << 32) | src_yx; the reference's total
+// order (K.320-336: closer, then smaller packed index; INF loses) is then
+// the plain unsigned order of keys (INF = all ones), so an offer is one
+// 64-bit atomicMin -- no CAS loop.  Keys are double-buffered and
+// interleaved per cell (16 B: the round-start key and the key being built
+// share a sector).  Next-frontier dedupe needs no stamp array: q is pushed
+// by the one offer whose atomicMin moves the building key from >= q's
+// round-start key to < it (values only decrease), which is exactly one
+// push per changed cell.
+// ===========================================================================
 
-size_t state_bytes(int64_t W, int64_t H) {
-  size_t n = (size_t)W * H;
-  Carver c(nullptr);
-  c.take<uint32_t>(n);
-  c.take<uint32_t>(n);
-  c.take<uint32_t>(n);
-  c.take<uint32_t>(n);
-  c.take<uint32_t>(n);
-  c.take<unsigned>(8);
-  c.take<unsigned long long>(EC_N);
-  return c.off + 256;
+constexpr unsigned long long KINF = ~0ull;
+
+__device__ __forceinline__ unsigned long long make_key(int qx, int qy, uint32_t src) {
+  int sy = (int)(src >> 16), sx = (int)(src & 0xffffu);
+  unsigned dx = (unsigned)abs(qx - sx), dy = (unsigned)abs(qy - sy);
+  unsigned d2 = dx * dx + dy * dy;  // < 2^32 by key_mode_ok
+  return ((unsigned long long)d2 << 32) | src;
 }
 
-EdtState carve_state(Carver &c, int64_t W, int64_t H) {
+template <int CONN>
+__global__ void edt_init_key_kernel(const uint8_t *__restrict__ mask, int W, int H, EdtState s) {
+  const unsigned FULL = 0xffffffffu;
+  size_t n = (size_t)W * H;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t base = (size_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n;
+       base += stride) {
+    size_t p = base + (threadIdx.x & 31u);
+    bool push = false;
+    uint32_t yx = 0;
+    if (p < n) {
+      int py = (int)(p / (unsigned)W), px = (int)(p - (size_t)py * W);
+      yx = ((uint32_t)py << 16) | (uint32_t)px;
+      bool bg = mask[p] == 0;
+      unsigned long long k = bg ? (unsigned long long)yx : KINF;  // d2 = 0 for itself
+      reinterpret_cast<ulonglong2 *>(s.keys)[p] = make_ulonglong2(k, k);
+      if (bg) {
+#pragma unroll
+        for (int k8 = 0; k8 < Nbr<CONN>::N; k8++) {
+          int qx = px + Nbr<CONN>::dx(k8), qy = py + Nbr<CONN>::dy(k8);
+          if (qx >= 0 && qx < W && qy >= 0 && qy < H && mask[(size_t)qy * W + qx] != 0) push = true;
+        }
+      }
+    }
+    unsigned pos = warp_reserve(&s.cnt[0], push ? 1u : 0u, FULL);
+    if (push) s.F[0][pos] = yx;
+  }
+}
+
+__global__ void edt_import_key_kernel(const int64_t *__restrict__ vr, int W, int H, EdtState s) {
+  size_t n = (size_t)W * H;
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (size_t)gridDim.x * blockDim.x) {
+    int64_t v = vr[p];
+    unsigned long long k = KINF;
+    if (v >= (int64_t)n) {
+      atomicAdd(&s.counters[EC_BAD], 1ull);
+    } else if (v >= 0) {
+      int sy = (int)(v / W), sx = (int)(v - (int64_t)sy * W);
+      int py = (int)(p / (unsigned)W), px = (int)(p - (size_t)py * W);
+      k = make_key(px, py, ((uint32_t)sy << 16) | (uint32_t)sx);
+    }
+    reinterpret_cast<ulonglong2 *>(s.keys)[p] = make_ulonglong2(k, k);
+  }
+}
+
+// seeds as given (duplicates are harmless: they offer identical keys and
+// the transition rule pushes each changed cell once)
+__global__ void edt_seed_key_kernel(const int64_t *__restrict__ seeds, int64_t n_seeds, int W,
+                                    int H, EdtState s) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_seeds;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p = seeds[i];
+    if (p < 0 || p >= (int64_t)W * H) {
+      atomicAdd(&s.counters[EC_BAD], 1ull);
+      s.F[0][i] = 0;  // harmless stand-in (cell (0,0) offers its own key)
+      continue;
+    }
+    int py = (int)(p / W), px = (int)(p - (int64_t)py * W);
+    s.F[0][i] = ((uint32_t)py << 16) | (uint32_t)px;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.cnt[0] = (unsigned)n_seeds;
+}
+
+template <int CONN>
+__global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, int H, EdtState s,
+                                                                       long long max_rounds) {
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31u;
+  // BQ: the block's next-frontier items, spilled to the global queue (GBQ)
+  // with one reservation per block per round
+  __shared__ uint32_t bq[kEdtBq];
+  __shared__ unsigned bq_n, bq_base;
+  unsigned long long visits = 0;
+  unsigned long long *K = s.keys;
+  int r = 0;
+  for (;; r++) {
+    unsigned n = ld_acquire(&s.cnt[r % 3]);
+    if (n == 0) break;
+    if (max_rounds >= 0 && r >= max_rounds) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) s.counters[EC_LIMIT] = 1;
+      break;
+    }
+    const int kr = r & 1, kw = kr ^ 1;  // round-start keys / keys being built
+    const uint32_t *cur = s.F[r & 1];
+    uint32_t *nxt = s.F[(r + 1) & 1];
+    unsigned *ncnt = &s.cnt[(r + 1) % 3];
+    if (threadIdx.x == 0) {
+      bq_n = 0;
+      if (blockIdx.x == 0) {
+        s.cnt[(r + 2) % 3] = 0;
+        visits += n;
+      }
+    }
+    __syncthreads();
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+      unsigned i = base + lane;
+      unsigned mask = 0;
+      int px = 0, py = 0;
+      if (i < n) {
+        uint32_t pyx = __ldcg(cur + i);
+        py = (int)(pyx >> 16);
+        px = (int)(pyx & 0xffffu);
+        size_t p = (size_t)py * W + px;
+        unsigned long long kp = __ldcg(K + 2 * p + kr);
+        atomicMin(K + 2 * p + kw, kp);  // the building key lags on the frontier
+        if (kp != KINF) {
+          const uint32_t src = (uint32_t)kp;
+          unsigned long long rq[Nbr<CONN>::N], nk[Nbr<CONN>::N];
+          unsigned cand = 0;
+#pragma unroll
+          for (int k = 0; k < Nbr<CONN>::N; k++) {  // loads first (independent)
+            int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+            bool in = qx >= 0 && qx < W && qy >= 0 && qy < H;
+            rq[k] = in ? __ldcg(K + 2 * ((size_t)qy * W + qx) + kr) : 0ull;
+          }
+#pragma unroll
+          for (int k = 0; k < Nbr<CONN>::N; k++) {
+            int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+            nk[k] = make_key(qx, qy, src);
+            if (nk[k] < rq[k]) cand |= 1u << k;  // beats q's round-start key
+          }
+          // the offers, issued back to back (predicated, no branches)
+#pragma unroll
+          for (int k = 0; k < Nbr<CONN>::N; k++) {
+            int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+            unsigned on = (cand >> k) & 1u;
+            unsigned long long old =
+                gmem_atomic_min_if(K + 2 * ((size_t)qy * W + qx) + kw, nk[k], on);
+            if (on && old >= rq[k]) mask |= 1u << k;  // this offer made q change
+          }
+        }
+      }
+      unsigned c = __popc(mask);
+      unsigned pos = warp_reserve(&bq_n, c, FULL);
+      while (mask) {
+        int k = __ffs(mask) - 1;
+        mask &= mask - 1;
+        int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+        uint32_t item = ((uint32_t)qy << 16) | (uint32_t)qx;
+        if (pos < kEdtBq)
+          bq[pos] = item;
+        else
+          nxt[atomicAdd(ncnt, 1u)] = item;  // BQ full: spill directly
+        pos++;
+      }
+    }
+    __syncthreads();
+    unsigned m = min(bq_n, (unsigned)kEdtBq);
+    if (threadIdx.x == 0 && m) bq_base = atomicAdd(ncnt, m);
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < m; i += blockDim.x) nxt[bq_base + i] = bq[i];
+    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s.counters[EC_ROUNDS] = (unsigned long long)r;
+    s.counters[EC_VISITS] = visits;
+    s.counters[EC_FINAL] = (unsigned long long)(r & 1);
+  }
+}
+
+__global__ void edt_finalize_key_kernel(EdtState s, int W, int H, int64_t *vr, float *dist,
+                                        int64_t *d2) {
+  const int fb = (int)s.counters[EC_FINAL];
+  size_t n = (size_t)W * H;
+  unsigned long long ninf = 0;
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (size_t)gridDim.x * blockDim.x) {
+    unsigned long long k = __ldcg(s.keys + 2 * p + fb);
+    if (k == KINF) {
+      ninf++;
+      if (vr) vr[p] = -1;
+      if (dist) dist[p] = 0.f;
+      if (d2) d2[p] = (int64_t)1 << 62;
+      continue;
+    }
+    uint32_t src = (uint32_t)k;
+    long long dd = (long long)(k >> 32);
+    if (vr) vr[p] = (int64_t)(src >> 16) * W + (src & 0xffffu);
+    if (dist) dist[p] = __double2float_rn(__dsqrt_rn((double)dd));
+    if (d2) d2[p] = dd;
+  }
+  for (int o = 16; o; o >>= 1) ninf += __shfl_xor_sync(0xffffffffu, ninf, o);
+  if ((threadIdx.x & 31) == 0 && ninf) atomicAdd(&s.counters[EC_NINF], ninf);
+}
+
+// ---- host side -------------------------------------------------------------
+
+static EdtState carve_any(Carver &c, int64_t W, int64_t H) {
   size_t n = (size_t)W * H;
   EdtState s;
-  s.buf[0] = c.take<uint32_t>(n);
-  s.buf[1] = c.take<uint32_t>(n);
-  s.stamp = c.take<uint32_t>(n);
+  s.keymode = key_mode_ok(W, H) ? 1 : 0;
+  s.keys = nullptr;
+  s.buf[0] = s.buf[1] = s.stamp = nullptr;
+  if (s.keymode) {
+    s.keys = c.take<unsigned long long>(2 * n);
+  } else {
+    s.buf[0] = c.take<uint32_t>(n);
+    s.buf[1] = c.take<uint32_t>(n);
+    s.stamp = c.take<uint32_t>(n);
+  }
   s.F[0] = c.take<uint32_t>(n);
   s.F[1] = c.take<uint32_t>(n);
   unsigned *ctl = c.take<unsigned>(8);
@@ -312,6 +487,14 @@ EdtState carve_state(Carver &c, int64_t W, int64_t H) {
   s.counters = c.take<unsigned long long>(EC_N);
   return s;
 }
+
+size_t state_bytes(int64_t W, int64_t H) {
+  Carver c(nullptr);
+  carve_any(c, W, H);
+  return c.off + 256;
+}
+
+EdtState carve_state(Carver &c, int64_t W, int64_t H) { return carve_any(c, W, H); }
 
 static int grid_for(size_t n, int threads) {
   size_t b = (n + threads - 1) / threads;
@@ -330,10 +513,17 @@ int reset_control(const EdtState &s, cudaStream_t st) {
 int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, cudaStream_t st) {
   size_t n = (size_t)W * H;
   int g = grid_for(n, 256);
-  if (conn == 8)
-    edt_init_kernel<8><<<g, 256, 0, st>>>(mask, W, H, s);
-  else
-    edt_init_kernel<4><<<g, 256, 0, st>>>(mask, W, H, s);
+  if (s.keymode) {
+    if (conn == 8)
+      edt_init_key_kernel<8><<<g, 256, 0, st>>>(mask, W, H, s);
+    else
+      edt_init_key_kernel<4><<<g, 256, 0, st>>>(mask, W, H, s);
+  } else {
+    if (conn == 8)
+      edt_init_kernel<8><<<g, 256, 0, st>>>(mask, W, H, s);
+    else
+      edt_init_kernel<4><<<g, 256, 0, st>>>(mask, W, H, s);
+  }
   IWPP_CUDA_TRY(cudaGetLastError());
   return IWPP_OK;
 }
@@ -341,6 +531,15 @@ int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, 
 int launch_import(const int64_t *vr, const int64_t *seeds, int64_t n_seeds, int W, int H,
                   const EdtState &s, cudaStream_t st) {
   size_t n = (size_t)W * H;
+  if (s.keymode) {
+    edt_import_key_kernel<<<grid_for(n, 256), 256, 0, st>>>(vr, W, H, s);
+    IWPP_CUDA_TRY(cudaGetLastError());
+    if (n_seeds > 0) {
+      edt_seed_key_kernel<<<grid_for((size_t)n_seeds, 256), 256, 0, st>>>(seeds, n_seeds, W, H, s);
+      IWPP_CUDA_TRY(cudaGetLastError());
+    }
+    return IWPP_OK;
+  }
   edt_import_kernel<<<grid_for(n, 256), 256, 0, st>>>(vr, W, H, s);
   IWPP_CUDA_TRY(cudaGetLastError());
   if (n_seeds > 0) {
@@ -352,9 +551,11 @@ int launch_import(const int64_t *vr, const int64_t *seeds, int64_t n_seeds, int 
 
 int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_rounds,
                   cudaStream_t st) {
-  void *kern = conn == 8 ? (void *)edt_rounds_kernel<8> : (void *)edt_rounds_kernel<4>;
-  static int blocks_cache[2] = {0, 0};
-  int &blocks = blocks_cache[conn == 8];
+  void *kern = s.keymode ? (conn == 8 ? (void *)edt_rounds_key_kernel<8>
+                                      : (void *)edt_rounds_key_kernel<4>)
+                         : (conn == 8 ? (void *)edt_rounds_kernel<8> : (void *)edt_rounds_kernel<4>);
+  static int blocks_cache[4] = {0, 0, 0, 0};
+  int &blocks = blocks_cache[(conn == 8) + 2 * s.keymode];
   if (blocks == 0) {
     int per_sm = 0;
     IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRoundThreads, 0));
@@ -366,15 +567,6 @@ int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_round
   EdtState ss = s;
   void *args[] = {&w, &h, &ss, &max_rounds};
   IWPP_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(blocks), dim3(kRoundThreads), args, 0, st));
-  return IWPP_OK;
-}
-
-int launch_finalize(const EdtState &s, int final_buf, int W, int H, int64_t *vr, float *dist,
-                    int64_t *d2, cudaStream_t st) {
-  size_t n = (size_t)W * H;
-  edt_finalize_kernel<<<grid_for(n, 256), 256, 0, st>>>(s.buf[final_buf], W, H, vr, dist, d2,
-                                                         s.counters);
-  IWPP_CUDA_TRY(cudaGetLastError());
   return IWPP_OK;
 }
 
@@ -424,7 +616,10 @@ __global__ void edt_select_final_kernel(EdtState s, int W, int H, int64_t *vr, f
 int launch_finalize_auto(const EdtState &s, int W, int H, int64_t *vr, float *dist, int64_t *d2,
                          cudaStream_t st) {
   size_t n = (size_t)W * H;
-  edt_select_final_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, W, H, vr, dist, d2);
+  if (s.keymode)
+    edt_finalize_key_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, W, H, vr, dist, d2);
+  else
+    edt_select_final_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, W, H, vr, dist, d2);
   IWPP_CUDA_TRY(cudaGetLastError());
   return IWPP_OK;
 }

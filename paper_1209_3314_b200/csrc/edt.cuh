@@ -9,21 +9,28 @@ constexpr uint32_t INF32 = 0xFFFFFFFFu;
 constexpr uint32_t SEED_STAMP = 0xFFFFFFFEu;
 constexpr int kRoundThreads = 512;
 constexpr int kRoundBlocksPerSm = 2;
+constexpr int kEdtBq = 6144;  // per-block next-frontier buffer (shared memory, 24 KB)
 
 enum { EC_ROUNDS = 0, EC_VISITS, EC_NINF, EC_LIMIT, EC_FINAL, EC_BAD, EC_N = 8 };
 
 struct EdtState {
-  uint32_t *buf[2];  // source per cell, (sy << 16 | sx), double-buffered
-  uint32_t *stamp;   // round stamp per cell (frontier dedupe)
-  uint32_t *F[2];    // frontier queues (yx codes)
-  unsigned *cnt;     // [3] frontier sizes (triple-buffered)
-  unsigned *bar;     // [2] grid barrier count / generation
+  int keymode;               // 1: 64-bit keys (d2 << 32 | src), 0: 32-bit sources + CAS
+  unsigned long long *keys;  // keymode: 2 keys per cell (AoS, double-buffered)
+  uint32_t *buf[2];          // !keymode: source per cell, (sy << 16 | sx), double-buffered
+  uint32_t *stamp;           // !keymode: round stamp per cell (frontier dedupe)
+  uint32_t *F[2];            // frontier queues (yx codes)
+  unsigned *cnt;             // [3] frontier sizes (triple-buffered)
+  unsigned *bar;             // [2] grid barrier count / generation
   unsigned long long *counters;
 };
 
 // Images the 32-bit (y,x) code can address (INF must stay unused).
 inline bool size_supported(int64_t W, int64_t H) {
   return W >= 1 && H >= 1 && W <= 65536 && H <= 65536 && !(W == 65536 && H == 65536);
+}
+// The key engine needs every squared distance to fit 32 bits.
+inline bool key_mode_ok(int64_t W, int64_t H) {
+  return (uint64_t)(W - 1) * (W - 1) + (uint64_t)(H - 1) * (H - 1) < (1ull << 32);
 }
 
 size_t state_bytes(int64_t W, int64_t H);

@@ -121,6 +121,20 @@ __device__ __forceinline__ unsigned smem_atomic_or_if(unsigned *p, unsigned v, u
   return old;
 }
 
+// Predicated global 64-bit atomicMin (predicated off: returns all-ones and
+// touches nothing).
+__device__ __forceinline__ unsigned long long gmem_atomic_min_if(unsigned long long *p,
+                                                                 unsigned long long v,
+                                                                 unsigned pred) {
+  unsigned long long old = ~0ull;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q atom.global.min.u64 %0, [%1], %2;\n\t}"
+      : "+l"(old)
+      : "l"(p), "l"(v), "r"(pred)
+      : "memory");
+  return old;
+}
+
 // Element traits: the engines keep values as int32 in shared memory so the
 // hardware atomicMax covers every element kind (u8/u16 widen losslessly).
 template <typename T>
