@@ -91,6 +91,10 @@ typedef struct iwpp_recon_opts {
   int halo_sweep_threshold; /* re-visit: sweep when more halo pixels than this are active (-1 = auto) */
   void *ev_begin;    /* optional events (iwpp_event_create) recorded on the stream */
   void *ev_end;      /* right before / after the tile-engine kernel (roofline timing) */
+  int slab_rows;     /* 0: normal run.  Multi-GPU slab waves: bit0 / bit1 = the first /
+                        last image row is a halo row that changed; only the tile rows
+                        holding or touching it are re-run (the rest of J must already be
+                        at its fixed point) */
 } iwpp_recon_opts;
 
 /* Timing helpers (events live in this library's CUDA runtime). */

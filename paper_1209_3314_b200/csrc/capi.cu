@@ -145,6 +145,7 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
     eo.halo_thresh = opts->halo_sweep_threshold;
     eo.ev_begin = opts->ev_begin;
     eo.ev_end = opts->ev_end;
+    eo.rows_mode = opts->slab_rows & 3;
   }
   if ((rc = recon::run_tile_engine(J, I, (int)W, (int)H, dtype, conn, w.q, w.counters, eo, st)))
     return rc;
@@ -187,7 +188,7 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   unsigned long long viol = 0;
   IWPP_CUDA_TRY(cudaMemcpyAsync(&viol, &w.counters[recon::CNT_VIOL], sizeof viol,
                                 cudaMemcpyDeviceToHost, st));
-  iwpp_recon_opts o = opts ? *opts : iwpp_recon_opts{-1, 0, 0, 0, -1, -1, nullptr, nullptr};
+  iwpp_recon_opts o = opts ? *opts : iwpp_recon_opts{-1, 0, 0, 0, -1, -1, nullptr, nullptr, 0};
   o.check_contract = 0;
   if ((rc = iwpp_recon(dJ, dI, W, H, dtype, conn, rest, rest_bytes, &o, nullptr, stream))) return rc;
   IWPP_CUDA_TRY(cudaMemcpyAsync(out, dJ, nb, cudaMemcpyDeviceToHost, st));

@@ -725,6 +725,49 @@ __global__ void tile_queue_init_kernel(TileQueue q, int ntx, int nty, unsigned l
   if (i < CNT_N) counters[i] = 0;
 }
 
+// Re-activation fill for slab runs (multi-GPU waves): only the tile rows
+// holding or touching a changed halo row are queued -- the first tile row
+// for the top halo, the last two for the bottom one -- as first visits
+// (the halo row may lie inside a tile, so full detection is needed there);
+// the rest of the slab is already at its local fixed point.
+__device__ __forceinline__ bool rows_sel(int ty, int nty, int top, int bottom) {
+  return (top && ty == 0) || (bottom && ty >= nty - 2);
+}
+
+__global__ void tile_queue_init_rows_kernel(TileQueue q, int ntx, int nty, int top, int bottom,
+                                            unsigned long long *counters) {
+  unsigned ntiles = (unsigned)ntx * nty;
+  unsigned stride = gridDim.x * blockDim.x;
+  unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned nrows = 0;
+  for (int ty = 0; ty < nty; ty++) {
+    if (ty > 0 && ty < nty - 2) ty = nty - 2;  // only rows 0, nty-2, nty-1 can be selected
+    nrows += rows_sel(ty, nty, top, bottom);
+  }
+  unsigned nq = (unsigned)ntx * nrows;
+  for (unsigned t = i; t < ntiles; t += stride) {
+    int tx = (int)(t % ntx), ty = (int)(t / ntx);
+    bool sel = rows_sel(ty, nty, top, bottom);
+    q.state[t] = sel ? (ST_Q | ST_V) : 0u;
+    if (sel) {
+      unsigned before = 0;  // selected rows above ty
+      for (int r = 0; r < ty; r++) {
+        if (r > 0 && r < nty - 2) r = nty - 2;
+        if (r < ty) before += rows_sel(r, nty, top, bottom);
+      }
+      unsigned slot = before * ntx + tx;
+      q.ring[slot] = ((unsigned long long)slot << 32) | t;
+    }
+  }
+  for (unsigned t = nq + i; t <= q.mask; t += stride) q.ring[t] = ~0ull;
+  if (i == 0) {
+    *q.head = 0;
+    *q.tail = nq;
+    *q.pending = nq;
+  }
+  if (i < CNT_N) counters[i] = 0;
+}
+
 size_t tile_queue_bytes(unsigned ntiles) {
   Carver c(nullptr);
   carve_tile_queue(c, ntiles);
@@ -767,7 +810,11 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   if ((unsigned)blocks > max_b) blocks = (int)max_b;
   unsigned ib = (q.mask + 1 + 255) / 256;
   if (ib > 1024) ib = 1024;
-  tile_queue_init_kernel<<<ib, 256, 0, st>>>(q, ntx, nty, counters);
+  if (o.rows_mode)
+    tile_queue_init_rows_kernel<<<ib, 256, 0, st>>>(q, ntx, nty, o.rows_mode & 1,
+                                                     (o.rows_mode >> 1) & 1, counters);
+  else
+    tile_queue_init_kernel<<<ib, 256, 0, st>>>(q, ntx, nty, counters);
   IWPP_CUDA_TRY(cudaGetLastError());
   unsigned qlimit = (o.qcap > 0 && o.qcap < RQ) ? (unsigned)o.qcap : (unsigned)RQ;
   unsigned hth = o.halo_thresh >= 0 ? (unsigned)o.halo_thresh : kHaloSweepThreshold;

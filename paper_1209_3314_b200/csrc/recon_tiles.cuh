@@ -43,6 +43,8 @@ struct EngineOpts {
   int sweeps = 1;        // in-tile sweep passes on a tile's first visit
   int halo_thresh = -1;  // re-activation front that triggers sweeps (-1 = default)
   void *ev_begin = nullptr, *ev_end = nullptr;  // cudaEvent_t around the engine kernel
+  int rows_mode = 0;     // 0: every tile, first visit; bit0 / bit1: only the top / bottom
+                         // tile row, as re-visits (slab waves after a halo exchange)
 };
 
 size_t tile_queue_bytes(unsigned ntiles);

@@ -1,0 +1,249 @@
+"""Multi-GPU slab execution: one process per GPU, horizontal
+slabs, border rows exchanged with the up/down neighbours, global
+termination by an all-reduce.
+
+This mirrors the reference's tiled pipeline (tiles.py:375-431): TP = each
+rank propagates its slab to the local fixed point; BP = the changed border
+rows cross the slab cuts; waves repeat until no border changes anywhere.
+Reconstruction's fixed point is unique (tiles.py:7-9), so the slab result
+equals the single-device result cell for cell.
+
+Slab layout (per rank, device buffers): ``J_ext``/``I_ext`` hold the rank's
+rows plus one halo row above and below.  Halo rows carry the neighbour's
+current border values in both J and I (J == I: never raised, never
+clamped), so the engine treats them as fixed sources.  A missing neighbour
+(image edge) is a min(T) row in both (never a source either).
+
+The protocol is written against a tiny transport interface so the same
+driver runs (a) one slab per rank over torch.distributed (NCCL on B200s,
+gloo on CPU for the tests) and (b) several virtual slabs in one process
+(the single-GPU parity tests).  The local solver is injected: the CUDA
+engine (``device_solver``) in production; tests may pass a CPU checker.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ContractViolation
+
+# sentinel (smallest) value per dtype, as stored in J/I halo rows
+_LO = {np.dtype(np.uint8): 0, np.dtype(np.uint16): 0, np.dtype(np.int32): -(2**31)}
+
+
+def slab_bounds(H: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows [y0, y1) of ``rank`` for H rows split into ``world`` near-equal
+    horizontal slabs (the reference's _bands, recon.py:260-272)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ContractViolation("bad slab rank/world")
+    base, rem = divmod(H, world)
+    y0 = rank * base + min(rank, rem)
+    return y0, y0 + base + (1 if rank < rem else 0)
+
+
+@dataclass
+class WaveStats:
+    waves: int = 0
+    halo_changes: int = 0
+
+
+class SlabRecon:
+    """One rank's slab of a reconstruction: ext buffers + protocol steps.
+
+    ``xp`` is the array module of the buffers (torch for device slabs,
+    numpy for CPU checker slabs); only element-wise copies and compares
+    are used here.
+    """
+
+    def __init__(self, J_rows, I_rows, has_up: bool, has_down: bool, conn: int, solver):
+        h, W = J_rows.shape
+        self.h, self.W, self.conn, self.solver = h, W, conn, solver
+        self.has_up, self.has_down = has_up, has_down
+        self.is_torch = not isinstance(J_rows, np.ndarray)
+        dt = np.dtype(np.uint8) if not self.is_torch else _np_dtype(J_rows)
+        lo = _LO[dt]
+        if self.is_torch:
+            import torch
+            self.J = torch.full((h + 2, W), lo, dtype=J_rows.dtype, device=J_rows.device)
+            self.I = torch.full((h + 2, W), lo, dtype=I_rows.dtype, device=I_rows.device)
+        else:
+            dt = J_rows.dtype
+            lo = _LO[np.dtype(dt)]
+            self.J = np.full((h + 2, W), lo, dtype=dt)
+            self.I = np.full((h + 2, W), lo, dtype=dt)
+        self.J[1:h + 1] = J_rows
+        self.I[1:h + 1] = I_rows
+        self.first = True
+
+    # -- protocol pieces --------------------------------------------------
+    def border_rows(self):
+        """(my first row, my last row) to send up / down."""
+        return self.J[1], self.J[self.h]
+
+    def set_halos(self, from_up, from_down):
+        """Install the neighbours' border rows; returns (top changed,
+        bottom changed).  Values only grow, so any difference is a rise."""
+        top = bot = False
+        if self.has_up and from_up is not None:
+            top = bool((from_up != self.J[0]).any())
+            self.J[0] = from_up
+            self.I[0] = from_up  # J == I: a fixed source, never raised or clamped
+        if self.has_down and from_down is not None:
+            bot = bool((from_down != self.J[self.h + 1]).any())
+            self.J[self.h + 1] = from_down
+            self.I[self.h + 1] = from_down
+        self._top, self._bot = top, bot
+        return top, bot
+
+    def solve(self):
+        """Propagate to the slab's fixed point (first wave: everything;
+        later waves: only the tile rows at changed halos)."""
+        if self.first:
+            rows = 0
+        else:
+            rows = (1 if self._top else 0) | (2 if self._bot else 0)
+            if rows == 0:
+                return
+        self.solver(self.J, self.I, self.conn, rows)
+        self.first = False
+
+    def result(self):
+        return self.J[1:self.h + 1]
+
+
+def _np_dtype(t):
+    import torch
+    return {torch.uint8: np.dtype(np.uint8), torch.uint16: np.dtype(np.uint16),
+            torch.int32: np.dtype(np.int32)}[t.dtype]
+
+
+# ---------------------------------------------------------------------------
+# solvers
+
+def device_solver(J, I, conn: int, rows: int):
+    """The CUDA tile engine on an ext slab (torch device tensors)."""
+    from . import _lib
+    L = _lib.lib()
+    code = {np.dtype(np.uint8): 0, np.dtype(np.uint16): 1, np.dtype(np.int32): 2}[_np_dtype(J)]
+    H, W = J.shape
+    ws = _lib.workspace(L.iwpp_recon_workspace_bytes(W, H, code, conn))
+    o = _lib.ReconOpts()
+    o.sweeps, o.max_blocks, o.check_contract, o.queue_capacity = 0, 0, 0, 0
+    o.tile_sweeps, o.halo_sweep_threshold, o.slab_rows = -1, -1, rows
+    _lib.check(L.iwpp_recon(_lib.ptr(J), _lib.ptr(I), W, H, code, conn, _lib.ptr(ws),
+                            ws.numel(), _lib.ctypes.byref(o), None, _lib.stream_ptr()), "slab")
+
+
+# ---------------------------------------------------------------------------
+# drivers
+
+def run_slabs_local(slabs: list[SlabRecon], max_waves: int | None = None) -> WaveStats:
+    """Several slabs in one process (virtual ranks), wave-synchronous."""
+    st = WaveStats()
+    n = len(slabs)
+    pending = [(None, None)] * n
+    # initial exchange: neighbours' marker rows
+    for i, s in enumerate(slabs):
+        up = slabs[i - 1].border_rows()[1] if i > 0 else None
+        dn = slabs[i + 1].border_rows()[0] if i + 1 < n else None
+        pending[i] = (_copy(up), _copy(dn))
+    for i, s in enumerate(slabs):
+        s.set_halos(*pending[i])
+    while True:
+        if max_waves is not None and st.waves >= max_waves:
+            raise ContractViolation(f"no stability within {max_waves} waves")
+        for s in slabs:
+            s.solve()
+        st.waves += 1
+        for i, s in enumerate(slabs):
+            up = slabs[i - 1].border_rows()[1] if i > 0 else None
+            dn = slabs[i + 1].border_rows()[0] if i + 1 < n else None
+            pending[i] = (_copy(up), _copy(dn))
+        changed = 0
+        for i, s in enumerate(slabs):
+            t, b = s.set_halos(*pending[i])
+            changed += int(t) + int(b)
+        st.halo_changes += changed
+        if changed == 0:
+            return st
+
+
+def _copy(x):
+    if x is None:
+        return None
+    return x.clone() if hasattr(x, "clone") else x.copy()
+
+
+def run_slab_dist(slab: SlabRecon, group=None, max_waves: int | None = None) -> WaveStats:
+    """One slab per rank over torch.distributed (NCCL between B200s; gloo
+    for CPU tests).  Border rows go to rank-1 / rank+1 with point-to-point
+    send/recv; the wave loop ends when an all-reduce of halo changes is 0."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    st = WaveStats()
+
+    def exchange():
+        first, last = slab.border_rows()
+        ops, up, dn = [], None, None
+        if rank > 0:
+            up = torch.empty_like(first)
+            ops.append(dist.P2POp(dist.isend, first.contiguous(), rank - 1, group))
+            ops.append(dist.P2POp(dist.irecv, up, rank - 1, group))
+        if rank + 1 < world:
+            dn = torch.empty_like(last)
+            ops.append(dist.P2POp(dist.isend, last.contiguous(), rank + 1, group))
+            ops.append(dist.P2POp(dist.irecv, dn, rank + 1, group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        return slab.set_halos(up, dn)
+
+    exchange()
+    dev = slab.J.device
+    while True:
+        if max_waves is not None and st.waves >= max_waves:
+            raise ContractViolation(f"no stability within {max_waves} waves")
+        slab.solve()
+        st.waves += 1
+        t, b = exchange()
+        flag = torch.tensor([int(t) + int(b)], device=dev, dtype=torch.int64)
+        dist.all_reduce(flag, group=group)
+        st.halo_changes += int(flag.item())
+        if int(flag.item()) == 0:
+            return st
+
+
+def recon_slabs(marker, mask, conn: int = 8, group=None, max_waves: int | None = None):
+    """Distributed reconstruction: every rank passes the FULL image (host
+    numpy or device tensor), computes its slab on its GPU, and receives the
+    full result (all-gather).  Returns (result, WaveStats)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    H, W = marker.shape
+    y0, y1 = slab_bounds(H, world, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Jt = torch.as_tensor(marker)[y0:y1].to(dev)
+    It = torch.as_tensor(mask)[y0:y1].to(dev)
+    slab = SlabRecon(Jt, It, rank > 0, rank + 1 < world, conn, device_solver)
+    st = run_slab_dist(slab, group, max_waves)
+    full = torch.empty((H, W), dtype=Jt.dtype, device=dev)
+    parts = [full[slice(*slab_bounds(H, world, r))] for r in range(world)]
+    if all(p.shape == parts[0].shape for p in parts):
+        dist.all_gather(parts, slab.result().contiguous(), group=group)
+    else:  # ragged slabs: gather padded rows
+        hmax = max(p.shape[0] for p in parts)
+        buf = torch.zeros((hmax, W), dtype=Jt.dtype, device=dev)
+        buf[:y1 - y0] = slab.result()
+        outs = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(outs, buf, group=group)
+        for r, p in enumerate(parts):
+            p.copy_(outs[r][:p.shape[0]])
+    if isinstance(marker, np.ndarray):
+        return full.cpu().numpy(), st
+    return full, st

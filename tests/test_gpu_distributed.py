@@ -1,0 +1,81 @@
+"""Slab (multi-GPU) reconstruction path with the CUDA engine as the slab
+solver.  Only one GPU is available to the tests, so G slabs run as virtual
+ranks on it (the same SlabRecon / wave protocol the NCCL driver runs), plus
+the real torch.distributed driver on a one-rank NCCL group.  Results must
+equal the single-image oracle bit for bit."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _slabs(J, I, G, conn):
+    import torch
+    from paper_1209_3314_b200.distributed import SlabRecon, device_solver, slab_bounds
+    out = []
+    for r in range(G):
+        y0, y1 = slab_bounds(J.shape[0], G, r)
+        out.append(SlabRecon(torch.from_numpy(J[y0:y1].copy()).cuda(),
+                             torch.from_numpy(I[y0:y1].copy()).cuda(), r > 0, r + 1 < G, conn,
+                             device_solver))
+    return out
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_virtual_slabs_random_u8(conn, G):
+    from paper_1209_3314_b200.distributed import run_slabs_local
+    J, I = oracle.gray_pair((1000, 777), 17 + G, h=40)
+    want = oracle.recon_fh(J, I, conn)
+    slabs = _slabs(J, I, G, conn)
+    run_slabs_local(slabs)
+    got = np.concatenate([s.result().cpu().numpy() for s in slabs])
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_virtual_slabs_imfill(conn):
+    from paper_1209_3314_b200.distributed import run_slabs_local
+    bw = oracle.gen_synthetic_mask(1024, 1024, 50, 7)
+    J, I = oracle.imfill_pair(bw)
+    want = oracle.recon_fh(J, I, conn)
+    slabs = _slabs(J, I, 8, conn)
+    st = run_slabs_local(slabs)
+    assert np.array_equal(np.concatenate([s.result().cpu().numpy() for s in slabs]), want)
+    assert st.waves >= 2
+
+
+def test_virtual_slabs_int32():
+    from paper_1209_3314_b200.distributed import run_slabs_local
+    J, I = oracle.gray_pair((300, 257), 5, h=1 << 27, dtype=np.int32)
+    want = oracle.recon_fh(J, I, 8)
+    slabs = _slabs(J, I, 3, 8)
+    run_slabs_local(slabs)
+    assert np.array_equal(np.concatenate([s.result().cpu().numpy() for s in slabs]), want)
+
+
+def test_recon_slabs_nccl_single_rank():
+    import torch
+    import torch.distributed as dist
+    from paper_1209_3314_b200.distributed import recon_slabs
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        J, I = oracle.gray_pair((256, 300), 3, h=40)
+        got, st = recon_slabs(J, I, 8)
+        assert np.array_equal(got, oracle.recon_fh(J, I, 8))
+    finally:
+        dist.destroy_process_group()
