@@ -169,6 +169,28 @@ int iwpp_edt_propagate(int64_t *vr, int64_t W, int64_t H, int conn,
  * Returns IWPP_E_NO_BACKGROUND if any vr == -1.  d2 may be NULL. */
 int iwpp_edt_finalize(const int64_t *vr, int64_t W, int64_t H, float *dist,
                       int64_t *d2, void *workspace, void *stream);
+/* ---- EDT on one horizontal slab of a multi-GPU run ----
+ * The rank owns rows [y0, y0+h) of an H-row image.  The synchronous rule
+ * needs one exchange per round (tiles.py:10-15, edt_bp_sweep K.493-522):
+ * each round takes the neighbours' boundary frontier rows (halo_up /
+ * halo_dn: W uint64 sources, all-ones = none; NULL at the image edge) and
+ * produces this slab's (out_up / out_dn).  Keys use global coordinates, so
+ * the result equals the single-device EDT cell for cell.
+ * mask_ext: (h + 2) x W device u8, rows 0 / h+1 = the neighbours' rows. */
+size_t iwpp_edt_slab_workspace_bytes(int64_t W, int64_t h);
+int iwpp_edt_slab_init(const uint8_t *mask_ext, int64_t W, int64_t h, int64_t y0, int64_t H,
+                       int conn, int has_up, int has_down, void *workspace,
+                       uint64_t *out_up, uint64_t *out_dn, void *stream);
+/* round r: *n_next_host = this slab's next frontier size (syncs) */
+int iwpp_edt_slab_round(void *workspace, int64_t W, int64_t h, int64_t y0, int conn, int64_t r,
+                        const uint64_t *halo_up, const uint64_t *halo_dn, uint64_t *out_up,
+                        uint64_t *out_dn, int64_t *n_next_host, void *stream);
+/* after `rounds` rounds: vr (h x W int64, global packed indices) and dist;
+ * returns IWPP_E_NO_BACKGROUND if a cell has no source, IWPP_E_OVERFLOW if
+ * a squared distance exceeded the 32-bit key range. */
+int iwpp_edt_slab_finalize(void *workspace, int64_t W, int64_t h, int64_t y0, int64_t rounds,
+                           int64_t *vr, float *dist, void *stream);
+
 /* Host-buffer variant: mask host -> device, edt, vr/dist device -> host. */
 size_t iwpp_edt_host_workspace_bytes(int64_t W, int64_t H, int conn);
 int iwpp_edt_host(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *vr,

@@ -34,6 +34,8 @@ EXPORTS = (
     "iwpp_recon_seed_scan", "iwpp_edt_workspace_bytes", "iwpp_edt", "iwpp_edt_propagate",
     "iwpp_edt_finalize", "iwpp_edt_host_workspace_bytes", "iwpp_edt_host",
     "iwpp_event_create", "iwpp_event_destroy", "iwpp_event_record", "iwpp_event_elapsed_ms",
+    "iwpp_edt_slab_workspace_bytes", "iwpp_edt_slab_init", "iwpp_edt_slab_round",
+    "iwpp_edt_slab_finalize",
 )
 
 
@@ -95,6 +97,11 @@ def load_library(path: str = LIB_PATH):
             "iwpp_event_destroy": ([P], I),
             "iwpp_event_record": ([P, P], I),
             "iwpp_event_elapsed_ms": ([P, P, ctypes.POINTER(ctypes.c_float)], I),
+            "iwpp_edt_slab_workspace_bytes": ([I64, I64], SZ),
+            "iwpp_edt_slab_init": ([P, I64, I64, I64, I64, I, I, I, P, P, P, P], I),
+            "iwpp_edt_slab_round": ([P, I64, I64, I64, I, I64, P, P, P, P,
+                                     ctypes.POINTER(I64), P], I),
+            "iwpp_edt_slab_finalize": ([P, I64, I64, I64, I64, P, P, P], I),
         }
         for name, (args, res) in proto.items():
             fn = getattr(L, name)

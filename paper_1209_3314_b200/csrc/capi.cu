@@ -384,3 +384,44 @@ int iwpp_edt_host(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- EDT slabs
+
+extern "C" {
+
+size_t iwpp_edt_slab_workspace_bytes(int64_t W, int64_t h) { return edt::slab_bytes(W, h); }
+
+int iwpp_edt_slab_init(const uint8_t *mask_ext, int64_t W, int64_t h, int64_t y0, int64_t H,
+                       int conn, int has_up, int has_down, void *workspace, uint64_t *out_up,
+                       uint64_t *out_dn, void *stream) {
+  int rc = check_dims(W, h);
+  if (rc) return rc;
+  if (W > 65536 || H > 65536 || y0 < 0 || y0 + h > H)
+    return set_error(IWPP_E_CONTRACT, "bad slab geometry");
+  if (conn != 4 && conn != 8) return set_error(IWPP_E_CONTRACT, "connectivity must be 4 or 8");
+  return edt::slab_init(mask_ext, W, h, y0, H, conn, has_up, has_down, workspace,
+                        (unsigned long long *)out_up, (unsigned long long *)out_dn,
+                        (cudaStream_t)stream);
+}
+
+int iwpp_edt_slab_round(void *workspace, int64_t W, int64_t h, int64_t y0, int conn, int64_t r,
+                        const uint64_t *halo_up, const uint64_t *halo_dn, uint64_t *out_up,
+                        uint64_t *out_dn, int64_t *n_next_host, void *stream) {
+  return edt::slab_round(workspace, W, h, y0, conn, r, (const unsigned long long *)halo_up,
+                         (const unsigned long long *)halo_dn, (unsigned long long *)out_up,
+                         (unsigned long long *)out_dn, n_next_host, (cudaStream_t)stream);
+}
+
+int iwpp_edt_slab_finalize(void *workspace, int64_t W, int64_t h, int64_t y0, int64_t rounds,
+                           int64_t *vr, float *dist, void *stream) {
+  int64_t ninf = 0, range = 0;
+  int rc = edt::slab_finalize(workspace, W, h, y0, rounds, vr, dist, &ninf, &range,
+                              (cudaStream_t)stream);
+  if (rc) return rc;
+  if (range)
+    return set_error(IWPP_E_OVERFLOW, "a squared distance exceeded the 32-bit key range");
+  if (ninf) return set_error(IWPP_E_NO_BACKGROUND, "no background reachable: distance map undefined");
+  return IWPP_OK;
+}
+
+}  // extern "C"

@@ -268,14 +268,6 @@ __global__ void edt_finalize_vr_kernel(const int64_t *__restrict__ vr, int W, in
 // push per changed cell.
 // ===========================================================================
 
-constexpr unsigned long long KINF = ~0ull;
-
-__device__ __forceinline__ unsigned long long make_key(int qx, int qy, uint32_t src) {
-  int sy = (int)(src >> 16), sx = (int)(src & 0xffffu);
-  unsigned dx = (unsigned)abs(qx - sx), dy = (unsigned)abs(qy - sy);
-  unsigned d2 = dx * dx + dy * dy;  // < 2^32 by key_mode_ok
-  return ((unsigned long long)d2 << 32) | src;
-}
 
 template <int CONN>
 __global__ void edt_init_key_kernel(const uint8_t *__restrict__ mask, int W, int H, EdtState s) {

@@ -11,7 +11,7 @@ constexpr int kRoundThreads = 512;
 constexpr int kRoundBlocksPerSm = 2;
 constexpr int kEdtBq = 6144;  // per-block next-frontier buffer (shared memory, 24 KB)
 
-enum { EC_ROUNDS = 0, EC_VISITS, EC_NINF, EC_LIMIT, EC_FINAL, EC_BAD, EC_N = 8 };
+enum { EC_ROUNDS = 0, EC_VISITS, EC_NINF, EC_LIMIT, EC_FINAL, EC_BAD, EC_RANGE, EC_N = 8 };
 
 struct EdtState {
   int keymode;               // 1: 64-bit keys (d2 << 32 | src), 0: 32-bit sources + CAS
@@ -33,7 +33,31 @@ inline bool key_mode_ok(int64_t W, int64_t H) {
   return (uint64_t)(W - 1) * (W - 1) + (uint64_t)(H - 1) * (H - 1) < (1ull << 32);
 }
 
+// key = (d2(q, src) << 32) | src_yx: the reference's total order at q
+// (K.320-336) as a plain unsigned order; INF (no source) = all ones.
+constexpr unsigned long long KINF = ~0ull;
+
+__device__ __forceinline__ unsigned long long make_key(int qx, int qy, uint32_t src) {
+  int sy = (int)(src >> 16), sx = (int)(src & 0xffffu);
+  unsigned dx = (unsigned)abs(qx - sx), dy = (unsigned)abs(qy - sy);
+  unsigned d2 = dx * dx + dy * dy;  // < 2^32 by key_mode_ok
+  return ((unsigned long long)d2 << 32) | src;
+}
+
 size_t state_bytes(int64_t W, int64_t H);
+
+// slab engine (edt_slab.cu): one round per launch, halo items from the
+// neighbours, boundary frontier rows out (source or KINF per column)
+size_t slab_bytes(int64_t W, int64_t h);
+int slab_init(const uint8_t *mask_ext, int64_t W, int64_t h, int64_t y0, int64_t H, int conn,
+              int has_up, int has_down, void *ws, unsigned long long *out_up,
+              unsigned long long *out_dn, cudaStream_t st);
+int slab_round(void *ws, int64_t W, int64_t h, int64_t y0, int conn, int64_t r,
+               const unsigned long long *halo_up, const unsigned long long *halo_dn,
+               unsigned long long *out_up, unsigned long long *out_dn, int64_t *n_next_host,
+               cudaStream_t st);
+int slab_finalize(void *ws, int64_t W, int64_t h, int64_t y0, int64_t rounds, int64_t *vr,
+                  float *dist, int64_t *n_inf_host, int64_t *range_err_host, cudaStream_t st);
 EdtState carve_state(Carver &c, int64_t W, int64_t H);
 int reset_control(const EdtState &s, cudaStream_t st);
 int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, cudaStream_t st);

@@ -247,3 +247,152 @@ def recon_slabs(marker, mask, conn: int = 8, group=None, max_waves: int | None =
     if isinstance(marker, np.ndarray):
         return full.cpu().numpy(), st
     return full, st
+
+
+# ---------------------------------------------------------------------------
+# EDT: one exchange per round (the synchronous rule, tiles.py:10-15)
+
+class SlabEDT:
+    """One rank's slab of a distance transform on the device: the slab
+    engine advances one two-phase round per call; the neighbours' boundary
+    frontier rows (sources, all-ones = none) are the halo items of the
+    round."""
+
+    def __init__(self, mask_ext, y0: int, H: int, has_up: bool, has_down: bool, conn: int):
+        import torch
+        from . import _lib
+        self._lib, self.L = _lib, _lib.lib()
+        h2, W = mask_ext.shape
+        self.h, self.W, self.y0, self.H, self.conn = h2 - 2, W, y0, H, conn
+        self.has_up, self.has_down = has_up, has_down
+        dev = mask_ext.device
+        self.ws = torch.empty(self.L.iwpp_edt_slab_workspace_bytes(W, self.h), dtype=torch.uint8,
+                              device=dev)
+        self.out = [torch.empty(W, dtype=torch.int64, device=dev) for _ in range(2)]
+        self.rounds = 0
+        self._lib.check(self.L.iwpp_edt_slab_init(
+            _lib.ptr(mask_ext.contiguous()), W, self.h, y0, H, conn, int(has_up), int(has_down),
+            _lib.ptr(self.ws), _lib.ptr(self.out[0]), _lib.ptr(self.out[1]), _lib.stream_ptr()),
+            "edt_slab_init")
+
+    def boundary_rows(self):
+        """(first-row, last-row) frontier sources of the coming round."""
+        return self.out[0], self.out[1]
+
+    def round(self, halo_up, halo_dn) -> int:
+        """Run one round; returns this slab's next frontier size."""
+        import torch
+        _lib = self._lib
+        new = [torch.empty_like(self.out[0]), torch.empty_like(self.out[1])]
+        n = _lib.ctypes.c_int64(0)
+        _lib.check(self.L.iwpp_edt_slab_round(
+            _lib.ptr(self.ws), self.W, self.h, self.y0, self.conn, self.rounds,
+            _lib.ptr(halo_up) if halo_up is not None else None,
+            _lib.ptr(halo_dn) if halo_dn is not None else None,
+            _lib.ptr(new[0]), _lib.ptr(new[1]), _lib.ctypes.byref(n), _lib.stream_ptr()),
+            "edt_slab_round")
+        self.out = new
+        self.rounds += 1
+        return int(n.value)
+
+    def finalize(self):
+        import torch
+        _lib = self._lib
+        dev = self.ws.device
+        vr = torch.empty((self.h, self.W), dtype=torch.int64, device=dev)
+        dist = torch.empty((self.h, self.W), dtype=torch.float32, device=dev)
+        _lib.check(self.L.iwpp_edt_slab_finalize(_lib.ptr(self.ws), self.W, self.h, self.y0,
+                                                 self.rounds, _lib.ptr(vr), _lib.ptr(dist),
+                                                 _lib.stream_ptr()), "edt_slab_finalize")
+        return vr, dist
+
+
+def mask_ext_rows(mask, y0: int, y1: int):
+    """(h + 2) x W slab of a full mask with the neighbours' rows (zeros past
+    the image edge; the engine ignores them there)."""
+    import torch
+    m = torch.as_tensor(mask)
+    H, W = m.shape
+    ext = torch.zeros((y1 - y0 + 2, W), dtype=torch.uint8)
+    ext[1:-1] = m[y0:y1]
+    if y0 > 0:
+        ext[0] = m[y0 - 1]
+    if y1 < H:
+        ext[-1] = m[y1]
+    return ext
+
+
+def run_edt_slabs_local(slabs: list[SlabEDT], max_rounds: int | None = None) -> int:
+    """Virtual ranks in one process: round-synchronous, one boundary-row
+    exchange per round.  Returns the number of rounds."""
+    n = len(slabs)
+    while True:
+        if max_rounds is not None and slabs[0].rounds >= max_rounds:
+            from .errors import EngineError
+            raise EngineError(f"no fixed point within {max_rounds} rounds")
+        halos = []
+        for i in range(n):
+            up = slabs[i - 1].boundary_rows()[1] if i > 0 else None
+            dn = slabs[i + 1].boundary_rows()[0] if i + 1 < n else None
+            halos.append((up, dn))
+        total = sum(s.round(*hl) for s, hl in zip(slabs, halos))
+        if total == 0:
+            return slabs[0].rounds
+
+
+def run_edt_slab_dist(slab: SlabEDT, group=None, max_rounds: int | None = None) -> int:
+    """One slab per rank: per round, boundary rows to rank-1 / rank+1
+    (send/recv), then an all-reduce of the next frontier sizes."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = slab.ws.device
+    while True:
+        if max_rounds is not None and slab.rounds >= max_rounds:
+            from .errors import EngineError
+            raise EngineError(f"no fixed point within {max_rounds} rounds")
+        first, last = slab.boundary_rows()
+        ops, up, dn = [], None, None
+        if rank > 0:
+            up = torch.empty_like(first)
+            ops.append(dist.P2POp(dist.isend, first, rank - 1, group))
+            ops.append(dist.P2POp(dist.irecv, up, rank - 1, group))
+        if rank + 1 < world:
+            dn = torch.empty_like(last)
+            ops.append(dist.P2POp(dist.isend, last, rank + 1, group))
+            ops.append(dist.P2POp(dist.irecv, dn, rank + 1, group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        nxt = slab.round(up, dn)
+        t = torch.tensor([nxt], device=dev, dtype=torch.int64)
+        dist.all_reduce(t, group=group)
+        if int(t.item()) == 0:
+            return slab.rounds
+
+
+def edt_slabs(mask, conn: int = 8, group=None, max_rounds: int | None = None):
+    """Distributed EDT: every rank passes the full binary mask; returns the
+    full (vr int64, dist f32) on every rank (all-gather)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    H, W = mask.shape
+    y0, y1 = slab_bounds(H, world, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    slab = SlabEDT(mask_ext_rows(mask, y0, y1).to(dev), y0, H, rank > 0, rank + 1 < world, conn)
+    run_edt_slab_dist(slab, group, max_rounds)
+    vr, dist_ = slab.finalize()
+    outs = []
+    for t in (vr, dist_):
+        hmax = max(b - a for a, b in (slab_bounds(H, world, r) for r in range(world)))
+        buf = torch.zeros((hmax, W), dtype=t.dtype, device=dev)
+        buf[:y1 - y0] = t
+        parts = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(parts, buf, group=group)
+        full = torch.cat([parts[r][:slab_bounds(H, world, r)[1] - slab_bounds(H, world, r)[0]]
+                          for r in range(world)])
+        outs.append(full.cpu().numpy() if isinstance(mask, np.ndarray) else full)
+    return outs[0], outs[1]
