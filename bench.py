@@ -211,6 +211,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-whole-slide", action="store_true",
+                    help="skip the 64K^2 whole-slide extras (recon + EDT)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -358,6 +360,15 @@ def main():
 
     if rank == 0 and world == 1 and not args.no_extras:
         line["extras"] = extras(L, _lib, dev, flush)
+    if not args.no_extras and not args.no_whole_slide:
+        del dJ, dI, out, ws, wsh
+        torch.cuda.empty_cache()
+        try:
+            ws_line = whole_slide(dev, rank, world, flush, peak)
+        except Exception as e:  # the headline line must still print
+            ws_line = {"whole_slide_error": f"{type(e).__name__}: {e}"[:300]}
+        if rank == 0:
+            line.setdefault("extras", {}).update(ws_line)
 
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -420,6 +431,123 @@ def extras(L, _lib, dev, flush):
         ms = timed(lambda: gw.reconstruct(dM, dK, conn), reps=3, warm=1)
         out[f"imfill_16k_c{conn}"] = {"ms": round(ms, 3), "mpx_s": round(n16 / ms / 1e3, 1)}
     return out
+
+
+WS_PX = 65536  # BASELINE configs[4]: 64K x 64K whole slide
+
+
+def whole_slide(dev, rank: int, world: int, flush, peak: float):
+    """BASELINE configs[4]: a 64K x 64K whole slide, reconstruction (u8,
+    8-conn, random marker/mask generated on the device) and EDT (the 4K
+    nuclei mask tiled 16 x 16), one GPU or horizontal slabs across the
+    ranks (NCCL border exchange + all-reduce termination, distributed.py).
+    Strong scaling: the slide is fixed, ``ms`` is the max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import oracle  # input generator only
+    import paper_1209_3314_b200 as gw
+    from paper_1209_3314_b200 import distributed as D
+
+    N = WS_PX
+    y0, y1 = D.slab_bounds(N, world, rank)
+    res = {}
+
+    def timed(fn, reps=2, warm=1):
+        for _ in range(warm):
+            fn()
+        ts = []
+        for i in range(reps):
+            flush.fill_(i & 0xff)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms = statistics.median(ts)
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    def entry(ms, bpp, **kw):
+        ach = bpp * N * N / (ms / 1e3) / 1e9
+        return {"ms": round(ms, 3), "mpx_s": round(N * N / ms / 1e3, 1), "n_gpus": world,
+                "roofline_frac": round(ach / (peak * world), 4), "alg_bytes_per_px": bpp, **kw}
+
+    # reconstruction: rank r generates its own rows (seeded per rank)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    I = torch.randint(0, 256, (y1 - y0, N), dtype=torch.uint8, device=dev, generator=g)
+    M = torch.clamp(I.to(torch.int16) - H_MARKER, min=0).to(torch.uint8)
+    info = {}
+    if world == 1:
+        def run():
+            info["J"] = gw.reconstruct(M, I, 8)
+        ms = timed(run)
+        ok = _fixed_point(info.pop("J"), I, M)
+        res["recon_64k_u8_c8"] = entry(ms, ALG_BYTES_PER_PX, fixed_point_equation=ok)
+    else:
+        def run():
+            slab = D.SlabRecon(M, I, rank > 0, rank + 1 < world, 8, D.device_solver)
+            info["waves"] = D.run_slab_dist(slab).waves
+        ms = timed(run)
+        res["recon_64k_u8_c8"] = entry(ms, ALG_BYTES_PER_PX, waves=info["waves"],
+                                       parallelism=f"slabs x{world}")
+    del I, M, info
+    torch.cuda.empty_cache()
+
+    # EDT: 4K nuclei mask tiled 16 x 16 (the rows of this rank + halo rows)
+    m4 = torch.from_numpy(oracle.gen_nuclei_mask(4096, 4096, 30.0, 7)).to(dev)
+    rows = torch.arange(max(y0 - 1, 0), min(y1 + 1, N), device=dev) % 4096
+    mrows = m4[rows].repeat(1, N // 4096)
+    if world == 1:
+        img = gw.Image2D(N, N, "binary", mrows)
+        info = {}
+
+        def run():
+            cfg = gw.EngineConfig()
+            gw.edt(img, gw.SE8, mode="parallel", cfg=cfg)
+            info["rounds"] = cfg.stats.rounds
+        ms = timed(run, reps=1)
+        res["edt_64k_nuclei_c8"] = entry(ms, 13, rounds=info["rounds"])
+    else:
+        ext = torch.zeros((y1 - y0 + 2, N), dtype=torch.uint8, device=dev)
+        top = 1 if y0 == 0 else 0  # no row above the image: ext row 0 stays zero
+        ext[top:top + mrows.shape[0]] = mrows
+        info = {}
+
+        def run():
+            slab = D.SlabEDT(ext, y0, N, rank > 0, rank + 1 < world, 8)
+            info["rounds"] = D.run_edt_slab_dist(slab)
+            slab.finalize()
+        ms = timed(run, reps=1)
+        res["edt_64k_nuclei_c8"] = entry(ms, 13, rounds=info["rounds"],
+                                         parallelism=f"slabs x{world}")
+    return res
+
+
+def _fixed_point(J, I, M) -> bool:
+    """Size-independent recon check (8-conn): marker <= J <= mask and
+    J = min(mask, max(J, dilate3x3(J))) everywhere."""
+    import torch
+    if not bool((J <= I).all()) or not bool((J >= M).all()):
+        return False
+    H = J.shape[0]
+    for y0 in range(0, H, 4096):
+        y1 = min(H, y0 + 4096)
+        a, b = max(0, y0 - 1), min(H, y1 + 1)
+        blk = torch.nn.functional.pad(J[a:b].float()[None, None], (1, 1, 1, 1), value=-1.0)
+        d = torch.nn.functional.max_pool2d(blk, 3, 1)[0, 0][y0 - a:y0 - a + (y1 - y0)]
+        if not bool((torch.minimum(I[y0:y1].float(), d) == J[y0:y1].float()).all()):
+            return False
+    return True
 
 
 if __name__ == "__main__":

@@ -95,6 +95,9 @@ typedef struct iwpp_recon_opts {
                         last image row is a halo row that changed; only the tile rows
                         holding or touching it are re-run (the rest of J must already be
                         at its fixed point) */
+  int pipeline_rows; /* iwpp_recon_host only: slab height of the transfer/compute pipeline
+                        (0 = auto, ~2 MB slabs; > 0 = this many rows, rounded up to the
+                        32-row tile side; < 0 = off: copy in, compute, copy out) */
 } iwpp_recon_opts;
 
 /* Timing helpers (events live in this library's CUDA runtime). */
@@ -165,6 +168,11 @@ int iwpp_edt_propagate(int64_t *vr, int64_t W, int64_t H, int conn,
                        const int64_t *seeds, int64_t n_seeds, void *workspace,
                        size_t workspace_bytes, int64_t max_rounds,
                        iwpp_stats *stats, void *stream);
+/* Engine selection for tests/diagnostics (process-wide, not thread-safe):
+ * 0 = auto (64-bit keys; range-checked with a CAS re-run when W, H exceed the
+ * 32-bit d^2 range), 1 = force the 32-bit-source CAS engine, 2 = force
+ * range-checked keys.  Results never depend on it. */
+int iwpp_edt_set_engine(int mode);
 /* finalize_distance_map (edt.py:272-281): dist = f32(sqrt(f64(d2))).
  * Returns IWPP_E_NO_BACKGROUND if any vr == -1.  d2 may be NULL. */
 int iwpp_edt_finalize(const int64_t *vr, int64_t W, int64_t H, float *dist,

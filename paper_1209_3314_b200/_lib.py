@@ -29,7 +29,7 @@ IWPP_E_OVERFLOW = -6
 EXPORTS = (
     "iwpp_last_error", "iwpp_version", "iwpp_device_info",
     "iwpp_recon_workspace_bytes", "iwpp_recon", "iwpp_recon_host_workspace_bytes",
-    "iwpp_recon_host", "iwpp_recon_engine_counters", "iwpp_check_le",
+    "iwpp_recon_host", "iwpp_recon_engine_counters", "iwpp_check_le", "iwpp_edt_set_engine",
     "iwpp_recon_sweep_rows", "iwpp_recon_sweep_cols",
     "iwpp_recon_seed_scan", "iwpp_edt_workspace_bytes", "iwpp_edt", "iwpp_edt_propagate",
     "iwpp_edt_finalize", "iwpp_edt_host_workspace_bytes", "iwpp_edt_host",
@@ -53,7 +53,7 @@ class ReconOpts(ctypes.Structure):
                 ("check_contract", ctypes.c_int), ("queue_capacity", ctypes.c_int),
                 ("tile_sweeps", ctypes.c_int), ("halo_sweep_threshold", ctypes.c_int),
                 ("ev_begin", ctypes.c_void_p), ("ev_end", ctypes.c_void_p),
-                ("slab_rows", ctypes.c_int)]
+                ("slab_rows", ctypes.c_int), ("pipeline_rows", ctypes.c_int)]
 
 
 _lib = None
@@ -91,6 +91,7 @@ def load_library(path: str = LIB_PATH):
             "iwpp_edt": ([P, I64, I64, I, P, P, P, SZ, I64, SP, P], I),
             "iwpp_edt_propagate": ([P, I64, I64, I, P, I64, P, SZ, I64, SP, P], I),
             "iwpp_edt_finalize": ([P, I64, I64, P, P, P, P], I),
+            "iwpp_edt_set_engine": ([I], I),
             "iwpp_edt_host_workspace_bytes": ([I64, I64, I], SZ),
             "iwpp_edt_host": ([P, I64, I64, I, P, P, P, SZ, I64, SP, P], I),
             "iwpp_event_create": ([ctypes.POINTER(P)], I),

@@ -2,8 +2,12 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <chrono>
 #include <mutex>
+#include <vector>
 
 #include "edt.cuh"
 #include "iwpp_common.cuh"
@@ -13,6 +17,7 @@
 namespace iwpp {
 
 static thread_local char g_err[512] = "";
+constexpr int kMaxSlabs = 256;
 
 int set_error(int status, const char *fmt, ...) {
   va_list ap;
@@ -158,9 +163,234 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
 }
 
 size_t iwpp_recon_host_workspace_bytes(int64_t W, int64_t H, int dtype, int conn) {
+  (void)conn;
   size_t img = align_up((size_t)W * H * elem_size(dtype), 256);
-  return 2 * img + recon_ws_bytes(W, H) + 256;
+  size_t nty = (size_t)((H + recon::TS - 1) / recon::TS);
+  return 2 * img + align_up(nty, 256) + recon_ws_bytes(W, H) + 512;
 }
+
+}  // extern "C"
+
+namespace iwpp {
+
+// Copy streams + events of the pipelined host path, one set per device
+// (created on first use; host calls on one device are serialised).
+struct HostPipe {
+  std::mutex m;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t start = nullptr, in[kMaxSlabs], ready[kMaxSlabs];
+};
+
+static int host_pipe(HostPipe *&hp) {
+  static HostPipe pipes[64];
+  int dev = 0;
+  IWPP_CUDA_TRY(cudaGetDevice(&dev));
+  hp = &pipes[dev & 63];
+  return IWPP_OK;
+}
+
+static int host_pipe_init(HostPipe &p) {
+  if (p.h2d) return IWPP_OK;
+  IWPP_CUDA_TRY(cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking));
+  IWPP_CUDA_TRY(cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking));
+  IWPP_CUDA_TRY(cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming));
+  for (int i = 0; i < kMaxSlabs; i++) {
+    IWPP_CUDA_TRY(cudaEventCreateWithFlags(&p.in[i], cudaEventDisableTiming));
+    IWPP_CUDA_TRY(cudaEventCreateWithFlags(&p.ready[i], cudaEventDisableTiming));
+  }
+  return IWPP_OK;
+}
+
+// Slab row bounds for the pipelined host path: slabs of ~4 MB of each image
+// (a multiple of the tile side, at least 8 tile rows), the last two tapered
+// to 1/2 and 1/4 of that so the compute + copy-back after the final H2D is
+// short.  `rows` > 0 forces uniform slabs of that height.  Returns false
+// (no pipelining) when the image is too small for two slabs.
+static bool host_slabs(int64_t W, int64_t H, size_t es, int64_t rows, std::vector<int64_t> &b) {
+  const int64_t TS = recon::TS;
+  b.clear();
+  bool taper = rows <= 0;
+  if (rows <= 0) {
+    rows = (int64_t)((size_t)(4u << 20) / ((size_t)W * es));
+    if (rows < 8 * TS) rows = 8 * TS;
+  }
+  rows = (rows + TS - 1) / TS * TS;
+  while ((H + rows - 1) / rows > kMaxSlabs - 2) rows *= 2;
+  if (H < 2 * rows) return false;
+  b.push_back(0);
+  int64_t tail = 0;
+  std::vector<int64_t> last;
+  if (taper) {
+    for (int64_t part : {rows / 4, rows / 2}) {
+      part = std::max<int64_t>(TS, part / TS * TS);
+      if (H - tail - part >= rows) {
+        last.push_back(part);
+        tail += part;
+      }
+    }
+  }
+  for (int64_t y = rows; y + rows / 2 < H - tail; y += rows) b.push_back(y);
+  int64_t y = H - tail;
+  for (auto it = last.rbegin(); it != last.rend(); ++it) {
+    b.push_back(y);
+    y += *it;
+  }
+  b.push_back(H);
+  return b.size() >= 3;
+}
+
+// Optional timeline of the pipelined host path (IWPP_TRACE=1 in the
+// environment): a one-thread kernel on each stream stamps %globaltimer when
+// the stream reaches it; printed to stderr at the end (diagnostics only).
+__global__ void trace_stamp_kernel(unsigned long long *slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = t;
+}
+
+struct Trace {
+  bool on = false;
+  int n = 0;
+  const char *what[256];
+  int idx[256];
+  unsigned long long *dev = nullptr;
+  Trace() {
+    const char *e = getenv("IWPP_TRACE");
+    on = e && e[0] == '1' && cudaMalloc(&dev, 256 * sizeof(unsigned long long)) == cudaSuccess;
+  }
+  void mark(cudaStream_t s, const char *w, int i) {
+    if (!on || n >= 256) return;
+    what[n] = w;
+    idx[n] = i;
+    trace_stamp_kernel<<<1, 1, 0, s>>>(dev + n);
+    n++;
+  }
+  ~Trace() {
+    if (!on) return;
+    unsigned long long t[256];
+    cudaDeviceSynchronize();
+    cudaMemcpy(t, dev, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < n; i++)
+      fprintf(stderr, "[iwpp trace] %8.3f ms  %s %d\n", (double)(t[i] - t[0]) * 1e-6, what[i], idx[i]);
+    cudaFree(dev);
+  }
+};
+
+// Pipelined e2e reconstruction (the reference-facing host call).
+//
+// The image streams in as horizontal slabs on a copy stream.  As soon as
+// slab k lands, one engine run over rows [0, end of slab k) processes the
+// slab's tiles and re-visits the tile row above its top cut: rows not yet
+// landed lie outside that run's image, so every intermediate state lies
+// between the marker and the true result, and each run carries raises across
+// the cut and on to wherever they reach (the fixed point is unique,
+// engine.py:9-18).  Once the cut below a slab has been crossed the slab is
+// copied back speculatively on a second copy stream while later slabs are
+// still arriving; every tile row a later run writes is flagged and copied
+// again at the end.  Transfers in both directions overlap the
+// compute, so the call costs ~ max(H2D, D2H) + one slab's compute.
+static int recon_host_pipelined(char *out, const char *marker, const char *mask, int64_t W,
+                                int64_t H, int dtype, int conn, const std::vector<int64_t> &bnd, char *dJ,
+                                char *dI, uint8_t *dirty, char *rest,
+                                const iwpp_recon_opts *opts, iwpp_stats *stats,
+                                cudaStream_t st) {
+  HostPipe *hp;
+  int rc = host_pipe(hp);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lock(hp->m);
+  if ((rc = host_pipe_init(*hp))) return rc;
+  const size_t es = elem_size(dtype), row_bytes = (size_t)W * es;
+  const int64_t TS = recon::TS, nty = (H + TS - 1) / TS;
+  const int S = (int)bnd.size() - 1;
+  Carver c2(rest);
+  ReconWs w = carve_recon(c2, W, H);
+  recon::EngineOpts eo;
+  if (opts) {
+    eo.max_blocks = opts->max_blocks;
+    eo.qcap = opts->queue_capacity;
+    if (opts->tile_sweeps >= 0) eo.sweeps = opts->tile_sweeps;
+    eo.halo_thresh = opts->halo_sweep_threshold;
+  }
+  Trace tr;
+  tr.mark(st, "start", 0);
+  IWPP_CUDA_TRY(cudaEventRecord(hp->start, st));
+  IWPP_CUDA_TRY(cudaStreamWaitEvent(hp->h2d, hp->start, 0));
+  IWPP_CUDA_TRY(cudaStreamWaitEvent(hp->d2h, hp->start, 0));
+  for (int k = 0; k < S; k++) {
+    size_t off = (size_t)bnd[k] * row_bytes;
+    size_t nb = (size_t)(bnd[k + 1] - bnd[k]) * row_bytes;
+    IWPP_CUDA_TRY(cudaMemcpyAsync(dJ + off, marker + off, nb, cudaMemcpyHostToDevice, hp->h2d));
+    IWPP_CUDA_TRY(cudaMemcpyAsync(dI + off, mask + off, nb, cudaMemcpyHostToDevice, hp->h2d));
+    IWPP_CUDA_TRY(cudaEventRecord(hp->in[k], hp->h2d));
+    tr.mark(hp->h2d, "h2d done", k);
+  }
+  IWPP_CUDA_TRY(cudaMemsetAsync(&w.counters[recon::CNT_VIOL], 0, sizeof(unsigned long long), st));
+  IWPP_CUDA_TRY(cudaMemsetAsync(dirty, 0, (size_t)nty, st));
+  auto copy_back = [&](int64_t r0, int64_t r1) -> int {  // rows [r0, r1) -> host (d2h)
+    size_t off = (size_t)r0 * row_bytes;
+    IWPP_CUDA_TRY(cudaMemcpyAsync(out + off, dJ + off, (size_t)(r1 - r0) * row_bytes,
+                                  cudaMemcpyDeviceToHost, hp->d2h));
+    return IWPP_OK;
+  };
+  for (int k = 0; k < S; k++) {
+    const int64_t y0 = bnd[k], y1 = bnd[k + 1];
+    size_t off = (size_t)y0 * row_bytes;
+    IWPP_CUDA_TRY(cudaStreamWaitEvent(st, hp->in[k], 0));
+    tr.mark(st, "compute begin", k);
+    if ((rc = recon::check_le(dJ + off, dI + off, (size_t)(y1 - y0) * W, dtype,
+                              &w.counters[recon::CNT_VIOL], st)))
+      return rc;
+    // Rows [0, y1): the slab's tiles (first visits) plus the tile row above
+    // the cut at y0 (re-visited with the slab's rows as its halo); a raise
+    // may run on into any earlier slab, so tile rows written are flagged.
+    // Rows below y1 have not landed: for this run they lie outside the image.
+    recon::EngineOpts so = eo;
+    so.init_mode = k == 0 ? recon::INIT_FULL : recon::INIT_CONTINUE;
+    so.keep_counters = k > 0;
+    so.sel_lo = k == 0 ? 0 : (int)(y0 / TS) - 1;
+    so.sel_hi = -1;
+    so.dirty = dirty;
+    if ((rc = recon::run_tile_engine(dJ, dI, (int)W, (int)y1, dtype, conn, w.q, w.counters, so, st)))
+      return rc;
+    tr.mark(st, "engine done", k);
+    if (k == 0) continue;
+    // slab k-1 (and, after the last slab, slab k) is final unless a later
+    // run reaches it: clear its flags, then copy it back
+    const int64_t p0 = bnd[k - 1], p1 = k == S - 1 ? H : y0;
+    IWPP_CUDA_TRY(cudaMemsetAsync(dirty + p0 / TS, 0, (size_t)((p1 + TS - 1) / TS - p0 / TS), st));
+    IWPP_CUDA_TRY(cudaEventRecord(hp->ready[k], st));
+    IWPP_CUDA_TRY(cudaStreamWaitEvent(hp->d2h, hp->ready[k], 0));
+    if ((rc = copy_back(p0, p1))) return rc;
+    tr.mark(hp->d2h, "d2h done", k - 1);
+  }
+  // tile rows written after their slab was copied: copy them again
+  std::vector<uint8_t> flags((size_t)nty);
+  unsigned long long viol = 0;
+  IWPP_CUDA_TRY(cudaMemcpyAsync(flags.data(), dirty, (size_t)nty, cudaMemcpyDeviceToHost, st));
+  IWPP_CUDA_TRY(cudaMemcpyAsync(&viol, &w.counters[recon::CNT_VIOL], sizeof viol,
+                                cudaMemcpyDeviceToHost, st));
+  IWPP_CUDA_TRY(cudaStreamSynchronize(st));
+  tr.mark(st, "flags read", 0);
+  for (int64_t t = 0; t < nty;) {
+    if (!flags[t]) {
+      t++;
+      continue;
+    }
+    int64_t e = t;
+    while (e < nty && flags[e]) e++;
+    if ((rc = copy_back(t * TS, std::min<int64_t>(H, e * TS)))) return rc;
+    t = e;
+  }
+  tr.mark(hp->d2h, "recopy done", 0);
+  IWPP_CUDA_TRY(cudaStreamSynchronize(hp->d2h));
+  if (viol) return set_error(IWPP_E_CONTRACT, "marker exceeds mask somewhere (%llu cells)", viol);
+  if (stats) return fill_recon_stats(w, stats, st);
+  return IWPP_OK;
+}
+
+}  // namespace iwpp
+
+extern "C" {
 
 int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, int64_t H,
                     int dtype, int conn, void *workspace, size_t workspace_bytes,
@@ -169,6 +399,8 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   if (rc) return rc;
   size_t es = elem_size(dtype);
   if (!es) return set_error(IWPP_E_CONTRACT, "unsupported dtype %d", dtype);
+  if (conn != 4 && conn != 8)
+    return set_error(IWPP_E_CONTRACT, "connectivity must be 4 or 8, got %d", conn);
   if (workspace_bytes < iwpp_recon_host_workspace_bytes(W, H, dtype, conn))
     return set_error(IWPP_E_WORKSPACE, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
@@ -176,8 +408,16 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   Carver c(workspace);
   char *dJ = c.take<char>(nb);
   char *dI = c.take<char>(nb);
+  uint8_t *dirty = c.take<uint8_t>((size_t)((H + recon::TS - 1) / recon::TS));
   char *rest = c.base + align_up(c.off, 256);
   size_t rest_bytes = workspace_bytes - align_up(c.off, 256);
+  std::vector<int64_t> bnd;
+  const bool pipelined =
+      !(opts && (opts->sweeps > 0 || opts->slab_rows || opts->pipeline_rows < 0)) &&
+      host_slabs(W, H, es, opts ? opts->pipeline_rows : 0, bnd);
+  if (pipelined)
+    return recon_host_pipelined((char *)out, (const char *)marker, (const char *)mask, W, H, dtype,
+                                conn, bnd, dJ, dI, dirty, rest, opts, stats, st);
   IWPP_CUDA_TRY(cudaMemcpyAsync(dJ, marker, nb, cudaMemcpyHostToDevice, st));
   IWPP_CUDA_TRY(cudaMemcpyAsync(dI, mask, nb, cudaMemcpyHostToDevice, st));
   // contract check (recon.py:60) fused into the same stream
@@ -188,7 +428,9 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   unsigned long long viol = 0;
   IWPP_CUDA_TRY(cudaMemcpyAsync(&viol, &w.counters[recon::CNT_VIOL], sizeof viol,
                                 cudaMemcpyDeviceToHost, st));
-  iwpp_recon_opts o = opts ? *opts : iwpp_recon_opts{-1, 0, 0, 0, -1, -1, nullptr, nullptr, 0};
+  iwpp_recon_opts o{};
+  if (opts) o = *opts;
+  else o.sweeps = o.tile_sweeps = o.halo_sweep_threshold = -1;
   o.check_contract = 0;
   if ((rc = iwpp_recon(dJ, dI, W, H, dtype, conn, rest, rest_bytes, &o, nullptr, stream))) return rc;
   IWPP_CUDA_TRY(cudaMemcpyAsync(out, dJ, nb, cudaMemcpyDeviceToHost, st));
@@ -284,7 +526,7 @@ static int edt_check(int64_t W, int64_t H, int conn, size_t ws, size_t need) {
   int rc = check_dims(W, H);
   if (rc) return rc;
   if (!edt::size_supported(W, H))
-    return set_error(IWPP_E_CONTRACT, "EDT on one device supports up to 65536 x 65535 (got %lld x %lld)",
+    return set_error(IWPP_E_CONTRACT, "EDT on one device supports up to 65536 x 65536 (got %lld x %lld)",
                      (long long)W, (long long)H);
   if (conn != 4 && conn != 8)
     return set_error(IWPP_E_CONTRACT, "connectivity must be 4 or 8, got %d", conn);
@@ -311,17 +553,61 @@ static int edt_finish(const edt::EdtState &s, iwpp_stats *stats, bool need_inf, 
   return IWPP_OK;
 }
 
+}  // extern "C"
+
+namespace iwpp {
+
+// init (from a mask, or from a user source map + seeds) + all rounds.  On
+// images whose squared distances may exceed 32 bits the key engine runs with
+// range-checked offers; if any offer was out of range it re-runs on the CAS
+// engine (same workspace).  `s` returns the state holding the result.
+static int edt_solve(edt::EdtState &s, void *workspace, int64_t W, int64_t H, int conn,
+                     const uint8_t *mask, const int64_t *vr_in, const int64_t *seeds,
+                     int64_t n_seeds, int64_t max_rounds, cudaStream_t st) {
+  int rc;
+  for (int attempt = 0; attempt < 2; attempt++) {
+    Carver c(workspace);
+    s = edt::carve_state(c, W, H, attempt == 1);
+    if ((rc = edt::reset_control(s, st))) return rc;
+    if (mask)
+      rc = edt::launch_init(mask, (int)W, (int)H, conn, s, st);
+    else
+      rc = edt::launch_import(vr_in, seeds, n_seeds, (int)W, (int)H, s, st);
+    if (rc) return rc;
+    if ((rc = edt::launch_rounds((int)W, (int)H, conn, s, (long long)max_rounds, st))) return rc;
+    if (!s.keycheck) return IWPP_OK;
+    unsigned long long c8[edt::EC_N];
+    if ((rc = edt::read_counters(s, c8, st))) return rc;
+    if (!c8[edt::EC_RANGE]) return IWPP_OK;
+    if (!edt::cas_supported(W, H))
+      return set_error(IWPP_E_OVERFLOW,
+                       "a squared distance exceeds 32 bits and the %lld x %lld image leaves no "
+                       "free source code for the CAS engine",
+                       (long long)W, (long long)H);
+  }
+  return IWPP_OK;
+}
+
+}  // namespace iwpp
+
+extern "C" {
+
+int iwpp_edt_set_engine(int mode) {
+  if (mode < edt::ENGINE_AUTO || mode > edt::ENGINE_KEYCHECK)
+    return set_error(IWPP_E_CONTRACT, "unknown EDT engine mode %d", mode);
+  edt::g_engine_override = mode;
+  return IWPP_OK;
+}
+
 int iwpp_edt(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *vr, float *dist,
              void *workspace, size_t workspace_bytes, int64_t max_rounds, iwpp_stats *stats,
              void *stream) {
   int rc = edt_check(W, H, conn, workspace_bytes, edt::state_bytes(W, H));
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  Carver c(workspace);
-  edt::EdtState s = edt::carve_state(c, W, H);
-  if ((rc = edt::reset_control(s, st))) return rc;
-  if ((rc = edt::launch_init(mask, (int)W, (int)H, conn, s, st))) return rc;
-  if ((rc = edt::launch_rounds((int)W, (int)H, conn, s, (long long)max_rounds, st))) return rc;
+  edt::EdtState s;
+  if ((rc = edt_solve(s, workspace, W, H, conn, mask, nullptr, nullptr, 0, max_rounds, st)))
+    return rc;
   if ((rc = edt::launch_finalize_auto(s, (int)W, (int)H, vr, dist, nullptr, st))) return rc;
   return edt_finish(s, stats, true, st);
 }
@@ -332,11 +618,9 @@ int iwpp_edt_propagate(int64_t *vr, int64_t W, int64_t H, int conn, const int64_
   int rc = edt_check(W, H, conn, workspace_bytes, edt::state_bytes(W, H));
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  Carver c(workspace);
-  edt::EdtState s = edt::carve_state(c, W, H);
-  if ((rc = edt::reset_control(s, st))) return rc;
-  if ((rc = edt::launch_import(vr, seeds, n_seeds, (int)W, (int)H, s, st))) return rc;
-  if ((rc = edt::launch_rounds((int)W, (int)H, conn, s, (long long)max_rounds, st))) return rc;
+  edt::EdtState s;
+  if ((rc = edt_solve(s, workspace, W, H, conn, nullptr, vr, seeds, n_seeds, max_rounds, st)))
+    return rc;
   if ((rc = edt::launch_finalize_auto(s, (int)W, (int)H, vr, nullptr, nullptr, st))) return rc;
   return edt_finish(s, stats, false, st);
 }
@@ -372,11 +656,10 @@ int iwpp_edt_host(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *
   uint8_t *dm = c.take<uint8_t>(n);
   int64_t *dvr = c.take<int64_t>(n);
   float *dd = c.take<float>(n);
-  edt::EdtState s = edt::carve_state(c, W, H);
+  char *rest = c.base + align_up(c.off, 256);
   IWPP_CUDA_TRY(cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, st));
-  if ((rc = edt::reset_control(s, st))) return rc;
-  if ((rc = edt::launch_init(dm, (int)W, (int)H, conn, s, st))) return rc;
-  if ((rc = edt::launch_rounds((int)W, (int)H, conn, s, (long long)max_rounds, st))) return rc;
+  edt::EdtState s;
+  if ((rc = edt_solve(s, rest, W, H, conn, dm, nullptr, nullptr, 0, max_rounds, st))) return rc;
   if ((rc = edt::launch_finalize_auto(s, (int)W, (int)H, dvr, dd, nullptr, st))) return rc;
   if (vr) IWPP_CUDA_TRY(cudaMemcpyAsync(vr, dvr, n * 8, cudaMemcpyDeviceToHost, st));
   if (dist) IWPP_CUDA_TRY(cudaMemcpyAsync(dist, dd, n * 4, cudaMemcpyDeviceToHost, st));

@@ -309,7 +309,12 @@ __global__ void edt_import_key_kernel(const int64_t *__restrict__ vr, int W, int
     } else if (v >= 0) {
       int sy = (int)(v / W), sx = (int)(v - (int64_t)sy * W);
       int py = (int)(p / (unsigned)W), px = (int)(p - (size_t)py * W);
-      k = make_key(px, py, ((uint32_t)sy << 16) | (uint32_t)sx);
+      bool ok;
+      k = make_key_checked(px, py, ((uint32_t)sy << 16) | (uint32_t)sx, ok);
+      if (!ok) {
+        k = KINF;
+        s.counters[EC_RANGE] = 1;
+      }
     }
     reinterpret_cast<ulonglong2 *>(s.keys)[p] = make_ulonglong2(k, k);
   }
@@ -333,7 +338,7 @@ __global__ void edt_seed_key_kernel(const int64_t *__restrict__ seeds, int64_t n
   if (blockIdx.x == 0 && threadIdx.x == 0) s.cnt[0] = (unsigned)n_seeds;
 }
 
-template <int CONN>
+template <int CONN, bool CHECK>
 __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, int H, EdtState s,
                                                                        long long max_rounds) {
   const unsigned FULL = 0xffffffffu;
@@ -389,7 +394,16 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
 #pragma unroll
           for (int k = 0; k < Nbr<CONN>::N; k++) {
             int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
-            nk[k] = make_key(qx, qy, src);
+            if (CHECK) {  // d2 beyond 32 bits: flag it (the host re-runs), never offer
+              bool ok;
+              nk[k] = make_key_checked(qx, qy, src, ok);
+              if (!ok) {
+                s.counters[EC_RANGE] = 1;
+                continue;
+              }
+            } else {
+              nk[k] = make_key(qx, qy, src);
+            }
             if (nk[k] < rq[k]) cand |= 1u << k;  // beats q's round-start key
           }
           // the offers, issued back to back (predicated, no branches)
@@ -458,18 +472,26 @@ __global__ void edt_finalize_key_kernel(EdtState s, int W, int H, int64_t *vr, f
 
 // ---- host side -------------------------------------------------------------
 
-static EdtState carve_any(Carver &c, int64_t W, int64_t H) {
+int g_engine_override = ENGINE_AUTO;
+
+// One layout for both engines: the key engine's 16 B/px key array doubles
+// as the CAS engine's two source buffers + stamps (12 B/px), so a key run
+// that overflows its range can re-run on the same workspace.
+static EdtState carve_any(Carver &c, int64_t W, int64_t H, bool cas) {
   size_t n = (size_t)W * H;
   EdtState s;
-  s.keymode = key_mode_ok(W, H) ? 1 : 0;
+  if (g_engine_override == ENGINE_CAS) cas = true;
+  s.keymode = cas ? 0 : 1;
+  s.keycheck = s.keymode && (!key_mode_ok(W, H) || g_engine_override == ENGINE_KEYCHECK);
+  unsigned long long *keys = c.take<unsigned long long>(2 * n);
   s.keys = nullptr;
   s.buf[0] = s.buf[1] = s.stamp = nullptr;
   if (s.keymode) {
-    s.keys = c.take<unsigned long long>(2 * n);
+    s.keys = keys;
   } else {
-    s.buf[0] = c.take<uint32_t>(n);
-    s.buf[1] = c.take<uint32_t>(n);
-    s.stamp = c.take<uint32_t>(n);
+    s.buf[0] = reinterpret_cast<uint32_t *>(keys);
+    s.buf[1] = s.buf[0] + n;
+    s.stamp = s.buf[1] + n;
   }
   s.F[0] = c.take<uint32_t>(n);
   s.F[1] = c.take<uint32_t>(n);
@@ -482,11 +504,18 @@ static EdtState carve_any(Carver &c, int64_t W, int64_t H) {
 
 size_t state_bytes(int64_t W, int64_t H) {
   Carver c(nullptr);
-  carve_any(c, W, H);
+  carve_any(c, W, H, false);
   return c.off + 256;
 }
 
-EdtState carve_state(Carver &c, int64_t W, int64_t H) { return carve_any(c, W, H); }
+EdtState carve_state(Carver &c, int64_t W, int64_t H, bool cas) { return carve_any(c, W, H, cas); }
+
+int read_counters(const EdtState &s, unsigned long long *c, cudaStream_t st) {
+  IWPP_CUDA_TRY(cudaMemcpyAsync(c, s.counters, sizeof(unsigned long long) * EC_N,
+                                cudaMemcpyDeviceToHost, st));
+  IWPP_CUDA_TRY(cudaStreamSynchronize(st));
+  return IWPP_OK;
+}
 
 static int grid_for(size_t n, int threads) {
   size_t b = (n + threads - 1) / threads;
@@ -543,11 +572,14 @@ int launch_import(const int64_t *vr, const int64_t *seeds, int64_t n_seeds, int 
 
 int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_rounds,
                   cudaStream_t st) {
-  void *kern = s.keymode ? (conn == 8 ? (void *)edt_rounds_key_kernel<8>
-                                      : (void *)edt_rounds_key_kernel<4>)
-                         : (conn == 8 ? (void *)edt_rounds_kernel<8> : (void *)edt_rounds_kernel<4>);
-  static int blocks_cache[4] = {0, 0, 0, 0};
-  int &blocks = blocks_cache[(conn == 8) + 2 * s.keymode];
+  void *kern = s.keymode
+                   ? (s.keycheck ? (conn == 8 ? (void *)edt_rounds_key_kernel<8, true>
+                                              : (void *)edt_rounds_key_kernel<4, true>)
+                                 : (conn == 8 ? (void *)edt_rounds_key_kernel<8, false>
+                                              : (void *)edt_rounds_key_kernel<4, false>))
+                   : (conn == 8 ? (void *)edt_rounds_kernel<8> : (void *)edt_rounds_kernel<4>);
+  static int blocks_cache[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int &blocks = blocks_cache[(conn == 8) + 2 * s.keymode + 4 * s.keycheck];
   if (blocks == 0) {
     int per_sm = 0;
     IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRoundThreads, 0));

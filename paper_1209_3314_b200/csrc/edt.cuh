@@ -15,6 +15,8 @@ enum { EC_ROUNDS = 0, EC_VISITS, EC_NINF, EC_LIMIT, EC_FINAL, EC_BAD, EC_RANGE, 
 
 struct EdtState {
   int keymode;               // 1: 64-bit keys (d2 << 32 | src), 0: 32-bit sources + CAS
+  int keycheck;              // keymode on an image whose d2 may exceed 32 bits: every offer
+                             // checks the range and flags EC_RANGE instead of wrapping
   unsigned long long *keys;  // keymode: 2 keys per cell (AoS, double-buffered)
   uint32_t *buf[2];          // !keymode: source per cell, (sy << 16 | sx), double-buffered
   uint32_t *stamp;           // !keymode: round stamp per cell (frontier dedupe)
@@ -24,10 +26,18 @@ struct EdtState {
   unsigned long long *counters;
 };
 
-// Images the 32-bit (y,x) code can address (INF must stay unused).
+// Images the 32-bit (y,x) source code can address.
 inline bool size_supported(int64_t W, int64_t H) {
-  return W >= 1 && H >= 1 && W <= 65536 && H <= 65536 && !(W == 65536 && H == 65536);
+  return W >= 1 && H >= 1 && W <= 65536 && H <= 65536;
 }
+// The CAS engine's INF code (all ones) must not be a cell's own code.
+inline bool cas_supported(int64_t W, int64_t H) {
+  return size_supported(W, H) && !(W == 65536 && H == 65536);
+}
+// Engine selection (tests / diagnostics): 0 auto, 1 force the CAS engine,
+// 2 force range-checked keys.
+enum { ENGINE_AUTO = 0, ENGINE_CAS = 1, ENGINE_KEYCHECK = 2 };
+extern int g_engine_override;
 // The key engine needs every squared distance to fit 32 bits.
 inline bool key_mode_ok(int64_t W, int64_t H) {
   return (uint64_t)(W - 1) * (W - 1) + (uint64_t)(H - 1) * (H - 1) < (1ull << 32);
@@ -42,6 +52,15 @@ __device__ __forceinline__ unsigned long long make_key(int qx, int qy, uint32_t 
   unsigned dx = (unsigned)abs(qx - sx), dy = (unsigned)abs(qy - sy);
   unsigned d2 = dx * dx + dy * dy;  // < 2^32 by key_mode_ok
   return ((unsigned long long)d2 << 32) | src;
+}
+// Range-checked key: d2 in 64 bits; *ok = false when it needs more than 32.
+__device__ __forceinline__ unsigned long long make_key_checked(int qx, int qy, uint32_t src,
+                                                               bool &ok) {
+  int sy = (int)(src >> 16), sx = (int)(src & 0xffffu);
+  unsigned long long dx = (unsigned)abs(qx - sx), dy = (unsigned)abs(qy - sy);
+  unsigned long long d2 = dx * dx + dy * dy;
+  ok = (d2 >> 32) == 0;
+  return (d2 << 32) | src;
 }
 
 size_t state_bytes(int64_t W, int64_t H);
@@ -58,7 +77,8 @@ int slab_round(void *ws, int64_t W, int64_t h, int64_t y0, int conn, int64_t r,
                cudaStream_t st);
 int slab_finalize(void *ws, int64_t W, int64_t h, int64_t y0, int64_t rounds, int64_t *vr,
                   float *dist, int64_t *n_inf_host, int64_t *range_err_host, cudaStream_t st);
-EdtState carve_state(Carver &c, int64_t W, int64_t H);
+EdtState carve_state(Carver &c, int64_t W, int64_t H, bool cas = false);
+int read_counters(const EdtState &s, unsigned long long *c, cudaStream_t st);
 int reset_control(const EdtState &s, cudaStream_t st);
 int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, cudaStream_t st);
 int launch_import(const int64_t *vr, const int64_t *seeds, int64_t n_seeds, int W, int H,

@@ -79,6 +79,7 @@ struct EngineArgs {
   unsigned halo_thresh;  // re-activation front above which to sweep first
   int sweeps;            // sweep passes on a tile's first visit
   int vec;               // rows are 16-byte aligned
+  uint8_t *dirty;        // per tile row: written by this run (nullable)
   TileQueue q;
 };
 
@@ -602,6 +603,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
       if (changed) {
         __syncwarp();
         store_tile<T>(a, s, x0, y0, limx, limy, lane);
+        if (a.dirty && l0) a.dirty[ty] = 1;
         // Which neighbour tiles can the changed border still raise?  Per
         // side, lane = position along it: cv = the border cell's value if it
         // changed since last published (else -inf); a halo cell needs its
@@ -699,7 +701,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
 
 // Initial GBQ: every tile, ordered by 2x2 colour class (then raster) so the
 // first wave of concurrently running tiles are never neighbours.
-__global__ void tile_queue_init_kernel(TileQueue q, int ntx, int nty, unsigned long long *counters) {
+__global__ void tile_queue_init_kernel(TileQueue q, int ntx, int nty, unsigned long long *counters,
+                                       int keep) {
   unsigned ntiles = (unsigned)ntx * nty;
   unsigned stride = gridDim.x * blockDim.x;
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -722,7 +725,7 @@ __global__ void tile_queue_init_kernel(TileQueue q, int ntx, int nty, unsigned l
     *q.tail = ntiles;
     *q.pending = ntiles;
   }
-  if (i < CNT_N) counters[i] = 0;
+  if (!keep && i < CNT_N) counters[i] = 0;
 }
 
 // Re-activation fill for slab runs (multi-GPU waves): only the tile rows
@@ -768,6 +771,44 @@ __global__ void tile_queue_init_rows_kernel(TileQueue q, int ntx, int nty, int t
   if (i < CNT_N) counters[i] = 0;
 }
 
+// INIT_CONTINUE: queue tile rows [lo, hi] (first visits, 2x2 colour order)
+// after the previous run's tickets.  Single CTA: it reads the previous run's
+// head/tail before publishing the new ones.  Slots are not cleared: every
+// stale slot holds a tag below `base`, so no later ticket can match it
+// before the ring wraps a full 2^32 tickets.
+__global__ void tile_queue_continue_kernel(TileQueue q, int ntx, int lo, int hi,
+                                           unsigned long long *counters, int keep) {
+  __shared__ unsigned base;
+  if (threadIdx.x == 0) {
+    unsigned h = *q.head, t = *q.tail;
+    base = (int)(h - t) > 0 ? h : t;
+  }
+  __syncthreads();
+  const int nty = hi - lo + 1;
+  const unsigned nq = (unsigned)ntx * nty;
+  unsigned cx[4], cy[4], cb[4];
+  for (int c = 0; c < 4; c++) {
+    cx[c] = (ntx - (c & 1) + 1) / 2;
+    cy[c] = (nty - (c >> 1) + 1) / 2;
+    cb[c] = c == 0 ? 0 : cb[c - 1] + cx[c - 1] * cy[c - 1];
+  }
+  for (unsigned i = threadIdx.x; i < nq; i += blockDim.x) {
+    unsigned tx = i % ntx, tyr = i / ntx;
+    unsigned c = (tx & 1) | ((tyr & 1) << 1);
+    unsigned pos = base + cb[c] + (tyr >> 1) * cx[c] + (tx >> 1);
+    unsigned t = (unsigned)(lo + tyr) * ntx + tx;
+    q.state[t] = ST_Q | ST_V;
+    q.ring[pos & q.mask] = ((unsigned long long)pos << 32) | t;
+  }
+  if (!keep && threadIdx.x < CNT_N) counters[threadIdx.x] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *q.head = base;
+    *q.tail = base + nq;
+    *q.pending = nq;
+  }
+}
+
 size_t tile_queue_bytes(unsigned ntiles) {
   Carver c(nullptr);
   carve_tile_queue(c, ntiles);
@@ -810,16 +851,22 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   if ((unsigned)blocks > max_b) blocks = (int)max_b;
   unsigned ib = (q.mask + 1 + 255) / 256;
   if (ib > 1024) ib = 1024;
-  if (o.rows_mode)
+  if (o.init_mode == INIT_CONTINUE) {
+    int lo = o.sel_lo < 0 ? 0 : o.sel_lo;
+    int hi = (o.sel_hi < 0 || o.sel_hi >= nty) ? nty - 1 : o.sel_hi;
+    if (lo > hi) return IWPP_OK;  // nothing to queue
+    tile_queue_continue_kernel<<<1, 1024, 0, st>>>(q, ntx, lo, hi, counters, o.keep_counters);
+  } else if (o.rows_mode) {
     tile_queue_init_rows_kernel<<<ib, 256, 0, st>>>(q, ntx, nty, o.rows_mode & 1,
                                                      (o.rows_mode >> 1) & 1, counters);
-  else
-    tile_queue_init_kernel<<<ib, 256, 0, st>>>(q, ntx, nty, counters);
+  } else {
+    tile_queue_init_kernel<<<ib, 256, 0, st>>>(q, ntx, nty, counters, o.keep_counters);
+  }
   IWPP_CUDA_TRY(cudaGetLastError());
   unsigned qlimit = (o.qcap > 0 && o.qcap < RQ) ? (unsigned)o.qcap : (unsigned)RQ;
   unsigned hth = o.halo_thresh >= 0 ? (unsigned)o.halo_thresh : kHaloSweepThreshold;
   bool vec = ((size_t)W * sizeof(T)) % 16 == 0 && (uintptr_t)J % 16 == 0 && (uintptr_t)I % 16 == 0;
-  EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, q};
+  EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, o.dirty, q};
   if (o.ev_begin) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_begin, st));
   kern<<<blocks, kCtaThreads, smem, st>>>(a, counters);
   IWPP_CUDA_TRY(cudaGetLastError());

@@ -45,7 +45,17 @@ struct EngineOpts {
   void *ev_begin = nullptr, *ev_end = nullptr;  // cudaEvent_t around the engine kernel
   int rows_mode = 0;     // 0: every tile, first visit; bit0 / bit1: only the top / bottom
                          // tile row, as re-visits (slab waves after a halo exchange)
+  // Queue initialisation.  INIT_FULL resets the ring (clears every slot) and
+  // queues every tile.  INIT_CONTINUE keeps the ring's ticket sequence of the
+  // previous run on this workspace (no clearing: stale slots carry older
+  // tags) and queues tile rows [sel_lo, sel_hi] as first visits; every other
+  // tile must be idle (it is after any completed run).
+  int init_mode = 0;
+  int sel_lo = 0, sel_hi = -1;  // INIT_CONTINUE: tile-row range (-1 = last row)
+  uint8_t *dirty = nullptr;     // optional: set to 1 for each tile row the run wrote
+  bool keep_counters = false;   // accumulate into the device counters (no reset)
 };
+enum { INIT_FULL = 0, INIT_CONTINUE = 1 };
 
 size_t tile_queue_bytes(unsigned ntiles);
 TileQueue carve_tile_queue(Carver &c, unsigned ntiles);

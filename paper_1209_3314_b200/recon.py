@@ -75,13 +75,15 @@ def _count_violations(m: Image2D, i: Image2D) -> int:
 # the device engine
 
 def _opts(cfg: EngineConfig | None, sweeps: int = -1, tile_sweeps: int = -1,
-          halo_sweep_threshold: int = -1, max_blocks: int = 0) -> _lib.ReconOpts:
+          halo_sweep_threshold: int = -1, max_blocks: int = 0,
+          pipeline_rows: int = 0) -> _lib.ReconOpts:
     o = _lib.ReconOpts()
     o.sweeps = sweeps
     o.max_blocks = max_blocks
     o.check_contract = 0
     o.tile_sweeps = tile_sweeps
     o.halo_sweep_threshold = halo_sweep_threshold
+    o.pipeline_rows = pipeline_rows
     if cfg is not None and cfg.queue.gbq_capacity is not None:
         o.queue_capacity = int(cfg.queue.gbq_capacity)
     else:
@@ -91,12 +93,14 @@ def _opts(cfg: EngineConfig | None, sweeps: int = -1, tile_sweeps: int = -1,
 
 def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
                 sweeps: int = -1, stats: dict | None = None, tile_sweeps: int = -1,
-                halo_sweep_threshold: int = -1, max_blocks: int = 0):
+                halo_sweep_threshold: int = -1, max_blocks: int = 0, pipeline_rows: int = 0):
     """Reconstruction of raw arrays (numpy -> numpy, CUDA tensor -> tensor).
 
     The marker is not modified.  ``stats`` (a dict) receives the device
     counters when given (this synchronizes the stream).  The remaining
-    keywords are engine tuning knobs (results never depend on them).
+    keywords are engine tuning knobs (results never depend on them);
+    ``pipeline_rows`` sets the slab height of the host path's transfer /
+    compute pipeline (0 = auto, < 0 = off).
     """
     L = _lib.lib()
     from .grid import np_dtype_of, is_device_array
@@ -107,7 +111,7 @@ def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
     H, W = marker.shape
     st = _lib.Stats()
     sp = _lib.ctypes.byref(st) if stats is not None else None
-    opts = _opts(cfg, sweeps, tile_sweeps, halo_sweep_threshold, max_blocks)
+    opts = _opts(cfg, sweeps, tile_sweeps, halo_sweep_threshold, max_blocks, pipeline_rows)
     if is_device_array(marker):
         torch = _lib._torch()
         J = marker.clone()

@@ -20,7 +20,7 @@ if "recon" in which:
   for n, conn in [(4096, 8), (4096, 4)]:
     J, I = oracle.gray_pair(n, 0, h=40)
     dJ, dI = torch.from_numpy(J).cuda(), torch.from_numpy(I).cuda()
-    for sw, tsw in [(0, 0), (0, 1), (0, 2)]:
+    for sw, tsw in [(0, 0), (0, 1), (0, 2), (0, 3), (0, 4)]:
         st = {}
         gw.reconstruct(dJ, dI, conn, sweeps=sw, tile_sweeps=tsw, stats=st)
         med, mn = timeit(lambda: gw.reconstruct(dJ, dI, conn, sweeps=sw, tile_sweeps=tsw))

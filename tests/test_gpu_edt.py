@@ -171,3 +171,67 @@ def test_tie_cases_counted_against_exact(gw):
         assert (d2 >= ex).all()
         if conn == 8:
             assert int((d2 > ex).sum()) == 0  # 8-conn refgen mask equals exact
+
+
+# ---------------------------------------------------------------------------
+# engine variants: the 32-bit-source CAS engine (used when a squared distance
+# leaves the 32-bit key range) and the range-checked key engine must give the
+# same canonical result as the default key engine.
+
+@pytest.fixture
+def engine_mode(gw):
+    from paper_1209_3314_b200 import _lib
+    L = _lib.lib()
+
+    def set_mode(m):
+        _lib.check(L.iwpp_edt_set_engine(m), "set_engine")
+    yield set_mode
+    set_mode(0)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("conn", [4, 8])
+def test_engine_variants_vs_oracle(gw, engine_mode, mode, conn):
+    engine_mode(mode)
+    rng = np.random.default_rng(77 + conn)
+    masks = [oracle.gen_synthetic_mask(300, 200, 50, 7),
+             (rng.random((129, 257)) < 0.9).astype(np.uint8) * 255]
+    for name in ENAMES[:6]:
+        if name.endswith("c%d" % conn) and not np.isnan(EZ[name + "__dist"]).all():
+            masks.append(EZ[name + "__mask"])
+    for m in masks:
+        if not (m == 0).any():
+            continue
+        vr_ref, d_ref = oracle.edt(m, conn)
+        vmap, dist = gw.edt(_img(gw, m, True), gw.StructuringElement(conn))
+        assert np.array_equal(_np(vmap.vr), vr_ref)
+        assert _np(dist.data).tobytes() == d_ref.tobytes()
+    # edt_propagate through the variant
+    m = masks[0]
+    vr_ref, _ = oracle.edt(m, conn)
+    vmap, seeds = gw.init_packed(_img(gw, m, True), gw.StructuringElement(conn))
+    gw.edt_propagate(vmap, seeds, gw.StructuringElement(conn))
+    assert np.array_equal(_np(vmap.vr), vr_ref)
+
+
+def test_key_range_overflow_reruns_exactly(gw):
+    """46342^2 with one background cell in a corner: the far corner's d^2 is
+    2 * 46341^2 > 2^32, beyond the 64-bit key's d^2 field.  The range-checked
+    key run flags it and the CAS engine re-runs; with a single source every
+    cell's source is that cell, so the exact answer is known in closed form."""
+    t = _t()
+    n = 46342
+    free = t.cuda.mem_get_info()[0]
+    if free < 90 << 30:
+        pytest.skip("needs ~90 GB of free device memory")
+    m = t.full((n, n), 255, dtype=t.uint8, device="cuda")
+    m[0, 0] = 0
+    vmap, dist = gw.edt(gw.Image2D(n, n, "binary", m), gw.SE8)
+    del m
+    assert bool((vmap.vr == 0).all())
+    corner = float(np.float32(np.sqrt(np.float64(2 * (n - 1) ** 2))))
+    assert float(dist.data[n - 1, n - 1]) == corner
+    ys = t.arange(0, n, 4097, device="cuda", dtype=t.float64)
+    got = dist.data[::4097, ::4097].double()
+    want = t.sqrt(ys[:, None] ** 2 + ys[None, :] ** 2).float().double()
+    assert bool((got == want).all())

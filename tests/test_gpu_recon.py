@@ -231,3 +231,57 @@ def test_sweeps_option_same_result(gw):
         got = gw.reconstruct(_torch().from_numpy(J).cuda(), _torch().from_numpy(I).cuda(), 8,
                              sweeps=sweeps)
         assert np.array_equal(got.cpu().numpy(), want)
+
+
+# ---------------------------------------------------------------------------
+# host path (iwpp_recon_host): slabs stream in and are reconstructed while
+# later slabs are still in flight, then each cut is repaired; results must
+# not depend on the slab height.
+
+@pytest.mark.parametrize("conn", [4, 8])
+@pytest.mark.parametrize("rows", [-1, 32, 64, 96, 256])
+def test_host_pipeline_any_slab_height(gw, conn, rows):
+    for shape, seed in [((1000, 300), 1), ((513, 700), 2), ((64, 33), 3)]:
+        J, I = oracle.gray_pair(shape, seed, h=40)
+        want = oracle.recon_fh(J, I, conn)
+        st = {}
+        got = gw.reconstruct(J, I, conn, pipeline_rows=rows, stats=st)
+        assert np.array_equal(got, want), (shape, rows)
+        assert st["contract_violations"] == 0
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_host_pipeline_long_range_imfill(gw, conn):
+    """imfill: raises cross many cuts (the fill enters from the image border
+    and runs through every slab), so later repairs rewrite earlier slabs."""
+    bw = oracle.gen_synthetic_mask(512, 2048, 50, 7)
+    marker, mask = oracle.imfill_pair(bw)
+    want = oracle.recon_fh(marker, mask, conn)
+    for rows in (0, 32, 128):
+        got = gw.reconstruct(marker, mask, conn, pipeline_rows=rows)
+        assert np.array_equal(got, want), rows
+    # a marker seeded only in the last row: everything propagates upwards
+    # through every cut after the earlier slabs were already copied back
+    I = np.full((1024, 256), 200, np.uint8)
+    I[::3, 1:] = 0  # a serpentine corridor
+    M = np.zeros_like(I)
+    M[-1, 0] = 200
+    want = oracle.recon_fh(M, I, conn)
+    for rows in (32, 64):
+        assert np.array_equal(gw.reconstruct(M, I, conn, pipeline_rows=rows), want)
+
+
+def test_host_pipeline_4k_auto(gw):
+    """The auto slab height at BASELINE configs[1] (4096^2 u8)."""
+    J, I = oracle.gray_pair(4096, 0, h=40)
+    want = oracle.recon_fh(J, I, 8)
+    assert np.array_equal(gw.reconstruct(J, I, 8), want)
+
+
+def test_host_pipeline_contract_in_late_slab(gw):
+    J, I = oracle.gray_pair((600, 128), 4, h=40)
+    J[590, 100] = 255
+    I[590, 100] = 3
+    from paper_1209_3314_b200 import _lib
+    with pytest.raises(gw.ContractViolation):
+        gw.reconstruct(J, I, 8, pipeline_rows=64)
