@@ -569,12 +569,27 @@ static int edt_solve(edt::EdtState &s, void *workspace, int64_t W, int64_t H, in
     Carver c(workspace);
     s = edt::carve_state(c, W, H, attempt == 1);
     if ((rc = edt::reset_control(s, st))) return rc;
-    if (mask)
+    if (s.block)
+      rc = edt::block_init(mask, vr_in, seeds, n_seeds, (int)W, (int)H, conn, s, st);
+    else if (mask)
       rc = edt::launch_init(mask, (int)W, (int)H, conn, s, st);
     else
       rc = edt::launch_import(vr_in, seeds, n_seeds, (int)W, (int)H, s, st);
     if (rc) return rc;
-    if ((rc = edt::launch_rounds((int)W, (int)H, conn, s, (long long)max_rounds, st))) return rc;
+    if (s.block)
+      rc = edt::block_rounds((int)W, (int)H, conn, s, (long long)max_rounds, st);
+    else
+      rc = edt::launch_rounds((int)W, (int)H, conn, s, (long long)max_rounds, st);
+    if (rc) return rc;
+    if (s.block && getenv("IWPP_TRACE") && getenv("IWPP_TRACE")[0] == '1') {
+      unsigned long long d[16];
+      cudaMemcpy(d, s.diag, sizeof d, cudaMemcpyDeviceToHost);
+      fprintf(stderr,
+              "[iwpp edt block] region-passes %llu (empty %llu, with frontier out %llu) items %llu "
+              "local-rounds %llu rounds %llu | cycles/region-pass load %.0f rounds %.0f out %.0f\n",
+              d[0], d[1], d[7], d[2], d[3], d[8], (double)d[4] / (d[0] - d[1] + 1e-9),
+              (double)d[5] / (d[0] - d[1] + 1e-9), (double)d[6] / (d[0] - d[1] + 1e-9));
+    }
     if (!s.keycheck) return IWPP_OK;
     unsigned long long c8[edt::EC_N];
     if ((rc = edt::read_counters(s, c8, st))) return rc;
@@ -593,7 +608,7 @@ static int edt_solve(edt::EdtState &s, void *workspace, int64_t W, int64_t H, in
 extern "C" {
 
 int iwpp_edt_set_engine(int mode) {
-  if (mode < edt::ENGINE_AUTO || mode > edt::ENGINE_KEYCHECK)
+  if (mode < edt::ENGINE_AUTO || mode > edt::ENGINE_BLOCK)
     return set_error(IWPP_E_CONTRACT, "unknown EDT engine mode %d", mode);
   edt::g_engine_override = mode;
   return IWPP_OK;

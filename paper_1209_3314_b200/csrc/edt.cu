@@ -56,24 +56,6 @@ __device__ __forceinline__ void cas_min(uint32_t *WR, size_t q, int qx, int qy, 
   }
 }
 
-__device__ void grid_barrier(unsigned *count, unsigned *gen, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned g = ld_acquire(gen);
-    __threadfence();
-    unsigned arrived = atomicAdd(count, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      while (ld_acquire(gen) == g) __nanosleep(16);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 // ---- init: fused assign (K.339-348) + contour seeds (K.351-373) -----------
 template <int CONN>
 __global__ void edt_init_kernel(const uint8_t *__restrict__ mask, int W, int H, EdtState s) {
@@ -495,10 +477,28 @@ static EdtState carve_any(Carver &c, int64_t W, int64_t H, bool cas) {
   }
   s.F[0] = c.take<uint32_t>(n);
   s.F[1] = c.take<uint32_t>(n);
-  unsigned *ctl = c.take<unsigned>(8);
+  unsigned *ctl = c.take<unsigned>(16);
   s.cnt = ctl;      // [0..2]
   s.bar = ctl + 4;  // [4..5]
+  s.acnt = ctl + 8;  // [8..10]
+  s.wc = ctl + 12;   // [12..14]
   s.counters = c.take<unsigned long long>(EC_N);
+  // block engine: two planes over the same 2n keys, frontier bitmaps, regions
+  s.block = s.keymode && g_engine_override != ENGINE_QUEUE &&
+            (g_engine_override == ENGINE_BLOCK || (int64_t)n >= kBlockMinCells);
+  s.plane[0] = keys;
+  s.plane[1] = keys + n;
+  const size_t words = (size_t)((W + 31) / 32) * H;
+  s.fbits[0] = c.take<uint32_t>(words);
+  s.fbits[1] = c.take<uint32_t>(words);
+  const size_t nreg = (size_t)block_regions(W, H);
+  s.rplane = c.take<unsigned>(nreg);
+  s.fstamp[0] = c.take<unsigned>(nreg);
+  s.fstamp[1] = c.take<unsigned>(nreg);
+  s.astamp = c.take<unsigned>(nreg);
+  s.rflag = c.take<unsigned>(nreg);
+  for (int i = 0; i < 3; i++) s.alist[i] = c.take<unsigned>(nreg);
+  s.diag = c.take<unsigned long long>(16);
   return s;
 }
 
@@ -639,6 +639,7 @@ __global__ void edt_select_final_kernel(EdtState s, int W, int H, int64_t *vr, f
 
 int launch_finalize_auto(const EdtState &s, int W, int H, int64_t *vr, float *dist, int64_t *d2,
                          cudaStream_t st) {
+  if (s.block) return block_finalize(s, W, H, vr, dist, d2, st);
   size_t n = (size_t)W * H;
   if (s.keymode)
     edt_finalize_key_kernel<<<grid_for(n, 256), 256, 0, st>>>(s, W, H, vr, dist, d2);

@@ -11,7 +11,7 @@ constexpr int kRoundThreads = 512;
 constexpr int kRoundBlocksPerSm = 2;
 constexpr int kEdtBq = 6144;  // per-block next-frontier buffer (shared memory, 24 KB)
 
-enum { EC_ROUNDS = 0, EC_VISITS, EC_NINF, EC_LIMIT, EC_FINAL, EC_BAD, EC_RANGE, EC_N = 8 };
+enum { EC_ROUNDS = 0, EC_VISITS, EC_NINF, EC_LIMIT, EC_FINAL, EC_BAD, EC_RANGE, EC_LASTCHG, EC_N = 8 };
 
 struct EdtState {
   int keymode;               // 1: 64-bit keys (d2 << 32 | src), 0: 32-bit sources + CAS
@@ -24,6 +24,17 @@ struct EdtState {
   unsigned *cnt;             // [3] frontier sizes (triple-buffered)
   unsigned *bar;             // [2] grid barrier count / generation
   unsigned long long *counters;
+  // block engine (edt_block.cu)
+  int block;                 // keymode runs on the temporally blocked engine
+  unsigned long long *plane[2];  // block engine: two key planes (no interleave)
+  uint32_t *fbits[2];        // frontier bitmaps (row-major, ceil(W/32) words per row)
+  unsigned *rplane;          // per region: (pass << 1) | plane holding its current keys
+  unsigned *fstamp[2];       // per region: pass for which fbits[b] holds its frontier
+  unsigned *astamp;          // per region: last pass it was activated for
+  unsigned *rflag;           // per region: holds seeds (init)
+  unsigned *alist[3];        // active region lists (triple-buffered)
+  unsigned *acnt, *wc;       // [3] list sizes, [3] work counters
+  unsigned long long *diag;  // [16] block-engine diagnostics (IWPP_TRACE)
 };
 
 // Images the 32-bit (y,x) source code can address.
@@ -36,7 +47,10 @@ inline bool cas_supported(int64_t W, int64_t H) {
 }
 // Engine selection (tests / diagnostics): 0 auto, 1 force the CAS engine,
 // 2 force range-checked keys.
-enum { ENGINE_AUTO = 0, ENGINE_CAS = 1, ENGINE_KEYCHECK = 2 };
+enum { ENGINE_AUTO = 0, ENGINE_CAS = 1, ENGINE_KEYCHECK = 2, ENGINE_QUEUE = 3, ENGINE_BLOCK = 4 };
+// auto: the temporally blocked engine from this many cells up (measured on
+// B200: it wins on whole-slide images, the frontier queue on 4K tiles)
+constexpr int64_t kBlockMinCells = (int64_t)1 << 25;
 extern int g_engine_override;
 // The key engine needs every squared distance to fit 32 bits.
 inline bool key_mode_ok(int64_t W, int64_t H) {
@@ -63,6 +77,25 @@ __device__ __forceinline__ unsigned long long make_key_checked(int qx, int qy, u
   return (d2 << 32) | src;
 }
 
+// Software grid barrier for the persistent cooperative kernels.
+__device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned g = ld_acquire(gen);
+    __threadfence();
+    unsigned arrived = atomicAdd(count, 1u);
+    if (arrived == nblocks - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (ld_acquire(gen) == g) __nanosleep(16);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 size_t state_bytes(int64_t W, int64_t H);
 
 // slab engine (edt_slab.cu): one round per launch, halo items from the
@@ -87,6 +120,20 @@ int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_round
                   cudaStream_t st);
 int launch_finalize_auto(const EdtState &s, int W, int H, int64_t *vr, float *dist, int64_t *d2,
                          cudaStream_t st);
+// block engine (edt_block.cu)
+constexpr int kBlockShift = 6;
+constexpr int kBlockC = 1 << kBlockShift;  // region side (central cells)
+constexpr int kBlockK = 8;                 // halo width = local rounds per pass
+constexpr int kBlockThreads = 512;
+constexpr int kBlockMinCtas = 2;
+inline int64_t block_regions(int64_t W, int64_t H) {
+  return ((W + kBlockC - 1) / kBlockC) * ((H + kBlockC - 1) / kBlockC);
+}
+int block_init(const uint8_t *mask, const int64_t *vr, const int64_t *seeds, int64_t n_seeds,
+               int W, int H, int conn, const EdtState &s, cudaStream_t st);
+int block_rounds(int W, int H, int conn, const EdtState &s, long long max_rounds, cudaStream_t st);
+int block_finalize(const EdtState &s, int W, int H, int64_t *vr, float *dist, int64_t *d2,
+                   cudaStream_t st);
 int launch_finalize_vr(const int64_t *vr, int W, int H, float *dist, int64_t *d2,
                        unsigned long long *counters, cudaStream_t st);
 

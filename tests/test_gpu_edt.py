@@ -189,13 +189,14 @@ def engine_mode(gw):
     set_mode(0)
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
 @pytest.mark.parametrize("conn", [4, 8])
 def test_engine_variants_vs_oracle(gw, engine_mode, mode, conn):
     engine_mode(mode)
     rng = np.random.default_rng(77 + conn)
     masks = [oracle.gen_synthetic_mask(300, 200, 50, 7),
-             (rng.random((129, 257)) < 0.9).astype(np.uint8) * 255]
+             (rng.random((129, 257)) < 0.9).astype(np.uint8) * 255,
+             oracle.gen_synthetic_mask(700, 517, 60, 3)]  # many passes, ragged regions
     for name in ENAMES[:6]:
         if name.endswith("c%d" % conn) and not np.isnan(EZ[name + "__dist"]).all():
             masks.append(EZ[name + "__mask"])
@@ -206,6 +207,14 @@ def test_engine_variants_vs_oracle(gw, engine_mode, mode, conn):
         vmap, dist = gw.edt(_img(gw, m, True), gw.StructuringElement(conn))
         assert np.array_equal(_np(vmap.vr), vr_ref)
         assert _np(dist.data).tobytes() == d_ref.tobytes()
+    # max_rounds through the variant: EngineError exactly when not converged
+    m = masks[2]
+    _, _, (rounds, _) = oracle.edt(m, conn, stats=True)
+    cfg = gw.EngineConfig(max_rounds=rounds)
+    gw.edt(_img(gw, m, True), gw.StructuringElement(conn), mode="parallel", cfg=cfg)
+    with pytest.raises(gw.EngineError):
+        gw.edt(_img(gw, m, True), gw.StructuringElement(conn), mode="parallel",
+               cfg=gw.EngineConfig(max_rounds=rounds - 2))
     # edt_propagate through the variant
     m = masks[0]
     vr_ref, _ = oracle.edt(m, conn)
