@@ -91,6 +91,12 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
 __device__ __forceinline__ void st_release64(unsigned long long *p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Acquire/release fence at GPU scope (MEMBAR.ALL.GPU): enough for the
+// message-passing patterns of the engines (publish data, then a flag / queue
+// slot; observe the flag, then read the data).  __threadfence() is a
+// sequentially consistent fence (MEMBAR.SC.GPU), which is costlier.
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -165,19 +165,36 @@ __device__ __forceinline__ bool activate_claim(const TileQueue &q, unsigned t) {
 template <typename T>
 __device__ void load_halo(const EngineArgs &a, WarpSmem<T> &s, int x0, int y0, int lane) {
   constexpr int LO = (int)Elem<T>::lo;
-  for (int h = lane; h < RING; h += 32) {
-    int lx, ly;
-    halo_cell(h, lx, ly);
-    int gx = x0 + lx - 1, gy = y0 + ly - 1;
-    int i = sidx(lx, ly);
-    s.I[i] = Elem<T>::lo;  // never raisable from inside the tile
-    if (gx >= 0 && gx < a.W && gy >= 0 && gy < a.H) {
-      size_t g = (size_t)gy * a.W + gx;
-      s.J[i] = (int)ld_cg((const T *)a.J + g);
-      s.Ih[h] = __ldg((const T *)a.I + g);
-    } else {
-      s.J[i] = LO;
-      s.Ih[h] = Elem<T>::lo;
+  constexpr int NH = (RING + 31) / 32;
+  // all of the lane's halo loads first (independent), then the stores
+  int jv[NH];
+  T iv[NH];
+#pragma unroll
+  for (int k = 0; k < NH; k++) {
+    const int h = lane + 32 * k;
+    jv[k] = LO;
+    iv[k] = Elem<T>::lo;
+    if (h < RING) {
+      int lx, ly;
+      halo_cell(h, lx, ly);
+      const int gx = x0 + lx - 1, gy = y0 + ly - 1;
+      if (gx >= 0 && gx < a.W && gy >= 0 && gy < a.H) {
+        const size_t g = (size_t)gy * a.W + gx;
+        jv[k] = (int)ld_cg((const T *)a.J + g);
+        iv[k] = __ldg((const T *)a.I + g);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NH; k++) {
+    const int h = lane + 32 * k;
+    if (h < RING) {
+      int lx, ly;
+      halo_cell(h, lx, ly);
+      const int i = sidx(lx, ly);
+      s.I[i] = Elem<T>::lo;  // never raisable from inside the tile
+      s.J[i] = jv[k];
+      s.Ih[h] = iv[k];
     }
   }
 }
@@ -306,7 +323,7 @@ __device__ __forceinline__ bool walk_line(WarpSmem<T> &s, int first, int carry_i
   constexpr int C = 8;
   int v = s.J[carry_idx];
   bool chg = false;
-#pragma unroll
+#pragma unroll 1
   for (int k0 = 0; k0 < TS; k0 += C) {
     int j[C], m[C];
 #pragma unroll
@@ -325,14 +342,60 @@ __device__ __forceinline__ bool walk_line(WarpSmem<T> &s, int first, int carry_i
   return chg;
 }
 
-template <typename T>
+// Column walk, lane = column.  8-connectivity takes the three cells of the
+// previous row (K.142-190: {NW, N, NE} forward, {SW, S, SE} backward): the
+// diagonal values come from the neighbouring lanes' registers (lanes 0 / 31
+// read the side halo column), so a diagonal wavefront crosses the tile in
+// one walk instead of being left to the queue.
+template <int CONN, int DIR, typename T>
+__device__ __forceinline__ bool walk_col(WarpSmem<T> &s, int lane) {
+  if (CONN == 4) {
+    const int k = lane + 1;
+    return DIR > 0 ? walk_line<PS>(s, sidx(k, 1), sidx(k, 0))
+                   : walk_line<-PS>(s, sidx(k, TS), sidx(k, TS + 1));
+  }
+  const int x = lane + 1;
+  const int y0 = DIR > 0 ? 1 : TS, yc = DIR > 0 ? 0 : TS + 1;
+  const bool edge = lane == 0 || lane == 31;
+  const int side = lane == 0 ? 0 : TS + 1;
+  int v = s.J[sidx(x, yc)];
+  int sv = edge ? s.J[sidx(side, yc)] : INT_MIN;
+  bool chg = false;
+  constexpr int C = 8;
+#pragma unroll 1
+  for (int k0 = 0; k0 < TS; k0 += C) {
+    int j[C], m[C], sn[C];
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+      const int y = y0 + DIR * (k0 + c);
+      j[c] = s.J[sidx(x, y)];
+      m[c] = (int)s.I[sidx(x, y)];
+      sn[c] = edge ? s.J[sidx(side, y)] : INT_MIN;
+    }
+#pragma unroll
+    for (int c = 0; c < C; c++) {
+      int l = __shfl_up_sync(FULL, v, 1), r = __shfl_down_sync(FULL, v, 1);
+      if (lane == 0) l = sv;
+      if (lane == 31) r = sv;
+      const int nv = clampi(max(v, max(l, r)), j[c], m[c]);
+      chg |= nv != j[c];
+      s.J[sidx(x, y0 + DIR * (k0 + c))] = nv;
+      v = nv;
+      sv = sn[c];
+    }
+  }
+  return chg;
+}
+
+template <int CONN, typename T>
 __device__ bool sweep_pass(WarpSmem<T> &s, int lane) {
   const int k = lane + 1;
   bool chg = walk_line<1>(s, sidx(1, k), sidx(0, k));
   chg |= walk_line<-1>(s, sidx(TS, k), sidx(TS + 1, k));
   __syncwarp();
-  chg |= walk_line<PS>(s, sidx(k, 1), sidx(k, 0));
-  chg |= walk_line<-PS>(s, sidx(k, TS), sidx(k, TS + 1));
+  chg |= walk_col<CONN, 1>(s, lane);
+  __syncwarp();
+  chg |= walk_col<CONN, -1>(s, lane);
   __syncwarp();
   return __any_sync(FULL, chg);
 }
@@ -373,6 +436,7 @@ __device__ unsigned detect_full(WarpSmem<T> &s, unsigned t, unsigned qlimit, int
   lr_p = lr_c;
   mrow(1, m_c, j_c);
   lr_c = lr_of(m_c, lane);
+#pragma unroll 4
   for (int y = 1; y <= TS; y++) {
     int m_n, j_n;
     mrow(y + 1, m_n, j_n);
@@ -397,25 +461,38 @@ __device__ bool sweep_detect(WarpSmem<T> &s, unsigned &t, unsigned qlimit, int l
   bool chg = walk_line<1>(s, sidx(1, k), sidx(0, k));
   chg |= walk_line<-1>(s, sidx(TS, k), sidx(TS + 1, k));
   __syncwarp();
-  chg |= walk_line<PS>(s, sidx(k, 1), sidx(k, 0));
+  chg |= walk_col<CONN, 1>(s, lane);
   __syncwarp();
   int v = s.J[sidx(x, TS + 1)];
+  const bool edge = lane == 0 || lane == 31;
+  const int side = lane == 0 ? 0 : TS + 1;
+  int sv = edge ? s.J[sidx(side, TS + 1)] : INT_MIN;
   // window (n, c, p) = rows (y, y+1, y+2); start with c = row TS+1 (halo),
   // p = beyond: both +inf
   int m_c = INT_MAX, lr_c = INT_MAX, j_c = 0, m_p = INT_MAX, lr_p = INT_MAX;
   constexpr int C = 8;
-#pragma unroll
+#pragma unroll 1
   for (int k0 = 0; k0 < TS; k0 += C) {
     int j[C], mm[C];
+    int sn[C];
 #pragma unroll
     for (int c = 0; c < C; c++) {
       j[c] = s.J[sidx(x, TS - k0 - c)];
       mm[c] = (int)s.I[sidx(x, TS - k0 - c)];
+      sn[c] = (CONN == 8 && edge) ? s.J[sidx(side, TS - k0 - c)] : INT_MIN;
     }
 #pragma unroll
     for (int c = 0; c < C; c++) {
       const int y = TS - k0 - c;
-      int nv = clampi(v, j[c], mm[c]);
+      int in = v;
+      if (CONN == 8) {  // {SW, S, SE} of the row below (K.142-190 backward)
+        int l = __shfl_up_sync(FULL, v, 1), r = __shfl_down_sync(FULL, v, 1);
+        if (lane == 0) l = sv;
+        if (lane == 31) r = sv;
+        in = max(v, max(l, r));
+        sv = sn[c];
+      }
+      int nv = clampi(in, j[c], mm[c]);
       chg |= nv != j[c];
       s.J[sidx(x, y)] = nv;
       v = nv;
@@ -468,7 +545,7 @@ __device__ void tile_fixpoint(WarpSmem<T> &s, unsigned qlimit, bool full, int sw
       if (full && !swept && sweeps > 0) {
         swept = true;
         n = 0;
-        for (int sp = 1; sp < sweeps; sp++) changed |= sweep_pass(s, lane);
+        for (int sp = 1; sp < sweeps; sp++) changed |= sweep_pass<CONN>(s, lane);
         changed |= sweep_detect<CONN>(s, n, qlimit, lane);
         if (l0) ph[2] += clock64() - d0;
       } else if (full) {
@@ -564,7 +641,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
       t = next_tile >= 0 ? next_tile : ring_pop(a.q);
       if (t >= 0) {
         unsigned old = atomicExch(&a.q.state[t], ST_R);
-        __threadfence();
+        fence_acq_rel();
         first = old & ST_V;
       }
     }
@@ -643,7 +720,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
           if (__any_sync(FULL, c6)) dirs |= 1u << 6;
           if (__any_sync(FULL, c8)) dirs |= 1u << 8;
         }
-        __threadfence();  // publish the interior before any neighbour is (re)queued
+        fence_acq_rel();  // publish the interior before any neighbour is (re)queued
         __syncwarp();
         // one lane per direction claims the neighbour; the warp keeps one
         // claimed idle neighbour as its own continuation (no queue round
@@ -672,12 +749,12 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
       if (l0) {
         unsigned old = atomicCAS(&a.q.state[t], ST_R, 0u);
         if (old == ST_R) {
-          __threadfence();
+          fence_acq_rel();
           atomicSub(a.q.pending, 1u);
           done = 1;
         } else {
           atomicExch(&a.q.state[t], ST_R);  // consume the request (acquire)
-          __threadfence();
+          fence_acq_rel();
         }
       }
       done = __shfl_sync(FULL, done, 0);
