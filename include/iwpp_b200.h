@@ -40,6 +40,8 @@ enum iwpp_dtype {
   IWPP_U8 = 0,  /* "u8" and "binary" */
   IWPP_U16 = 1, /* "u16" */
   IWPP_I32 = 2, /* "i32" (not an Image2D kind in the reference; its kernels accept it) */
+  IWPP_F32 = 3, /* "f32": runs the int32 engine on an order-preserving bit map of the
+                   floats (-0.0 is taken as +0.0; NaN fails the marker <= mask contract) */
 };
 
 enum iwpp_status {

@@ -50,6 +50,7 @@ static size_t elem_size(int dtype) {
     case IWPP_U8: return 1;
     case IWPP_U16: return 2;
     case IWPP_I32: return 4;
+    case IWPP_F32: return 4;
   }
   return 0;
 }
@@ -102,9 +103,10 @@ int iwpp_device_info(int device, int *sm_count, int *cc_major, int *cc_minor) {
 // ---------------------------------------------------------------- recon
 
 size_t iwpp_recon_workspace_bytes(int64_t W, int64_t H, int dtype, int conn) {
-  (void)dtype;
   (void)conn;
-  return recon_ws_bytes(W, H);
+  size_t b = recon_ws_bytes(W, H);
+  if (dtype == IWPP_F32) b += align_up((size_t)W * H * 4, 256) + 256;  // the mask as ordered ints
+  return b;
 }
 
 static int fill_recon_stats(const ReconWs &w, iwpp_stats *stats, cudaStream_t st) {
@@ -130,12 +132,24 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
   if (conn != 4 && conn != 8)
     return set_error(IWPP_E_CONTRACT, "connectivity must be 4 or 8, got %d", conn);
   if (!elem_size(dtype)) return set_error(IWPP_E_CONTRACT, "unsupported dtype %d", dtype);
-  if (workspace_bytes < recon_ws_bytes(W, H))
+  if (workspace_bytes < iwpp_recon_workspace_bytes(W, H, dtype, conn))
     return set_error(IWPP_E_WORKSPACE, "workspace too small (%zu < %zu)", workspace_bytes,
-                     recon_ws_bytes(W, H));
+                     iwpp_recon_workspace_bytes(W, H, dtype, conn));
   cudaStream_t st = (cudaStream_t)stream;
   Carver c(workspace);
   ReconWs w = carve_recon(c, W, H);
+  if (dtype == IWPP_F32) {  // int32 engine on order-preserving ints, then back
+    const size_t n = (size_t)W * H;
+    void *Io = c.take<int32_t>(n);
+    if ((rc = recon::f32_to_ord(J, J, n, st))) return rc;
+    if ((rc = recon::f32_to_ord(I, Io, n, st))) return rc;
+    iwpp_recon_opts o{};
+    if (opts) o = *opts;
+    else o.sweeps = o.tile_sweeps = o.halo_sweep_threshold = -1;
+    rc = iwpp_recon(J, Io, W, H, IWPP_I32, conn, workspace, recon_ws_bytes(W, H), &o, stats, stream);
+    int rc2 = recon::ord_to_f32(J, J, n, st);
+    return rc ? rc : rc2;
+  }
   int sweeps = opts ? opts->sweeps : -1;
   if (sweeps < 0) sweeps = 0;  // auto: the tile engine alone (measured best on random inputs)
   for (int s = 0; s < sweeps; s++) {
@@ -413,6 +427,7 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   size_t rest_bytes = workspace_bytes - align_up(c.off, 256);
   std::vector<int64_t> bnd;
   const bool pipelined =
+      dtype != IWPP_F32 &&
       !(opts && (opts->sweeps > 0 || opts->slab_rows || opts->pipeline_rows < 0)) &&
       host_slabs(W, H, es, opts ? opts->pipeline_rows : 0, bnd);
   if (pipelined)
@@ -432,7 +447,14 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   if (opts) o = *opts;
   else o.sweeps = o.tile_sweeps = o.halo_sweep_threshold = -1;
   o.check_contract = 0;
-  if ((rc = iwpp_recon(dJ, dI, W, H, dtype, conn, rest, rest_bytes, &o, nullptr, stream))) return rc;
+  int edtype = dtype;
+  if (dtype == IWPP_F32) {  // our own device copies: convert in place
+    if ((rc = recon::f32_to_ord(dJ, dJ, (size_t)W * H, st))) return rc;
+    if ((rc = recon::f32_to_ord(dI, dI, (size_t)W * H, st))) return rc;
+    edtype = IWPP_I32;
+  }
+  if ((rc = iwpp_recon(dJ, dI, W, H, edtype, conn, rest, rest_bytes, &o, nullptr, stream))) return rc;
+  if (dtype == IWPP_F32 && (rc = recon::ord_to_f32(dJ, dJ, (size_t)W * H, st))) return rc;
   IWPP_CUDA_TRY(cudaMemcpyAsync(out, dJ, nb, cudaMemcpyDeviceToHost, st));
   IWPP_CUDA_TRY(cudaStreamSynchronize(st));
   if (viol) return set_error(IWPP_E_CONTRACT, "marker exceeds mask somewhere (%llu cells)", viol);

@@ -275,7 +275,7 @@ __global__ void check_le_kernel(const T *__restrict__ J, const T *__restrict__ I
   unsigned long long c = 0;
   for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
        p += (size_t)gridDim.x * blockDim.x)
-    c += J[p] > I[p];
+    c += !(J[p] <= I[p]);  // a NaN anywhere is a violation (recon.py:60, np.all(m <= i))
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(viol, c);
 }
@@ -367,8 +367,43 @@ int check_le(const void *J, const void *I, size_t n, int dtype, unsigned long lo
       break;
     case IWPP_U16: check_le_kernel<uint16_t><<<g, 256, 0, st>>>((const uint16_t *)J, (const uint16_t *)I, n, viol); break;
     case IWPP_I32: check_le_kernel<int32_t><<<g, 256, 0, st>>>((const int32_t *)J, (const int32_t *)I, n, viol); break;
+    case IWPP_F32: check_le_kernel<float><<<g, 256, 0, st>>>((const float *)J, (const float *)I, n, viol); break;
     default: return set_error(IWPP_E_CONTRACT, "unsupported dtype %d", dtype);
   }
+  IWPP_CUDA_TRY(cudaGetLastError());
+  return IWPP_OK;
+}
+
+// f32 <-> order-preserving int32: non-negative floats keep their bits,
+// negative floats flip the magnitude bits, so signed-int order = float order
+// (the engines then run their int32 path: hardware atomicMax, same fixed
+// point).  -0.0 maps to +0.0 (they compare equal as floats).  NaN never
+// reaches the engine: the marker <= mask contract rejects it.
+__global__ void f32_to_ord_kernel(const uint32_t *__restrict__ src, int32_t *__restrict__ dst,
+                                  size_t n) {
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (size_t)gridDim.x * blockDim.x) {
+    uint32_t b = src[p];
+    if (b == 0x80000000u) b = 0u;
+    dst[p] = (int32_t)b >= 0 ? (int32_t)b : (int32_t)(b ^ 0x7FFFFFFFu);
+  }
+}
+__global__ void ord_to_f32_kernel(const int32_t *__restrict__ src, uint32_t *__restrict__ dst,
+                                  size_t n) {
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (size_t)gridDim.x * blockDim.x) {
+    int32_t v = src[p];
+    dst[p] = v >= 0 ? (uint32_t)v : ((uint32_t)v ^ 0x7FFFFFFFu);
+  }
+}
+
+int f32_to_ord(const void *src, void *dst, size_t n, cudaStream_t st) {
+  f32_to_ord_kernel<<<grid_cap(n, 256), 256, 0, st>>>((const uint32_t *)src, (int32_t *)dst, n);
+  IWPP_CUDA_TRY(cudaGetLastError());
+  return IWPP_OK;
+}
+int ord_to_f32(const void *src, void *dst, size_t n, cudaStream_t st) {
+  ord_to_f32_kernel<<<grid_cap(n, 256), 256, 0, st>>>((const int32_t *)src, (uint32_t *)dst, n);
   IWPP_CUDA_TRY(cudaGetLastError());
   return IWPP_OK;
 }

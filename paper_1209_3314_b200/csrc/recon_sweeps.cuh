@@ -13,6 +13,9 @@ int seed_scan(const void *J, const void *I, int W, int H, int dtype, int conn, i
               unsigned long long *n_out, cudaStream_t st);
 int check_le(const void *J, const void *I, size_t n, int dtype, unsigned long long *viol,
              cudaStream_t st);
+// f32 <-> order-preserving int32 (in place allowed)
+int f32_to_ord(const void *src, void *dst, size_t n, cudaStream_t st);
+int ord_to_f32(const void *src, void *dst, size_t n, cudaStream_t st);
 
 }  // namespace recon
 }  // namespace iwpp

@@ -105,7 +105,8 @@ def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
     L = _lib.lib()
     from .grid import np_dtype_of, is_device_array
     dt = np_dtype_of(marker)
-    code = {np.dtype(np.uint8): 0, np.dtype(np.uint16): 1, np.dtype(np.int32): 2}.get(dt)
+    code = {np.dtype(np.uint8): 0, np.dtype(np.uint16): 1, np.dtype(np.int32): 2,
+            np.dtype(np.float32): 3}.get(dt)
     if code is None:
         raise ContractViolation(f"no device engine for dtype {dt}")
     H, W = marker.shape

@@ -84,6 +84,13 @@ def main():
     J = np.maximum(I.astype(np.int64) - 2**28, -2**31).astype(np.int32)
     for conn in (4, 8):
         recon[f"i32_128_22_c{conn}"] = (J, I, recon_ref_kernels(J, I, conn))
+    # f32 (a reference Image2D kind): signed values, ties, a flat plateau
+    rng = np.random.default_rng(23)
+    I = (rng.standard_normal((80, 96)) * 1000.0).astype(np.float32)
+    I[10:20, 10:30] = np.float32(12.5)
+    J = (I - np.float32(300.0)).astype(np.float32)
+    for conn in (4, 8):
+        recon[f"f32_80x96_23_c{conn}"] = (J, I, recon_ref(J, I, conn, "f32"))
     # binary: component selection + imfill
     rng = np.random.default_rng(1004)
     for i in range(4):

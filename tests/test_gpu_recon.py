@@ -33,7 +33,7 @@ def _torch():
 def _kind(a, name=""):
     if name.startswith(("bin", "imfill")):
         return "binary"
-    return {np.uint8: "u8", np.uint16: "u16", np.int32: "i32"}[a.dtype.type]
+    return {np.uint8: "u8", np.uint16: "u16", np.int32: "i32", np.float32: "f32"}[a.dtype.type]
 
 
 def _pair(gw, J, I, conn, kind, device):
@@ -285,3 +285,36 @@ def test_host_pipeline_contract_in_late_slab(gw):
     from paper_1209_3314_b200 import _lib
     with pytest.raises(gw.ContractViolation):
         gw.reconstruct(J, I, 8, pipeline_rows=64)
+
+
+# ---------------------------------------------------------------------------
+# f32 (a reference Image2D kind): the int32 engine on order-preserving bits
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_f32_random_vs_oracle(gw, conn):
+    rng = np.random.default_rng(300 + conn)
+    for shape in [(1, 1), (37, 300), (257, 129), (1024, 768)]:
+        I = (rng.standard_normal(shape) * 1e3).astype(np.float32)
+        I[::7, ::5] = np.float32(-1e30)  # deep negatives
+        J = (I - np.float32(250.0)).astype(np.float32)
+        want = oracle.recon_fh(J, I, conn)
+        got_d = gw.reconstruct(_torch().from_numpy(J).cuda(), _torch().from_numpy(I).cuda(), conn)
+        assert got_d.cpu().numpy().tobytes() == want.tobytes(), shape
+        got_h = gw.reconstruct(J, I, conn)  # host path (C ABI, H2D/D2H inside)
+        assert got_h.tobytes() == want.tobytes(), shape
+
+
+def test_f32_operator_api_and_nan_contract(gw):
+    rng = np.random.default_rng(5)
+    I = rng.random((64, 80)).astype(np.float32)
+    J = (I * np.float32(0.5)).astype(np.float32)
+    want = oracle.recon_fh(J, I, 8)
+    for device in (False, True):
+        out = gw.recon_fh(_pair(gw, J, I, 8, "f32", device))
+        assert out.elem_kind == "f32"
+        assert _np(out.data).tobytes() == want.tobytes()
+    Jn = J.copy()
+    Jn[3, 3] = np.nan  # NaN <= x is false: recon.py:60 rejects it
+    for device in (False, True):
+        with pytest.raises(gw.ContractViolation):
+            _pair(gw, Jn, I, 8, "f32", device)
