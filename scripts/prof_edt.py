@@ -7,6 +7,9 @@ import paper_1209_3314_b200 as gw
 kind, n, conn = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 m = oracle.gen_synthetic_mask(n, n, 50, 7) if kind == "blob" else oracle.gen_nuclei_mask(n, n, 30.0, 7)
+if os.environ.get("EDT_ENGINE"):  # 3 = frontier queue, 4 = temporally blocked
+    from paper_1209_3314_b200 import _lib
+    _lib.lib().iwpp_edt_set_engine(int(os.environ["EDT_ENGINE"]))
 img = gw.Image2D(n, n, "binary", torch.from_numpy(m).cuda())
 cfg = gw.EngineConfig()
 gw.edt(img, gw.StructuringElement(conn), mode="parallel", cfg=cfg)
