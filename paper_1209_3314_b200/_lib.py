@@ -53,7 +53,7 @@ class ReconOpts(ctypes.Structure):
                 ("check_contract", ctypes.c_int), ("queue_capacity", ctypes.c_int),
                 ("tile_sweeps", ctypes.c_int), ("halo_sweep_threshold", ctypes.c_int),
                 ("ev_begin", ctypes.c_void_p), ("ev_end", ctypes.c_void_p),
-                ("slab_rows", ctypes.c_int), ("pipeline_rows", ctypes.c_int)]
+                ("slab_rows", ctypes.c_int), ("pipeline_rows", ctypes.c_int), ("engine", ctypes.c_int)]
 
 
 _lib = None

@@ -160,7 +160,11 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
   if (opts) {
     eo.max_blocks = opts->max_blocks;
     eo.qcap = opts->queue_capacity;
-    if (opts->tile_sweeps >= 0) eo.sweeps = opts->tile_sweeps;
+    if (opts->tile_sweeps >= 0) {
+      eo.sweeps = opts->tile_sweeps;
+      eo.sweeps_set = 1;
+    }
+    eo.engine = opts->engine;
     eo.halo_thresh = opts->halo_sweep_threshold;
     eo.ev_begin = opts->ev_begin;
     eo.ev_end = opts->ev_end;
@@ -322,7 +326,11 @@ static int recon_host_pipelined(char *out, const char *marker, const char *mask,
   if (opts) {
     eo.max_blocks = opts->max_blocks;
     eo.qcap = opts->queue_capacity;
-    if (opts->tile_sweeps >= 0) eo.sweeps = opts->tile_sweeps;
+    if (opts->tile_sweeps >= 0) {
+      eo.sweeps = opts->tile_sweeps;
+      eo.sweeps_set = 1;
+    }
+    eo.engine = opts->engine;
     eo.halo_thresh = opts->halo_sweep_threshold;
   }
   Trace tr;

@@ -749,7 +749,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
       if (l0) {
         unsigned old = atomicCAS(&a.q.state[t], ST_R, 0u);
         if (old == ST_R) {
-          fence_acq_rel();
+          // no fence: pending is only ever changed by RMWs, whose per-location
+          // order already puts our activations' increments before this
           atomicSub(a.q.pending, 1u);
           done = 1;
         } else {
@@ -772,6 +773,313 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
     atomicAdd(&counters[CNT_PUSHES], n_push);
     atomicAdd(&counters[CNT_OVERFLOW], n_over);
     atomicAdd(&counters[CNT_SEEDS], n_seeds);
+    for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
+  }
+}
+
+// --- register engine (u8) -------------------------------------------------------
+//
+// One warp holds one 32 x 32 u8 tile in registers: lane = row, 8 words of 4
+// packed pixels for J and for I.  The tile's fixed point (given its halo) is
+// reached by Jacobi steps on the packed bytes,
+//     J <- max(J, min(I, max over N(p) of J)),
+// with the 3 x 3 (8-conn) / cross (4-conn) maximum built from byte-SIMD max
+// (vmaxu4), funnel shifts for the row neighbours and shfl for the rows above
+// and below.  Each step is a valid set of raise operations of the reference
+// rule (recon.py:92-101, K.220-270), so the unique fixed point is unchanged;
+// on random marker/mask pairs a tile converges in ~8 steps of ~100
+// instructions, with no shared memory at all.  The queue protocol (pop,
+// activation of the neighbours a changed border can still raise, finish,
+// re-run) is the same as the shared-memory engine's.
+struct RegHalo {
+  unsigned row[8], rowI[8];  // lane 0: the row above the tile; lane 31: the row below
+  unsigned l, r, lI, rI;     // the cells left / right of my row (J, I)
+  unsigned cl, cr, clI, crI; // lane 0: corners above; lane 31: corners below
+};
+
+__device__ __forceinline__ void reg_load_row(const uint8_t *base, int W, int x0, int gy, int H,
+                                             bool vec, bool cg, unsigned *w) {
+  if (gy < 0 || gy >= H) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) w[k] = 0;
+    return;
+  }
+  const uint8_t *p = base + (size_t)gy * W + x0;
+  if (vec && x0 + TS <= W) {
+    const uint4 a = cg ? __ldcg(reinterpret_cast<const uint4 *>(p)) : __ldg(reinterpret_cast<const uint4 *>(p));
+    const uint4 b = cg ? __ldcg(reinterpret_cast<const uint4 *>(p) + 1)
+                       : __ldg(reinterpret_cast<const uint4 *>(p) + 1);
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    unsigned v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      const int x = x0 + 4 * k + b;
+      if (x < W) v |= (unsigned)(cg ? ld_cg(p + 4 * k + b) : __ldg(p + 4 * k + b)) << (8 * b);
+    }
+    w[k] = v;
+  }
+}
+
+__device__ __forceinline__ unsigned reg_cell(const uint8_t *base, int W, int H, int gx, int gy,
+                                             bool cg) {
+  if (gx < 0 || gx >= W || gy < 0 || gy >= H) return 0u;
+  const uint8_t *p = base + (size_t)gy * W + gx;
+  return cg ? (unsigned)ld_cg(p) : (unsigned)__ldg(p);
+}
+
+__device__ __forceinline__ void reg_load_halo(const EngineArgs &a, int x0, int y0, int lane,
+                                              RegHalo &h) {
+  const uint8_t *J = (const uint8_t *)a.J, *I = (const uint8_t *)a.I;
+  const int gy = y0 + lane;
+  const int hy = lane == 0 ? y0 - 1 : (lane == 31 ? y0 + TS : -1);
+  h.l = reg_cell(J, a.W, a.H, x0 - 1, gy, true);
+  h.r = reg_cell(J, a.W, a.H, x0 + TS, gy, true);
+  h.lI = reg_cell(I, a.W, a.H, x0 - 1, gy, false);
+  h.rI = reg_cell(I, a.W, a.H, x0 + TS, gy, false);
+  h.cl = reg_cell(J, a.W, a.H, x0 - 1, hy, true);
+  h.cr = reg_cell(J, a.W, a.H, x0 + TS, hy, true);
+  h.clI = reg_cell(I, a.W, a.H, x0 - 1, hy, false);
+  h.crI = reg_cell(I, a.W, a.H, x0 + TS, hy, false);
+  reg_load_row(J, a.W, x0, hy, a.H, a.vec, true, h.row);
+  reg_load_row(I, a.W, x0, hy, a.H, a.vec, false, h.rowI);
+}
+
+// 16-bit lane SIMD (VIMNMX.U16x2: one instruction for two pixels)
+__device__ __forceinline__ unsigned max2(unsigned a, unsigned b) {
+  unsigned r;
+  asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned min2(unsigned a, unsigned b) {
+  unsigned r;
+  asm("min.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// Jacobi steps to the tile's fixed point; returns the number of steps.
+// The row's 32 pixels are split into even / odd pixels, two per word as
+// 16-bit lanes: e[k] = (p[4k], p[4k+2]), o[k] = (p[4k+1], p[4k+3]).  Then a
+// pixel's left / right neighbours are the other parity's word (same word or
+// one funnel shift away) and every max/min is one VIMNMX.U16x2.
+template <int CONN>
+__device__ __forceinline__ int reg_fixpoint(unsigned *j, const unsigned *m, const RegHalo &h,
+                                            int lane, bool &changed) {
+  constexpr unsigned LO8 = 0x00FF00FFu;
+  unsigned e[8], o[8], ie[8], io[8], he[8], ho[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    e[k] = j[k] & LO8;
+    o[k] = (j[k] >> 8) & LO8;
+    ie[k] = m[k] & LO8;
+    io[k] = (m[k] >> 8) & LO8;
+    he[k] = h.row[k] & LO8;
+    ho[k] = (h.row[k] >> 8) & LO8;
+  }
+  // the halo columns' values (vertical maxima for 8-conn) are constant
+  unsigned hlv = h.l, hrv = h.r;
+  if (CONN == 8) {
+    unsigned lu = __shfl_up_sync(FULL, h.l, 1), ld = __shfl_down_sync(FULL, h.l, 1);
+    unsigned ru = __shfl_up_sync(FULL, h.r, 1), rd = __shfl_down_sync(FULL, h.r, 1);
+    if (lane == 0) { lu = h.cl; ru = h.cr; }
+    if (lane == 31) { ld = h.cl; rd = h.cr; }
+    hlv = max(h.l, max(lu, ld));
+    hrv = max(h.r, max(ru, rd));
+  }
+  int steps = 0;
+  for (;;) {
+    steps++;
+    unsigned ve[8], vo[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      unsigned ue = __shfl_up_sync(FULL, e[k], 1), de = __shfl_down_sync(FULL, e[k], 1);
+      unsigned uo = __shfl_up_sync(FULL, o[k], 1), dn = __shfl_down_sync(FULL, o[k], 1);
+      if (lane == 0) { ue = he[k]; uo = ho[k]; }
+      if (lane == 31) { de = he[k]; dn = ho[k]; }
+      ve[k] = CONN == 8 ? max2(e[k], max2(ue, de)) : max2(ue, de);
+      vo[k] = CONN == 8 ? max2(o[k], max2(uo, dn)) : max2(uo, dn);
+    }
+    unsigned ch = 0;
+    if (CONN == 8) {
+      // 3x3 max = horizontal max of the vertical maxima
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const unsigned lE = __funnelshift_l(k ? vo[k - 1] : (hlv << 16), vo[k], 16);
+        const unsigned rO = __funnelshift_r(ve[k], k < 7 ? ve[k + 1] : hrv, 16);
+        const unsigned dE = max2(ve[k], max2(lE, vo[k]));
+        const unsigned dO = max2(vo[k], max2(ve[k], rO));
+        const unsigned nE = min2(ie[k], dE), nO = min2(io[k], dO);  // D >= J (centre included)
+        ch |= (nE ^ e[k]) | (nO ^ o[k]);
+        e[k] = nE;
+        o[k] = nO;
+      }
+    } else {
+      unsigned prevo = h.l << 16;
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const unsigned lE = __funnelshift_l(prevo, o[k], 16);
+        const unsigned rO = __funnelshift_r(e[k], k < 7 ? e[k + 1] : h.r, 16);
+        const unsigned dE = max2(max2(ve[k], e[k]), max2(lE, o[k]));
+        const unsigned dO = max2(max2(vo[k], o[k]), max2(e[k], rO));
+        prevo = o[k];  // the old odd word, for word k + 1
+        const unsigned nE = min2(ie[k], dE), nO = min2(io[k], dO);
+        ch |= (nE ^ e[k]) | (nO ^ o[k]);
+        e[k] = nE;
+        o[k] = nO;
+      }
+    }
+    if (!__any_sync(FULL, ch != 0)) break;
+    changed = true;
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k++) j[k] = e[k] | (o[k] << 8);
+  return steps;
+}
+
+template <int CONN>
+__global__ void __launch_bounds__(kCtaThreads, 4)
+    tile_engine_reg_kernel(EngineArgs a, unsigned long long *counters) {
+  const int lane = threadIdx.x & 31;
+  const bool l0 = lane == 0;
+  unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0;
+  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  int next_tile = -1;
+  for (;;) {
+    long long c_pop = l0 ? clock64() : 0;
+    int t = -1;
+    if (l0) {
+      t = next_tile >= 0 ? next_tile : ring_pop(a.q);
+      if (t >= 0) {
+        atomicExch(&a.q.state[t], ST_R);
+        fence_acq_rel();
+      }
+    }
+    t = __shfl_sync(FULL, t, 0);
+    next_tile = -1;
+    if (t < 0) break;
+    const int tx = t % a.ntx, ty = t / a.ntx;
+    const int x0 = tx * TS, y0 = ty * TS;
+    long long c_load = l0 ? clock64() : 0;
+    if (l0) ph[0] += c_load - c_pop;
+
+    unsigned j[8], m[8];
+    RegHalo h;
+    reg_load_row((const uint8_t *)a.J, a.W, x0, y0 + lane, a.H, a.vec, true, j);
+    reg_load_row((const uint8_t *)a.I, a.W, x0, y0 + lane, a.H, a.vec, false, m);
+    reg_load_halo(a, x0, y0, lane, h);
+    // the border as last published (lanes 0 / 31: whole rows; every lane: its ends)
+    unsigned ob[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) ob[k] = j[k];
+    if (l0) ph[1] += clock64() - c_load;
+    bool rerun = false;
+    for (;;) {  // re-run while neighbours request it
+      n_tiles += l0;
+      n_reruns += l0 && rerun;
+      long long c_fix = l0 ? clock64() : 0;
+      bool changed = false;
+      const int steps = reg_fixpoint<CONN>(j, m, h, lane, changed);
+      if (l0) n_steps += steps;
+      changed = __any_sync(FULL, changed);
+      long long c_st = l0 ? clock64() : 0;
+      if (l0) ph[2] += c_st - c_fix;
+      if (changed) {
+        // store my row
+        const int gy = y0 + lane;
+        if (gy < a.H) {
+          uint8_t *p = (uint8_t *)a.J + (size_t)gy * a.W + x0;
+          if (a.vec && x0 + TS <= a.W) {
+            reinterpret_cast<uint4 *>(p)[0] = make_uint4(j[0], j[1], j[2], j[3]);
+            reinterpret_cast<uint4 *>(p)[1] = make_uint4(j[4], j[5], j[6], j[7]);
+          } else {
+            for (int x = 0; x < TS && x0 + x < a.W; x++) p[x] = (uint8_t)(j[x >> 2] >> (8 * (x & 3)));
+          }
+        }
+        if (a.dirty && l0) a.dirty[ty] = 1;
+        // which neighbours can the changed border still raise (J < I, J < the
+        // max of the adjacent changed border cells)?
+        unsigned need_row = 0;  // lanes 0 / 31: the row above / below
+        unsigned cv[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) cv[k] = j[k] & __vcmpne4(j[k], ob[k]);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          unsigned D = cv[k];
+          if (CONN == 8) {
+            const unsigned L = __funnelshift_l(k ? cv[k - 1] : 0u, cv[k], 8);
+            const unsigned R = __funnelshift_r(cv[k], k < 7 ? cv[k + 1] : 0u, 8);
+            D = __vmaxu4(D, __vmaxu4(L, R));
+          }
+          need_row |= __vcmpltu4(h.row[k], h.rowI[k]) & __vcmpltu4(h.row[k], D);
+        }
+        const unsigned cl = cv[0] & 0xffu, cr = cv[7] >> 24;  // changed row ends (or 0)
+        unsigned dl = cl, dr = cr;
+        if (CONN == 8) {
+          unsigned lu = __shfl_up_sync(FULL, cl, 1), ld = __shfl_down_sync(FULL, cl, 1);
+          unsigned ru = __shfl_up_sync(FULL, cr, 1), rd = __shfl_down_sync(FULL, cr, 1);
+          if (lane == 0) lu = ru = 0;
+          if (lane == 31) ld = rd = 0;
+          dl = max(cl, max(lu, ld));
+          dr = max(cr, max(ru, rd));
+        }
+        unsigned dirs = 0;
+        if (__any_sync(FULL, l0 && need_row)) dirs |= 1u << 1;             // N
+        if (__any_sync(FULL, lane == 31 && need_row)) dirs |= 1u << 7;     // S
+        if (__any_sync(FULL, h.l < h.lI && h.l < dl)) dirs |= 1u << 3;    // W
+        if (__any_sync(FULL, h.r < h.rI && h.r < dr)) dirs |= 1u << 5;    // E
+        if (CONN == 8) {  // corners: one interior cell each
+          const bool cwl = h.cl < h.clI && h.cl < cl, cwr = h.cr < h.crI && h.cr < cr;
+          if (__any_sync(FULL, l0 && cwl)) dirs |= 1u << 0;
+          if (__any_sync(FULL, l0 && cwr)) dirs |= 1u << 2;
+          if (__any_sync(FULL, lane == 31 && cwl)) dirs |= 1u << 6;
+          if (__any_sync(FULL, lane == 31 && cwr)) dirs |= 1u << 8;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) ob[k] = j[k];
+        fence_acq_rel();  // publish the tile before any neighbour is (re)queued
+        __syncwarp();
+        bool own = false;
+        unsigned ntile = 0;
+        if (lane < 9 && ((dirs >> lane) & 1u)) {
+          int ntxi = tx + (lane % 3) - 1, ntyi = ty + (lane / 3) - 1;
+          if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty) {
+            ntile = (unsigned)(ntyi * a.ntx + ntxi);
+            own = activate_claim(a.q, ntile);
+          }
+        }
+        unsigned ownmask = __ballot_sync(FULL, own);
+        int keep = (ownmask && next_tile < 0) ? __ffs(ownmask) - 1 : -1;
+        if (own && lane != keep) ring_push(a.q, ntile);
+        if (keep >= 0) next_tile = __shfl_sync(FULL, (int)ntile, keep);
+      }
+      int done = 0;
+      if (l0) {
+        unsigned old = atomicCAS(&a.q.state[t], ST_R, 0u);
+        if (old == ST_R) {
+          // no fence: pending is only ever changed by RMWs, whose per-location
+          // order already puts our activations' increments before this
+          atomicSub(a.q.pending, 1u);
+          done = 1;
+        } else {
+          atomicExch(&a.q.state[t], ST_R);  // consume the request (acquire)
+          fence_acq_rel();
+        }
+      }
+      done = __shfl_sync(FULL, done, 0);
+      if (l0) ph[5] += clock64() - c_st;
+      if (done) break;
+      reg_load_halo(a, x0, y0, lane, h);  // the interior is ours and current
+      rerun = true;
+    }
+  }
+  if (l0) {
+    atomicAdd(&counters[CNT_TILES], n_tiles);
+    atomicAdd(&counters[CNT_RERUNS], n_reruns);
+    atomicAdd(&counters[CNT_STEPS], n_steps);
     for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
   }
 }
@@ -908,6 +1216,17 @@ TileQueue carve_tile_queue(Carver &c, unsigned ntiles) {
   return q;
 }
 
+// the register engine covers u8 (and binary); the shared-memory engine stays
+// for u16 / int32 / f32 and whenever its knobs are asked for (queue capacity
+// for the forced-overflow path, in-tile sweep counts)
+template <typename T>
+static bool use_reg_engine(const EngineOpts &o) {
+  if (sizeof(T) != 1) return false;
+  if (o.engine == ENGINE_SMEM) return false;
+  if (o.engine == ENGINE_REG) return true;
+  return o.qcap <= 0 && o.sweeps_set == 0;
+}
+
 template <typename T, int CONN>
 static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
                          unsigned long long *counters, const EngineOpts &o, cudaStream_t st) {
@@ -945,7 +1264,21 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   bool vec = ((size_t)W * sizeof(T)) % 16 == 0 && (uintptr_t)J % 16 == 0 && (uintptr_t)I % 16 == 0;
   EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, o.dirty, q};
   if (o.ev_begin) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_begin, st));
-  kern<<<blocks, kCtaThreads, smem, st>>>(a, counters);
+  if (use_reg_engine<T>(o)) {
+    static int reg_blocks = 0;
+    if (reg_blocks == 0) {
+      int per_sm = 0;
+      IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_engine_reg_kernel<CONN>,
+                                                                  kCtaThreads, 0));
+      reg_blocks = device_sm_count() * (per_sm < 1 ? 1 : per_sm);
+    }
+    int rb = reg_blocks;
+    if (o.max_blocks > 0 && rb > o.max_blocks) rb = o.max_blocks;
+    if ((unsigned)rb > max_b) rb = (int)max_b;
+    tile_engine_reg_kernel<CONN><<<rb, kCtaThreads, 0, st>>>(a, counters);
+  } else {
+    kern<<<blocks, kCtaThreads, smem, st>>>(a, counters);
+  }
   IWPP_CUDA_TRY(cudaGetLastError());
   if (o.ev_end) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_end, st));
   return IWPP_OK;

@@ -74,9 +74,11 @@ def _count_violations(m: Image2D, i: Image2D) -> int:
 # ---------------------------------------------------------------------------
 # the device engine
 
+ENGINE_AUTO, ENGINE_SMEM, ENGINE_REG = 0, 1, 2  # iwpp_recon_opts.engine
+
 def _opts(cfg: EngineConfig | None, sweeps: int = -1, tile_sweeps: int = -1,
           halo_sweep_threshold: int = -1, max_blocks: int = 0,
-          pipeline_rows: int = 0) -> _lib.ReconOpts:
+          pipeline_rows: int = 0, engine: int = 0) -> _lib.ReconOpts:
     o = _lib.ReconOpts()
     o.sweeps = sweeps
     o.max_blocks = max_blocks
@@ -84,6 +86,7 @@ def _opts(cfg: EngineConfig | None, sweeps: int = -1, tile_sweeps: int = -1,
     o.tile_sweeps = tile_sweeps
     o.halo_sweep_threshold = halo_sweep_threshold
     o.pipeline_rows = pipeline_rows
+    o.engine = engine
     if cfg is not None and cfg.queue.gbq_capacity is not None:
         o.queue_capacity = int(cfg.queue.gbq_capacity)
     else:
@@ -93,14 +96,16 @@ def _opts(cfg: EngineConfig | None, sweeps: int = -1, tile_sweeps: int = -1,
 
 def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
                 sweeps: int = -1, stats: dict | None = None, tile_sweeps: int = -1,
-                halo_sweep_threshold: int = -1, max_blocks: int = 0, pipeline_rows: int = 0):
+                halo_sweep_threshold: int = -1, max_blocks: int = 0, pipeline_rows: int = 0,
+                engine: int = 0):
     """Reconstruction of raw arrays (numpy -> numpy, CUDA tensor -> tensor).
 
     The marker is not modified.  ``stats`` (a dict) receives the device
     counters when given (this synchronizes the stream).  The remaining
     keywords are engine tuning knobs (results never depend on them);
     ``pipeline_rows`` sets the slab height of the host path's transfer /
-    compute pipeline (0 = auto, < 0 = off).
+    compute pipeline (0 = auto, < 0 = off); ``engine`` picks the tile engine
+    (0 = auto, 1 = shared-memory queue engine, 2 = register engine, u8 only).
     """
     L = _lib.lib()
     from .grid import np_dtype_of, is_device_array
@@ -112,7 +117,8 @@ def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
     H, W = marker.shape
     st = _lib.Stats()
     sp = _lib.ctypes.byref(st) if stats is not None else None
-    opts = _opts(cfg, sweeps, tile_sweeps, halo_sweep_threshold, max_blocks, pipeline_rows)
+    opts = _opts(cfg, sweeps, tile_sweeps, halo_sweep_threshold, max_blocks, pipeline_rows,
+                 engine)
     if is_device_array(marker):
         torch = _lib._torch()
         J = marker.clone()

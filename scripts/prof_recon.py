@@ -23,7 +23,7 @@ L = _lib.lib()
 H, W = J.shape
 ws = _lib.workspace(L.iwpp_recon_workspace_bytes(W, H, 0, conn))
 out = dJ.clone()
-o = _lib.ReconOpts(); o.sweeps = int(os.environ.get("GSW", "0")); o.max_blocks = mb; o.check_contract = 0; o.queue_capacity = 0; o.tile_sweeps = tsw; o.halo_sweep_threshold = hth
+o = _lib.ReconOpts(); o.engine = int(os.environ.get("ENGINE", "0")); o.sweeps = int(os.environ.get("GSW", "0")); o.max_blocks = mb; o.check_contract = 0; o.queue_capacity = 0; o.tile_sweeps = tsw; o.halo_sweep_threshold = hth
 st = _lib.Stats()
 ts = []
 for r in range(reps + 2):
@@ -39,5 +39,5 @@ cnt = (_lib.ctypes.c_uint64 * 16)()
 L.iwpp_recon_engine_counters(_lib.ptr(ws), W, H, cnt, 16, _lib.stream_ptr())
 phs = list(cnt)[8:14]; tot = sum(phs) or 1
 ph_str = " ".join(f"{n}={v/tot*100:.0f}%" for n, v in zip(["pop","load","sweep","detect","bfs","store"], phs))
-print(f"  phases: {ph_str}; per-activation cycles {tot/max(cnt[0],1):.0f}")
+print(f"  phases: {ph_str}; per-activation cycles {tot/max(cnt[0],1):.0f}; jacobi steps/activation {cnt[6]/max(cnt[0],1):.2f}")
 print(f"{case} {n}^2 c{conn} tsw={tsw} mb={mb} hth={hth} gsw={o.sweeps}: median {np.median(ts):.3f} ms min {min(ts):.3f}  stats={st.as_dict()}", flush=True)

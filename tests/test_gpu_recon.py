@@ -318,3 +318,29 @@ def test_f32_operator_api_and_nan_contract(gw):
     for device in (False, True):
         with pytest.raises(gw.ContractViolation):
             _pair(gw, Jn, I, 8, "f32", device)
+
+
+# ---------------------------------------------------------------------------
+# both u8 tile engines (register Jacobi engine = auto; shared-memory queue
+# engine = forced) on the same inputs
+
+@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("conn", [4, 8])
+def test_u8_engines_vs_oracle(gw, engine, conn):
+    t = _torch()
+    rng = np.random.default_rng(700 + conn)
+    cases = [oracle.gray_pair(s, int(rng.integers(1 << 30)), h=40)
+             for s in [(1, 1), (31, 33), (64, 64), (97, 130), (513, 257), (1000, 999)]]
+    bw = oracle.gen_synthetic_mask(700, 530, 50, 7)
+    cases.append(oracle.imfill_pair(bw))
+    I = np.full((300, 260), 200, np.uint8)
+    I[::3, 1:] = 0  # long corridor
+    M = np.zeros_like(I)
+    M[-1, 0] = 200
+    cases.append((M, I))
+    for J, I in cases:
+        want = oracle.recon_fh(J, I, conn)
+        got = gw.reconstruct(t.from_numpy(J).cuda(), t.from_numpy(I).cuda(), conn, engine=engine)
+        assert np.array_equal(got.cpu().numpy(), want), (J.shape, engine, conn)
+        got = gw.reconstruct(J, I, conn, engine=engine, pipeline_rows=64)
+        assert np.array_equal(got, want), (J.shape, engine, conn, "host")
