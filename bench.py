@@ -341,7 +341,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": ncu_traffic("recon_tile_engine_u8_c8"),
-                     "kernel": "tile_engine_kernel<uint8,8>",
+                     "kernel": "tile_engine_reg_kernel<8> (u8 register engine)",
                      "kernel_ms": round(kavg, 4), "alg_bytes_per_px": ALG_BYTES_PER_PX,
                      "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
         "library": os.path.relpath(LIB, ROOT),

@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
 // activation of the neighbours a changed border can still raise, finish,
 // re-run) is the same as the shared-memory engine's.
 struct RegHalo {
-  unsigned row[8], rowI[8];  // lane 0: the row above the tile; lane 31: the row below
+  unsigned row[8];           // lane 0: the row above the tile; lane 31: the row below
   unsigned l, r, lI, rI;     // the cells left / right of my row (J, I)
   unsigned cl, cr, clI, crI; // lane 0: corners above; lane 31: corners below
 };
@@ -846,8 +846,15 @@ __device__ __forceinline__ void reg_load_halo(const EngineArgs &a, int x0, int y
   h.clI = reg_cell(I, a.W, a.H, x0 - 1, hy, false);
   h.crI = reg_cell(I, a.W, a.H, x0 + TS, hy, false);
   reg_load_row(J, a.W, x0, hy, a.H, a.vec, true, h.row);
-  reg_load_row(I, a.W, x0, hy, a.H, a.vec, false, h.rowI);
 }
+
+// Per-warp shared memory of the register engine (keeps registers for the
+// Jacobi state): lanes 0 / 31 park the halo row's I and their row as last
+// published (the activation test's inputs).
+struct RegWarpSmem {
+  unsigned rowI[2][8];
+  unsigned ob[2][8];
+};
 
 // 16-bit lane SIMD (VIMNMX.U16x2: one instruction for two pixels)
 __device__ __forceinline__ unsigned max2(unsigned a, unsigned b) {
@@ -941,10 +948,14 @@ __device__ __forceinline__ int reg_fixpoint(unsigned *j, const unsigned *m, cons
 }
 
 template <int CONN>
-__global__ void __launch_bounds__(kCtaThreads, 4)
+__global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     tile_engine_reg_kernel(EngineArgs a, unsigned long long *counters) {
+  __shared__ RegWarpSmem wsm[kWarpsPerCta];
   const int lane = threadIdx.x & 31;
   const bool l0 = lane == 0;
+  const bool edge = lane == 0 || lane == 31;
+  const int sel = lane == 31;
+  RegWarpSmem &ws = wsm[threadIdx.x >> 5];
   unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0;
   unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
   int next_tile = -1;
@@ -972,9 +983,18 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
     reg_load_row((const uint8_t *)a.I, a.W, x0, y0 + lane, a.H, a.vec, false, m);
     reg_load_halo(a, x0, y0, lane, h);
     // the border as last published (lanes 0 / 31: whole rows; every lane: its ends)
-    unsigned ob[8];
+    if (edge) {
+      const int hy = lane == 0 ? y0 - 1 : y0 + TS;
+      unsigned hI[8];
+      reg_load_row((const uint8_t *)a.I, a.W, x0, hy, a.H, a.vec, false, hI);
 #pragma unroll
-    for (int k = 0; k < 8; k++) ob[k] = j[k];
+      for (int k = 0; k < 8; k++) {
+        ws.rowI[sel][k] = hI[k];
+        ws.ob[sel][k] = j[k];
+      }
+    }
+    unsigned obl = j[0] & 0xffu, obr = j[7] >> 24;
+    __syncwarp();
     if (l0) ph[1] += clock64() - c_load;
     bool rerun = false;
     for (;;) {  // re-run while neighbours request it
@@ -1003,20 +1023,24 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
         // which neighbours can the changed border still raise (J < I, J < the
         // max of the adjacent changed border cells)?
         unsigned need_row = 0;  // lanes 0 / 31: the row above / below
-        unsigned cv[8];
+        if (edge) {
+          unsigned cv[8];
 #pragma unroll
-        for (int k = 0; k < 8; k++) cv[k] = j[k] & __vcmpne4(j[k], ob[k]);
+          for (int k = 0; k < 8; k++) cv[k] = j[k] & __vcmpne4(j[k], ws.ob[sel][k]);
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-          unsigned D = cv[k];
-          if (CONN == 8) {
-            const unsigned L = __funnelshift_l(k ? cv[k - 1] : 0u, cv[k], 8);
-            const unsigned R = __funnelshift_r(cv[k], k < 7 ? cv[k + 1] : 0u, 8);
-            D = __vmaxu4(D, __vmaxu4(L, R));
+          for (int k = 0; k < 8; k++) {
+            unsigned D = cv[k];
+            if (CONN == 8) {
+              const unsigned L = __funnelshift_l(k ? cv[k - 1] : 0u, cv[k], 8);
+              const unsigned R = __funnelshift_r(cv[k], k < 7 ? cv[k + 1] : 0u, 8);
+              D = __vmaxu4(D, __vmaxu4(L, R));
+            }
+            need_row |= __vcmpltu4(h.row[k], ws.rowI[sel][k]) & __vcmpltu4(h.row[k], D);
           }
-          need_row |= __vcmpltu4(h.row[k], h.rowI[k]) & __vcmpltu4(h.row[k], D);
         }
-        const unsigned cl = cv[0] & 0xffu, cr = cv[7] >> 24;  // changed row ends (or 0)
+        // changed row ends (or 0)
+        const unsigned jl = j[0] & 0xffu, jr = j[7] >> 24;
+        const unsigned cl = jl != obl ? jl : 0u, cr = jr != obr ? jr : 0u;
         unsigned dl = cl, dr = cr;
         if (CONN == 8) {
           unsigned lu = __shfl_up_sync(FULL, cl, 1), ld = __shfl_down_sync(FULL, cl, 1);
@@ -1038,8 +1062,11 @@ __global__ void __launch_bounds__(kCtaThreads, 4)
           if (__any_sync(FULL, lane == 31 && cwl)) dirs |= 1u << 6;
           if (__any_sync(FULL, lane == 31 && cwr)) dirs |= 1u << 8;
         }
+        if (edge)
 #pragma unroll
-        for (int k = 0; k < 8; k++) ob[k] = j[k];
+          for (int k = 0; k < 8; k++) ws.ob[sel][k] = j[k];
+        obl = jl;
+        obr = jr;
         fence_acq_rel();  // publish the tile before any neighbour is (re)queued
         __syncwarp();
         bool own = false;

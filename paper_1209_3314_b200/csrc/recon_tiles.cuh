@@ -16,6 +16,7 @@ constexpr int BITW = (PNS + 31) / 32;    // in-queue bitmap words
 constexpr int kWarpsPerCta = 4;
 constexpr int kCtaThreads = 32 * kWarpsPerCta;
 constexpr int kCtaMinBlocks = 5;  // resident CTAs per SM (shared memory allows 5 for u8)
+constexpr int kRegCtaMinBlocks = 4;  // register engine: registers are the limit
 static_assert(RQ >= PN && (RQ & (RQ - 1)) == 0, "ring must hold a full rescan");
 static_assert(PNS < 65536, "queue entries are 16-bit");
 
