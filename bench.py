@@ -428,7 +428,7 @@ def extras(L, _lib, dev, flush):
     dM, dK = torch.from_numpy(mk).to(dev), torch.from_numpy(msk).to(dev)
     n16 = bw.size
     for conn in (4, 8):
-        ms = timed(lambda: gw.reconstruct(dM, dK, conn), reps=3, warm=1)
+        ms = timed(lambda: gw.reconstruct(dM, dK, conn, kind="binary"), reps=3, warm=1)
         out[f"imfill_16k_c{conn}"] = {"ms": round(ms, 3), "mpx_s": round(n16 / ms / 1e3, 1)}
     return out
 

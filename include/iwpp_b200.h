@@ -42,6 +42,8 @@ enum iwpp_dtype {
   IWPP_I32 = 2, /* "i32" (not an Image2D kind in the reference; its kernels accept it) */
   IWPP_F32 = 3, /* "f32": runs the int32 engine on an order-preserving bit map of the
                    floats (-0.0 is taken as +0.0; NaN fails the marker <= mask contract) */
+  IWPP_BIN = 4, /* "binary": u8 storage holding only 0 / 255 (grid.py binary); runs a
+                   one-bit-per-pixel engine.  Other byte values are read as 255 */
 };
 
 enum iwpp_status {

@@ -48,6 +48,7 @@ int device_sm_count() {
 static size_t elem_size(int dtype) {
   switch (dtype) {
     case IWPP_U8: return 1;
+    case IWPP_BIN: return 1;
     case IWPP_U16: return 2;
     case IWPP_I32: return 4;
     case IWPP_F32: return 4;

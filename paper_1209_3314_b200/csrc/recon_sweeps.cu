@@ -318,7 +318,8 @@ static int rows_impl(void *J, const void *I, int W, int H, cudaStream_t st) {
 
 int sweep_rows(void *J, const void *I, int W, int H, int dtype, cudaStream_t st) {
   switch (dtype) {
-    case IWPP_U8: return rows_impl<uint8_t>(J, I, W, H, st);
+    case IWPP_U8:
+    case IWPP_BIN: return rows_impl<uint8_t>(J, I, W, H, st);
     case IWPP_U16: return rows_impl<uint16_t>(J, I, W, H, st);
     case IWPP_I32: return rows_impl<int32_t>(J, I, W, H, st);
   }
@@ -327,7 +328,8 @@ int sweep_rows(void *J, const void *I, int W, int H, int dtype, cudaStream_t st)
 
 int sweep_cols(void *J, const void *I, int W, int H, int dtype, void *scratch, cudaStream_t st) {
   switch (dtype) {
-    case IWPP_U8: return cols_impl<uint8_t>(J, I, W, H, scratch, st);
+    case IWPP_U8:
+    case IWPP_BIN: return cols_impl<uint8_t>(J, I, W, H, scratch, st);
     case IWPP_U16: return cols_impl<uint16_t>(J, I, W, H, scratch, st);
     case IWPP_I32: return cols_impl<int32_t>(J, I, W, H, scratch, st);
   }
@@ -344,7 +346,8 @@ int seed_scan(const void *J, const void *I, int W, int H, int dtype, int conn, i
   else                                                                                            \
     seed_scan_kernel<T, 4><<<g, 256, 0, st>>>((const T *)J, (const T *)I, W, H, out, n_out);
   switch (dtype) {
-    case IWPP_U8: SS(uint8_t); break;
+    case IWPP_U8:
+    case IWPP_BIN: SS(uint8_t); break;
     case IWPP_U16: SS(uint16_t); break;
     case IWPP_I32: SS(int32_t); break;
     default: return set_error(IWPP_E_CONTRACT, "unsupported dtype %d", dtype);
@@ -359,6 +362,7 @@ int check_le(const void *J, const void *I, size_t n, int dtype, unsigned long lo
   int g = grid_cap(n, 256);
   switch (dtype) {
     case IWPP_U8:
+    case IWPP_BIN:
       if (n % 16 == 0 && (uintptr_t)J % 16 == 0 && (uintptr_t)I % 16 == 0)
         check_le_u8x16_kernel<<<grid_cap(n / 16, 256), 256, 0, st>>>((const uint4 *)J, (const uint4 *)I,
                                                                      n / 16, viol);

@@ -1111,6 +1111,219 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
   }
 }
 
+// --- binary engine (u8 storage, values 0 / 255) -------------------------------
+//
+// The "binary" element kind (grid.py binary, imfill): one bit per pixel, so
+// a 32 x 32 tile is one 32-bit word per lane (lane = row).  A Jacobi step is
+//     J <- I & (J | J_up | J_down | the same shifted by one column),
+// about a dozen instructions for the whole tile.  Same queue protocol.
+
+// 32 bytes of 0 / 255 (8 words) -> 32 bits (bit x = byte x != 0)
+__device__ __forceinline__ unsigned bin_pack(const unsigned *w) {
+  unsigned b = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const unsigned t = (w[k] | (w[k] << 1) | (w[k] << 2) | (w[k] << 3) | (w[k] << 4) |
+                        (w[k] << 5) | (w[k] << 6) | (w[k] << 7)) & 0x80808080u;  // any bit set
+    b |= ((t * 0x00204081u) >> 28) << (4 * k);
+  }
+  return b;
+}
+// 32 bits -> 32 bytes of 0 / 255
+__device__ __forceinline__ void bin_unpack(unsigned b, unsigned *w) {
+#pragma unroll
+  for (int k = 0; k < 8; k++) w[k] = ((((b >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu;
+}
+
+struct BinHalo {
+  unsigned row, rowI;      // lane 0: the row above (bits); lane 31: the row below
+  unsigned l, r, lI, rI;   // bits (0 / 1) of the cells left / right of my row
+  unsigned cl, cr, clI, crI;
+};
+
+__device__ __forceinline__ unsigned bin_row(const uint8_t *base, int W, int x0, int gy, int H,
+                                            bool vec, bool cg) {
+  unsigned w[8];
+  reg_load_row(base, W, x0, gy, H, vec, cg, w);
+  return bin_pack(w);
+}
+
+__device__ __forceinline__ void bin_load_halo(const EngineArgs &a, int x0, int y0, int lane,
+                                              BinHalo &h) {
+  const uint8_t *J = (const uint8_t *)a.J, *I = (const uint8_t *)a.I;
+  const int gy = y0 + lane;
+  const int hy = lane == 0 ? y0 - 1 : (lane == 31 ? y0 + TS : -1);
+  h.l = reg_cell(J, a.W, a.H, x0 - 1, gy, true) != 0;
+  h.r = reg_cell(J, a.W, a.H, x0 + TS, gy, true) != 0;
+  h.lI = reg_cell(I, a.W, a.H, x0 - 1, gy, false) != 0;
+  h.rI = reg_cell(I, a.W, a.H, x0 + TS, gy, false) != 0;
+  h.cl = reg_cell(J, a.W, a.H, x0 - 1, hy, true) != 0;
+  h.cr = reg_cell(J, a.W, a.H, x0 + TS, hy, true) != 0;
+  h.clI = reg_cell(I, a.W, a.H, x0 - 1, hy, false) != 0;
+  h.crI = reg_cell(I, a.W, a.H, x0 + TS, hy, false) != 0;
+  h.row = bin_row(J, a.W, x0, hy, a.H, a.vec, true);
+  h.rowI = bin_row(I, a.W, x0, hy, a.H, a.vec, false);
+}
+
+template <int CONN>
+__device__ __forceinline__ int bin_fixpoint(unsigned &j, unsigned m, const BinHalo &h, int lane,
+                                            bool &changed) {
+  unsigned hlv = h.l, hrv = h.r;
+  if (CONN == 8) {
+    unsigned lu = __shfl_up_sync(FULL, h.l, 1), ld = __shfl_down_sync(FULL, h.l, 1);
+    unsigned ru = __shfl_up_sync(FULL, h.r, 1), rd = __shfl_down_sync(FULL, h.r, 1);
+    if (lane == 0) { lu = h.cl; ru = h.cr; }
+    if (lane == 31) { ld = h.cl; rd = h.cr; }
+    hlv = h.l | lu | ld;
+    hrv = h.r | ru | rd;
+  }
+  int steps = 0;
+  for (;;) {
+    steps++;
+    unsigned u = __shfl_up_sync(FULL, j, 1), d = __shfl_down_sync(FULL, j, 1);
+    if (lane == 0) u = h.row;
+    if (lane == 31) d = h.row;
+    unsigned D;
+    if (CONN == 8) {
+      const unsigned v = j | u | d;
+      D = v | (v << 1) | hlv | (v >> 1) | (hrv << 31);
+    } else {
+      D = j | u | d | (j << 1) | h.l | (j >> 1) | (h.r << 31);
+    }
+    const unsigned nj = m & D;
+    const bool ch = nj != j;
+    j = nj;
+    if (!__any_sync(FULL, ch)) break;
+    changed = true;
+  }
+  return steps;
+}
+
+template <int CONN>
+__global__ void __launch_bounds__(kCtaThreads)
+    tile_engine_bin_kernel(EngineArgs a, unsigned long long *counters) {
+  const int lane = threadIdx.x & 31;
+  const bool l0 = lane == 0;
+  unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0;
+  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  int next_tile = -1;
+  for (;;) {
+    long long c_pop = l0 ? clock64() : 0;
+    int t = -1;
+    if (l0) {
+      t = next_tile >= 0 ? next_tile : ring_pop(a.q);
+      if (t >= 0) {
+        atomicExch(&a.q.state[t], ST_R);
+        fence_acq_rel();
+      }
+    }
+    t = __shfl_sync(FULL, t, 0);
+    next_tile = -1;
+    if (t < 0) break;
+    const int tx = t % a.ntx, ty = t / a.ntx;
+    const int x0 = tx * TS, y0 = ty * TS;
+    long long c_load = l0 ? clock64() : 0;
+    if (l0) ph[0] += c_load - c_pop;
+    unsigned j = bin_row((const uint8_t *)a.J, a.W, x0, y0 + lane, a.H, a.vec, true);
+    const unsigned m = bin_row((const uint8_t *)a.I, a.W, x0, y0 + lane, a.H, a.vec, false);
+    BinHalo h;
+    bin_load_halo(a, x0, y0, lane, h);
+    unsigned ob = j;  // my row as last published
+    if (l0) ph[1] += clock64() - c_load;
+    bool rerun = false;
+    for (;;) {
+      n_tiles += l0;
+      n_reruns += l0 && rerun;
+      long long c_fix = l0 ? clock64() : 0;
+      bool changed = false;
+      const int steps = bin_fixpoint<CONN>(j, m, h, lane, changed);
+      if (l0) n_steps += steps;
+      changed = __any_sync(FULL, changed);
+      long long c_st = l0 ? clock64() : 0;
+      if (l0) ph[2] += c_st - c_fix;
+      if (changed) {
+        const int gy = y0 + lane;
+        if (gy < a.H && j != ob) {
+          unsigned w[8];
+          bin_unpack(j, w);
+          uint8_t *p = (uint8_t *)a.J + (size_t)gy * a.W + x0;
+          if (a.vec && x0 + TS <= a.W) {
+            reinterpret_cast<uint4 *>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            reinterpret_cast<uint4 *>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+          } else {
+            for (int x = 0; x < TS && x0 + x < a.W; x++) p[x] = (uint8_t)(w[x >> 2] >> (8 * (x & 3)));
+          }
+        }
+        if (a.dirty && l0) a.dirty[ty] = 1;
+        // neighbours a newly set border cell can still raise (halo J = 0, I = 1)
+        const unsigned cv = j & ~ob;
+        const unsigned Dr = CONN == 8 ? (cv | (cv << 1) | (cv >> 1)) : cv;
+        const unsigned need_row = Dr & h.rowI & ~h.row;
+        const unsigned cl = cv & 1u, cr = cv >> 31;
+        unsigned dl = cl, dr = cr;
+        if (CONN == 8) {
+          unsigned lu = __shfl_up_sync(FULL, cl, 1), ld = __shfl_down_sync(FULL, cl, 1);
+          unsigned ru = __shfl_up_sync(FULL, cr, 1), rd = __shfl_down_sync(FULL, cr, 1);
+          if (lane == 0) lu = ru = 0;
+          if (lane == 31) ld = rd = 0;
+          dl |= lu | ld;
+          dr |= ru | rd;
+        }
+        unsigned dirs = 0;
+        if (__any_sync(FULL, l0 && need_row)) dirs |= 1u << 1;          // N
+        if (__any_sync(FULL, lane == 31 && need_row)) dirs |= 1u << 7;  // S
+        if (__any_sync(FULL, dl & h.lI & ~h.l)) dirs |= 1u << 3;          // W
+        if (__any_sync(FULL, dr & h.rI & ~h.r)) dirs |= 1u << 5;          // E
+        if (CONN == 8) {
+          const bool cwl = cl & h.clI & ~h.cl, cwr = cr & h.crI & ~h.cr;
+          if (__any_sync(FULL, l0 && cwl)) dirs |= 1u << 0;
+          if (__any_sync(FULL, l0 && cwr)) dirs |= 1u << 2;
+          if (__any_sync(FULL, lane == 31 && cwl)) dirs |= 1u << 6;
+          if (__any_sync(FULL, lane == 31 && cwr)) dirs |= 1u << 8;
+        }
+        ob = j;
+        fence_acq_rel();  // publish the tile before any neighbour is (re)queued
+        __syncwarp();
+        bool own = false;
+        unsigned ntile = 0;
+        if (lane < 9 && ((dirs >> lane) & 1u)) {
+          int ntxi = tx + (lane % 3) - 1, ntyi = ty + (lane / 3) - 1;
+          if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty) {
+            ntile = (unsigned)(ntyi * a.ntx + ntxi);
+            own = activate_claim(a.q, ntile);
+          }
+        }
+        unsigned ownmask = __ballot_sync(FULL, own);
+        int keep = (ownmask && next_tile < 0) ? __ffs(ownmask) - 1 : -1;
+        if (own && lane != keep) ring_push(a.q, ntile);
+        if (keep >= 0) next_tile = __shfl_sync(FULL, (int)ntile, keep);
+      }
+      int done = 0;
+      if (l0) {
+        unsigned old = atomicCAS(&a.q.state[t], ST_R, 0u);
+        if (old == ST_R) {
+          atomicSub(a.q.pending, 1u);  // (see the register engine: no fence needed)
+          done = 1;
+        } else {
+          atomicExch(&a.q.state[t], ST_R);  // consume the request (acquire)
+          fence_acq_rel();
+        }
+      }
+      done = __shfl_sync(FULL, done, 0);
+      if (l0) ph[5] += clock64() - c_st;
+      if (done) break;
+      bin_load_halo(a, x0, y0, lane, h);
+      rerun = true;
+    }
+  }
+  if (l0) {
+    atomicAdd(&counters[CNT_TILES], n_tiles);
+    atomicAdd(&counters[CNT_RERUNS], n_reruns);
+    atomicAdd(&counters[CNT_STEPS], n_steps);
+    for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
+  }
+}
+
 // Initial GBQ: every tile, ordered by 2x2 colour class (then raster) so the
 // first wave of concurrently running tiles are never neighbours.
 __global__ void tile_queue_init_kernel(TileQueue q, int ntx, int nty, unsigned long long *counters,
@@ -1256,7 +1469,8 @@ static bool use_reg_engine(const EngineOpts &o) {
 
 template <typename T, int CONN>
 static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
-                         unsigned long long *counters, const EngineOpts &o, cudaStream_t st) {
+                         unsigned long long *counters, const EngineOpts &o, cudaStream_t st,
+                         bool binary = false) {
   int ntx = (W + TS - 1) / TS, nty = (H + TS - 1) / TS;
   unsigned ntiles = (unsigned)ntx * nty;
   size_t smem = sizeof(WarpSmem<T>) * kWarpsPerCta;
@@ -1291,7 +1505,20 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   bool vec = ((size_t)W * sizeof(T)) % 16 == 0 && (uintptr_t)J % 16 == 0 && (uintptr_t)I % 16 == 0;
   EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, o.dirty, q};
   if (o.ev_begin) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_begin, st));
-  if (use_reg_engine<T>(o)) {
+  if (binary && o.engine != ENGINE_SMEM && o.engine != ENGINE_REG && o.qcap <= 0 &&
+      o.sweeps_set == 0) {
+    static int bin_blocks = 0;
+    if (bin_blocks == 0) {
+      int per_sm = 0;
+      IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_engine_bin_kernel<CONN>,
+                                                                  kCtaThreads, 0));
+      bin_blocks = device_sm_count() * (per_sm < 1 ? 1 : per_sm);
+    }
+    int bb = bin_blocks;
+    if (o.max_blocks > 0 && bb > o.max_blocks) bb = o.max_blocks;
+    if ((unsigned)bb > max_b) bb = (int)max_b;
+    tile_engine_bin_kernel<CONN><<<bb, kCtaThreads, 0, st>>>(a, counters);
+  } else if (use_reg_engine<T>(o)) {
     static int reg_blocks = 0;
     if (reg_blocks == 0) {
       int per_sm = 0;
@@ -1317,6 +1544,9 @@ int run_tile_engine(void *J, const void *I, int W, int H, int dtype, int conn, T
   return conn == 8 ? launch_engine<T, 8>(J, I, W, H, q, counters, o, st) \
                    : launch_engine<T, 4>(J, I, W, H, q, counters, o, st)
   switch (dtype) {
+    case IWPP_BIN:
+      return conn == 8 ? launch_engine<uint8_t, 8>(J, I, W, H, q, counters, o, st, true)
+                       : launch_engine<uint8_t, 4>(J, I, W, H, q, counters, o, st, true);
     case IWPP_U8:
       DISPATCH(uint8_t);
     case IWPP_U16:

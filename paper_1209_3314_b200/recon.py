@@ -97,7 +97,7 @@ def _opts(cfg: EngineConfig | None, sweeps: int = -1, tile_sweeps: int = -1,
 def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
                 sweeps: int = -1, stats: dict | None = None, tile_sweeps: int = -1,
                 halo_sweep_threshold: int = -1, max_blocks: int = 0, pipeline_rows: int = 0,
-                engine: int = 0):
+                engine: int = 0, kind: str | None = None):
     """Reconstruction of raw arrays (numpy -> numpy, CUDA tensor -> tensor).
 
     The marker is not modified.  ``stats`` (a dict) receives the device
@@ -106,12 +106,16 @@ def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
     ``pipeline_rows`` sets the slab height of the host path's transfer /
     compute pipeline (0 = auto, < 0 = off); ``engine`` picks the tile engine
     (0 = auto, 1 = shared-memory queue engine, 2 = register engine, u8 only).
+    ``kind="binary"`` (u8 arrays holding only 0 / 255, grid.py binary) runs
+    the one-bit-per-pixel engine.
     """
     L = _lib.lib()
     from .grid import np_dtype_of, is_device_array
     dt = np_dtype_of(marker)
     code = {np.dtype(np.uint8): 0, np.dtype(np.uint16): 1, np.dtype(np.int32): 2,
             np.dtype(np.float32): 3}.get(dt)
+    if kind == "binary" and code == 0:
+        code = 4
     if code is None:
         raise ContractViolation(f"no device engine for dtype {dt}")
     H, W = marker.shape
@@ -148,7 +152,8 @@ def _run(inp: ReconInput, cfg: EngineConfig | None = None, sweeps: int = -1) -> 
         raise ContractViolation(f"no B200 engine for elem_kind {inp.marker.elem_kind!r}")
     want_stats = cfg is not None
     d = {} if want_stats else None
-    J = reconstruct(inp.marker.data, inp.mask.data, inp.se.connectivity, cfg, sweeps, d)
+    J = reconstruct(inp.marker.data, inp.mask.data, inp.se.connectivity, cfg, sweeps, d,
+                    kind=inp.marker.elem_kind)
     if want_stats:
         cfg.stats.add(d)
     return Image2D(inp.marker.width, inp.marker.height, inp.marker.elem_kind, J)

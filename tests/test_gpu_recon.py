@@ -344,3 +344,28 @@ def test_u8_engines_vs_oracle(gw, engine, conn):
         assert np.array_equal(got.cpu().numpy(), want), (J.shape, engine, conn)
         got = gw.reconstruct(J, I, conn, engine=engine, pipeline_rows=64)
         assert np.array_equal(got, want), (J.shape, engine, conn, "host")
+
+
+# ---------------------------------------------------------------------------
+# the binary kind (0 / 255): one-bit-per-pixel engine vs the grey engines
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_binary_engine_vs_oracle(gw, conn):
+    t = _torch()
+    rng = np.random.default_rng(900 + conn)
+    cases = []
+    for shape, cov in [((1, 1), 0.5), ((33, 65), 0.6), ((257, 300), 0.55), ((1000, 999), 0.5)]:
+        mask = (rng.random(shape) < cov).astype(np.uint8) * 255
+        marker = np.where((rng.random(shape) < 0.02) & (mask == 255), 255, 0).astype(np.uint8)
+        cases.append((marker, mask))
+    for n, cov in [(700, 50), (1024, 30)]:
+        cases.append(oracle.imfill_pair(oracle.gen_synthetic_mask(n, n + 37, cov, 7)))
+    for marker, mask in cases:
+        want = oracle.recon_fh(marker, mask, conn)
+        got = gw.reconstruct(t.from_numpy(marker).cuda(), t.from_numpy(mask).cuda(), conn,
+                             kind="binary")
+        assert np.array_equal(got.cpu().numpy(), want), marker.shape
+        got = gw.reconstruct(marker, mask, conn, kind="binary", pipeline_rows=64)
+        assert np.array_equal(got, want), (marker.shape, "host")
+        out = gw.recon_fh(_pair(gw, marker, mask, conn, "binary", True))
+        assert np.array_equal(_np(out.data), want)
