@@ -320,7 +320,16 @@ __global__ void edt_seed_key_kernel(const int64_t *__restrict__ seeds, int64_t n
   if (blockIdx.x == 0 && threadIdx.x == 0) s.cnt[0] = (unsigned)n_seeds;
 }
 
-template <int CONN, bool CHECK>
+// QMODE selects how the next frontier is appended (the paper's queue study,
+// PAPER.md:1563-1595, Table 1): QM_BQ = warp-aggregated reservations into a
+// per-block shared-memory queue, spilled with one global atomic per block
+// (the default; the paper's TQ + block queue); QM_PF = warp-aggregated
+// reservations straight into the global queue (one atomic per warp, the
+// paper's prefix-sum variant); QM_NAIVE = one global atomicAdd per pushed
+// item (the paper's naive queue).
+enum { QM_BQ = 0, QM_PF = 1, QM_NAIVE = 2 };
+
+template <int CONN, bool CHECK, int QMODE = QM_BQ>
 __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, int H, EdtState s,
                                                                        long long max_rounds) {
   const unsigned FULL = 0xffffffffu;
@@ -400,13 +409,24 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
         }
       }
       unsigned c = __popc(mask);
-      unsigned pos = warp_reserve(&bq_n, c, FULL);
+      if (QMODE == QM_NAIVE) {
+        while (mask) {
+          int k = __ffs(mask) - 1;
+          mask &= mask - 1;
+          int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+          nxt[atomicAdd(ncnt, 1u)] = ((uint32_t)qy << 16) | (uint32_t)qx;
+        }
+        continue;
+      }
+      unsigned pos = QMODE == QM_PF ? warp_reserve(ncnt, c, FULL) : warp_reserve(&bq_n, c, FULL);
       while (mask) {
         int k = __ffs(mask) - 1;
         mask &= mask - 1;
         int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
         uint32_t item = ((uint32_t)qy << 16) | (uint32_t)qx;
-        if (pos < kEdtBq)
+        if (QMODE == QM_PF)
+          nxt[pos] = item;
+        else if (pos < kEdtBq)
           bq[pos] = item;
         else
           nxt[atomicAdd(ncnt, 1u)] = item;  // BQ full: spill directly
@@ -484,7 +504,10 @@ static EdtState carve_any(Carver &c, int64_t W, int64_t H, bool cas) {
   s.wc = ctl + 12;   // [12..14]
   s.counters = c.take<unsigned long long>(EC_N);
   // block engine: two planes over the same 2n keys, frontier bitmaps, regions
-  s.block = s.keymode && g_engine_override != ENGINE_QUEUE &&
+  const bool force_queue = g_engine_override == ENGINE_QUEUE ||
+                           g_engine_override == ENGINE_QUEUE_PF ||
+                           g_engine_override == ENGINE_QUEUE_NAIVE;
+  s.block = s.keymode && !force_queue &&
             (g_engine_override == ENGINE_BLOCK || (int64_t)n >= kBlockMinCells);
   s.plane[0] = keys;
   s.plane[1] = keys + n;
@@ -572,14 +595,21 @@ int launch_import(const int64_t *vr, const int64_t *seeds, int64_t n_seeds, int 
 
 int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_rounds,
                   cudaStream_t st) {
+  const int qm = g_engine_override == ENGINE_QUEUE_PF ? QM_PF
+                 : g_engine_override == ENGINE_QUEUE_NAIVE ? QM_NAIVE : QM_BQ;
   void *kern = s.keymode
                    ? (s.keycheck ? (conn == 8 ? (void *)edt_rounds_key_kernel<8, true>
                                               : (void *)edt_rounds_key_kernel<4, true>)
-                                 : (conn == 8 ? (void *)edt_rounds_key_kernel<8, false>
-                                              : (void *)edt_rounds_key_kernel<4, false>))
+                                 : (qm == QM_PF ? (conn == 8 ? (void *)edt_rounds_key_kernel<8, false, QM_PF>
+                                                             : (void *)edt_rounds_key_kernel<4, false, QM_PF>)
+                                    : qm == QM_NAIVE
+                                        ? (conn == 8 ? (void *)edt_rounds_key_kernel<8, false, QM_NAIVE>
+                                                     : (void *)edt_rounds_key_kernel<4, false, QM_NAIVE>)
+                                        : (conn == 8 ? (void *)edt_rounds_key_kernel<8, false>
+                                                     : (void *)edt_rounds_key_kernel<4, false>)))
                    : (conn == 8 ? (void *)edt_rounds_kernel<8> : (void *)edt_rounds_kernel<4>);
-  static int blocks_cache[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int &blocks = blocks_cache[(conn == 8) + 2 * s.keymode + 4 * s.keycheck];
+  static int blocks_cache[16] = {0};
+  int &blocks = blocks_cache[(conn == 8) + 2 * s.keymode + 4 * s.keycheck + 8 * (qm != QM_BQ)];
   if (blocks == 0) {
     int per_sm = 0;
     IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRoundThreads, 0));

@@ -47,7 +47,11 @@ inline bool cas_supported(int64_t W, int64_t H) {
 }
 // Engine selection (tests / diagnostics): 0 auto, 1 force the CAS engine,
 // 2 force range-checked keys.
-enum { ENGINE_AUTO = 0, ENGINE_CAS = 1, ENGINE_KEYCHECK = 2, ENGINE_QUEUE = 3, ENGINE_BLOCK = 4 };
+enum {
+  ENGINE_AUTO = 0, ENGINE_CAS = 1, ENGINE_KEYCHECK = 2, ENGINE_QUEUE = 3, ENGINE_BLOCK = 4,
+  ENGINE_QUEUE_PF = 5,    // queue engine, next frontier by warp reservations in global memory
+  ENGINE_QUEUE_NAIVE = 6  // queue engine, one global atomic per pushed item
+};
 // auto: the temporally blocked engine from this many cells up (measured on
 // B200: it wins on whole-slide images, the frontier queue on 4K tiles)
 constexpr int64_t kBlockMinCells = (int64_t)1 << 25;
