@@ -226,7 +226,7 @@ static int host_pipe_init(HostPipe &p) {
 // short.  `rows` > 0 forces uniform slabs of that height.  Returns false
 // (no pipelining) when the image is too small for two slabs.
 static bool host_slabs(int64_t W, int64_t H, size_t es, int64_t rows, std::vector<int64_t> &b) {
-  const int64_t TS = recon::TS;
+  const int64_t TS = recon::TSB;  // cuts on every engine's tile grid
   b.clear();
   bool taper = rows <= 0;
   if (rows <= 0) {
@@ -319,7 +319,6 @@ static int recon_host_pipelined(char *out, const char *marker, const char *mask,
   std::lock_guard<std::mutex> lock(hp->m);
   if ((rc = host_pipe_init(*hp))) return rc;
   const size_t es = elem_size(dtype), row_bytes = (size_t)W * es;
-  const int64_t TS = recon::TS, nty = (H + TS - 1) / TS;
   const int S = (int)bnd.size() - 1;
   Carver c2(rest);
   ReconWs w = carve_recon(c2, W, H);
@@ -334,6 +333,8 @@ static int recon_host_pipelined(char *out, const char *marker, const char *mask,
     eo.engine = opts->engine;
     eo.halo_thresh = opts->halo_sweep_threshold;
   }
+  // the engine's tile rows: slab cuts (multiples of TSB) fall on them
+  const int64_t TS = recon::tile_side(dtype, eo), nty = (H + TS - 1) / TS;
   Trace tr;
   tr.mark(st, "start", 0);
   IWPP_CUDA_TRY(cudaEventRecord(hp->start, st));

@@ -132,10 +132,15 @@ __device__ __forceinline__ void ring_push(const TileQueue &q, unsigned t) {
 // engine has terminated (no tile queued or running: nothing can be pushed
 // any more, and a filled slot would imply a queued tile).  Idle workers back
 // off to ~1 us so they do not steal issue slots from busy ones.
+#ifndef IWPP_POP_MAX_SLEEP_NS
+#define IWPP_POP_MAX_SLEEP_NS 2048
+#endif
+constexpr unsigned kPopMaxSleepNs = IWPP_POP_MAX_SLEEP_NS;
+
 __device__ __forceinline__ int ring_pop(const TileQueue &q) {
   unsigned ticket = atomicAdd(q.head, 1u);
   unsigned long long *slot = &q.ring[ticket & q.mask];
-  for (unsigned ns = 64;; ns = ns < 1024 ? ns * 2 : 1024) {
+  for (unsigned ns = 32;; ns = ns < kPopMaxSleepNs ? ns * 2 : kPopMaxSleepNs) {
     unsigned long long v = ld_acquire64(slot);
     if ((unsigned)(v >> 32) == ticket) return (int)(v & 0xffffffffu);
     if (ld_acquire(q.pending) == 0) return -1;
@@ -1113,12 +1118,15 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
 
 // --- binary engine (u8 storage, values 0 / 255) -------------------------------
 //
-// The "binary" element kind (grid.py binary, imfill): one bit per pixel, so
-// a 32 x 32 tile is one 32-bit word per lane (lane = row).  A Jacobi step is
-//     J <- I & (J | J_up | J_down | the same shifted by one column),
-// about a dozen instructions for the whole tile.  Same queue protocol.
-
-// 32 bytes of 0 / 255 (8 words) -> 32 bits (bit x = byte x != 0)
+// The "binary" element kind (grid.py binary, imfill): one bit per pixel.  A
+// warp owns a 64 x 64 tile -- lane = rows lane and lane + 32, two 32-bit
+// words per row -- so a Jacobi step
+//     J <- I & (J | J_up | J_down | the same shifted by one column)
+// is a few dozen instructions for 4096 pixels.  Binary fills are long
+// narrow fronts that cross the image tile by tile; 64-pixel tiles halve the
+// number of tile hops on that critical path.  Same queue protocol as the
+// other engines, on a 64-pixel tile grid.
+// 32 bytes (8 words) -> 32 bits, bit x = byte x != 0
 __device__ __forceinline__ unsigned bin_pack(const unsigned *w) {
   unsigned b = 0;
 #pragma unroll
@@ -1135,64 +1143,192 @@ __device__ __forceinline__ void bin_unpack(unsigned b, unsigned *w) {
   for (int k = 0; k < 8; k++) w[k] = ((((b >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu;
 }
 
-struct BinHalo {
-  unsigned row, rowI;      // lane 0: the row above (bits); lane 31: the row below
-  unsigned l, r, lI, rI;   // bits (0 / 1) of the cells left / right of my row
-  unsigned cl, cr, clI, crI;
-};
-
-__device__ __forceinline__ unsigned bin_row(const uint8_t *base, int W, int x0, int gy, int H,
-                                            bool vec, bool cg) {
+// 64 pixels of row gy from x0 -> two bit words (0 outside the image)
+__device__ __forceinline__ void bin_row64(const uint8_t *base, int W, int x0, int gy, int H, bool vec,
+                                          bool cg, unsigned &w0, unsigned &w1) {
   unsigned w[8];
   reg_load_row(base, W, x0, gy, H, vec, cg, w);
-  return bin_pack(w);
+  w0 = bin_pack(w);
+  reg_load_row(base, W, x0 + 32, gy, H, vec, cg, w);
+  w1 = bin_pack(w);
 }
+
+// rows gy and gy + 32 (64 pixels each from x0) -> bit words, with all eight
+// 16-byte loads in flight together (fast path: full, aligned tiles)
+__device__ __forceinline__ void bin_rows2(const uint8_t *base, int W, int x0, int gy, int H, bool vec,
+                                          bool cg, unsigned &a0, unsigned &a1, unsigned &b0,
+                                          unsigned &b1) {
+  if (vec && x0 + 64 <= W && gy + 32 < H && gy >= 0) {
+    const uint4 *pa = reinterpret_cast<const uint4 *>(base + (size_t)gy * W + x0);
+    const uint4 *pb = reinterpret_cast<const uint4 *>(base + (size_t)(gy + 32) * W + x0);
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      v[k] = cg ? __ldcg(pa + k) : __ldg(pa + k);
+      v[4 + k] = cg ? __ldcg(pb + k) : __ldg(pb + k);
+    }
+    unsigned w[8];
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      w[0] = v[2 * r].x; w[1] = v[2 * r].y; w[2] = v[2 * r].z; w[3] = v[2 * r].w;
+      w[4] = v[2 * r + 1].x; w[5] = v[2 * r + 1].y; w[6] = v[2 * r + 1].z; w[7] = v[2 * r + 1].w;
+      const unsigned bits = bin_pack(w);
+      if (r == 0) a0 = bits;
+      else if (r == 1) a1 = bits;
+      else if (r == 2) b0 = bits;
+      else b1 = bits;
+    }
+    return;
+  }
+  bin_row64(base, W, x0, gy, H, vec, cg, a0, a1);
+  bin_row64(base, W, x0, gy + 32, H, vec, cg, b0, b1);
+}
+
+// The whole tile (J and I rows lane and lane + 32) with all sixteen 16-byte
+// loads in flight together; the halo loads are issued before the packing so
+// their latency overlaps too.
+template <typename HaloFn>
+__device__ __forceinline__ void bin_tile_load(const EngineArgs &a, int x0, int y0, int lane,
+                                              unsigned &a0, unsigned &a1, unsigned &b0,
+                                              unsigned &b1, unsigned &ma0, unsigned &ma1,
+                                              unsigned &mb0, unsigned &mb1, HaloFn halo) {
+  const int gy = y0 + lane;
+  if (!(a.vec && x0 + 64 <= a.W && gy + 32 < a.H)) {
+    halo();
+    bin_rows2((const uint8_t *)a.J, a.W, x0, gy, a.H, a.vec, true, a0, a1, b0, b1);
+    bin_rows2((const uint8_t *)a.I, a.W, x0, gy, a.H, a.vec, false, ma0, ma1, mb0, mb1);
+    return;
+  }
+  const uint4 *ja = reinterpret_cast<const uint4 *>((const uint8_t *)a.J + (size_t)gy * a.W + x0);
+  const uint4 *jb = reinterpret_cast<const uint4 *>((const uint8_t *)a.J + (size_t)(gy + 32) * a.W + x0);
+  const uint4 *ia = reinterpret_cast<const uint4 *>((const uint8_t *)a.I + (size_t)gy * a.W + x0);
+  const uint4 *ib = reinterpret_cast<const uint4 *>((const uint8_t *)a.I + (size_t)(gy + 32) * a.W + x0);
+  uint4 v[16];
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    v[k] = __ldcg(ja + k);
+    v[4 + k] = __ldcg(jb + k);
+    v[8 + k] = __ldg(ia + k);
+    v[12 + k] = __ldg(ib + k);
+  }
+  halo();
+  unsigned out[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    unsigned w[8] = {v[2 * r].x, v[2 * r].y, v[2 * r].z, v[2 * r].w,
+                     v[2 * r + 1].x, v[2 * r + 1].y, v[2 * r + 1].z, v[2 * r + 1].w};
+    out[r] = bin_pack(w);
+  }
+  a0 = out[0]; a1 = out[1]; b0 = out[2]; b1 = out[3];
+  ma0 = out[4]; ma1 = out[5]; mb0 = out[6]; mb1 = out[7];
+}
+
+__device__ __forceinline__ void bin_store64(const EngineArgs &a, int x0, int gy, unsigned w0,
+                                            unsigned w1) {
+  if (gy >= a.H) return;
+  uint8_t *p = (uint8_t *)a.J + (size_t)gy * a.W + x0;
+  unsigned w[8];
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int xh = x0 + 32 * h;
+    if (xh >= a.W) break;
+    bin_unpack(h ? w1 : w0, w);
+    uint8_t *q = p + 32 * h;
+    if (a.vec && xh + 32 <= a.W) {
+      reinterpret_cast<uint4 *>(q)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      reinterpret_cast<uint4 *>(q)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+      for (int x = 0; x < 32 && xh + x < a.W; x++) q[x] = (uint8_t)(w[x >> 2] >> (8 * (x & 3)));
+    }
+  }
+}
+
+struct BinHalo {
+  unsigned row0, row1, rowI0, rowI1;  // lane 0: the row above (bits); lane 31: the row below
+  unsigned la, ra, lIa, rIa;          // bits left / right of row lane (J, I)
+  unsigned lb, rb, lIb, rIb;          // ... of row lane + 32
+  unsigned cl, cr, clI, crI;          // lane 0: corners above; lane 31: corners below
+};
 
 __device__ __forceinline__ void bin_load_halo(const EngineArgs &a, int x0, int y0, int lane,
                                               BinHalo &h) {
   const uint8_t *J = (const uint8_t *)a.J, *I = (const uint8_t *)a.I;
-  const int gy = y0 + lane;
-  const int hy = lane == 0 ? y0 - 1 : (lane == 31 ? y0 + TS : -1);
-  h.l = reg_cell(J, a.W, a.H, x0 - 1, gy, true) != 0;
-  h.r = reg_cell(J, a.W, a.H, x0 + TS, gy, true) != 0;
-  h.lI = reg_cell(I, a.W, a.H, x0 - 1, gy, false) != 0;
-  h.rI = reg_cell(I, a.W, a.H, x0 + TS, gy, false) != 0;
+  const int ya = y0 + lane, yb = y0 + lane + 32;
+  const int hy = lane == 0 ? y0 - 1 : (lane == 31 ? y0 + TSB : -1);
+  h.la = reg_cell(J, a.W, a.H, x0 - 1, ya, true) != 0;
+  h.ra = reg_cell(J, a.W, a.H, x0 + TSB, ya, true) != 0;
+  h.lIa = reg_cell(I, a.W, a.H, x0 - 1, ya, false) != 0;
+  h.rIa = reg_cell(I, a.W, a.H, x0 + TSB, ya, false) != 0;
+  h.lb = reg_cell(J, a.W, a.H, x0 - 1, yb, true) != 0;
+  h.rb = reg_cell(J, a.W, a.H, x0 + TSB, yb, true) != 0;
+  h.lIb = reg_cell(I, a.W, a.H, x0 - 1, yb, false) != 0;
+  h.rIb = reg_cell(I, a.W, a.H, x0 + TSB, yb, false) != 0;
   h.cl = reg_cell(J, a.W, a.H, x0 - 1, hy, true) != 0;
-  h.cr = reg_cell(J, a.W, a.H, x0 + TS, hy, true) != 0;
+  h.cr = reg_cell(J, a.W, a.H, x0 + TSB, hy, true) != 0;
   h.clI = reg_cell(I, a.W, a.H, x0 - 1, hy, false) != 0;
-  h.crI = reg_cell(I, a.W, a.H, x0 + TS, hy, false) != 0;
-  h.row = bin_row(J, a.W, x0, hy, a.H, a.vec, true);
-  h.rowI = bin_row(I, a.W, x0, hy, a.H, a.vec, false);
+  h.crI = reg_cell(I, a.W, a.H, x0 + TSB, hy, false) != 0;
+  bin_row64(J, a.W, x0, hy, a.H, a.vec, true, h.row0, h.row1);
+  bin_row64(I, a.W, x0, hy, a.H, a.vec, false, h.rowI0, h.rowI1);
+}
+
+// 3x3 (8-conn) / cross (4-conn) dilation of a 64-bit row (w0, w1) with the
+// halo bits at its ends
+__device__ __forceinline__ void bin_hdil(unsigned w0, unsigned w1, unsigned hl, unsigned hr,
+                                         unsigned &d0, unsigned &d1) {
+  d0 = w0 | (w0 << 1) | hl | (w0 >> 1) | (w1 << 31);
+  d1 = w1 | (w1 << 1) | (w0 >> 31) | (w1 >> 1) | (hr << 31);
 }
 
 template <int CONN>
-__device__ __forceinline__ int bin_fixpoint(unsigned &j, unsigned m, const BinHalo &h, int lane,
-                                            bool &changed) {
-  unsigned hlv = h.l, hrv = h.r;
+__device__ __forceinline__ int bin_fixpoint(unsigned &a0, unsigned &a1, unsigned &b0, unsigned &b1,
+                                            unsigned ma0, unsigned ma1, unsigned mb0, unsigned mb1,
+                                            const BinHalo &h, int lane, bool &changed) {
+  // halo column bits, vertically dilated for 8-conn (rows lane, lane + 32)
+  unsigned hla = h.la, hra = h.ra, hlb = h.lb, hrb = h.rb;
   if (CONN == 8) {
-    unsigned lu = __shfl_up_sync(FULL, h.l, 1), ld = __shfl_down_sync(FULL, h.l, 1);
-    unsigned ru = __shfl_up_sync(FULL, h.r, 1), rd = __shfl_down_sync(FULL, h.r, 1);
-    if (lane == 0) { lu = h.cl; ru = h.cr; }
-    if (lane == 31) { ld = h.cl; rd = h.cr; }
-    hlv = h.l | lu | ld;
-    hrv = h.r | ru | rd;
+    unsigned lau = __shfl_up_sync(FULL, h.la, 1), lad = __shfl_down_sync(FULL, h.la, 1);
+    unsigned rau = __shfl_up_sync(FULL, h.ra, 1), rad = __shfl_down_sync(FULL, h.ra, 1);
+    unsigned lbu = __shfl_up_sync(FULL, h.lb, 1), lbd = __shfl_down_sync(FULL, h.lb, 1);
+    unsigned rbu = __shfl_up_sync(FULL, h.rb, 1), rbd = __shfl_down_sync(FULL, h.rb, 1);
+    const unsigned lb0 = __shfl_sync(FULL, h.lb, 0), rb0 = __shfl_sync(FULL, h.rb, 0);
+    const unsigned la31 = __shfl_sync(FULL, h.la, 31), ra31 = __shfl_sync(FULL, h.ra, 31);
+    if (lane == 0) { lau = h.cl; rau = h.cr; lbu = la31; rbu = ra31; }
+    if (lane == 31) { lad = lb0; rad = rb0; lbd = h.cl; rbd = h.cr; }
+    hla = h.la | lau | lad;
+    hra = h.ra | rau | rad;
+    hlb = h.lb | lbu | lbd;
+    hrb = h.rb | rbu | rbd;
   }
   int steps = 0;
   for (;;) {
     steps++;
-    unsigned u = __shfl_up_sync(FULL, j, 1), d = __shfl_down_sync(FULL, j, 1);
-    if (lane == 0) u = h.row;
-    if (lane == 31) d = h.row;
-    unsigned D;
+    // rows above / below: row lane +- 1 and row lane + 32 +- 1
+    unsigned ua0 = __shfl_up_sync(FULL, a0, 1), ua1 = __shfl_up_sync(FULL, a1, 1);
+    unsigned da0 = __shfl_down_sync(FULL, a0, 1), da1 = __shfl_down_sync(FULL, a1, 1);
+    unsigned ub0 = __shfl_up_sync(FULL, b0, 1), ub1 = __shfl_up_sync(FULL, b1, 1);
+    unsigned db0 = __shfl_down_sync(FULL, b0, 1), db1 = __shfl_down_sync(FULL, b1, 1);
+    const unsigned b00 = __shfl_sync(FULL, b0, 0), b10 = __shfl_sync(FULL, b1, 0);
+    const unsigned a031 = __shfl_sync(FULL, a0, 31), a131 = __shfl_sync(FULL, a1, 31);
+    if (lane == 0) { ua0 = h.row0; ua1 = h.row1; ub0 = a031; ub1 = a131; }
+    if (lane == 31) { da0 = b00; da1 = b10; db0 = h.row0; db1 = h.row1; }
+    unsigned Da0, Da1, Db0, Db1;
     if (CONN == 8) {
-      const unsigned v = j | u | d;
-      D = v | (v << 1) | hlv | (v >> 1) | (hrv << 31);
+      bin_hdil(a0 | ua0 | da0, a1 | ua1 | da1, hla, hra, Da0, Da1);
+      bin_hdil(b0 | ub0 | db0, b1 | ub1 | db1, hlb, hrb, Db0, Db1);
     } else {
-      D = j | u | d | (j << 1) | h.l | (j >> 1) | (h.r << 31);
+      bin_hdil(a0, a1, h.la, h.ra, Da0, Da1);
+      bin_hdil(b0, b1, h.lb, h.rb, Db0, Db1);
+      Da0 |= ua0 | da0;
+      Da1 |= ua1 | da1;
+      Db0 |= ub0 | db0;
+      Db1 |= ub1 | db1;
     }
-    const unsigned nj = m & D;
-    const bool ch = nj != j;
-    j = nj;
+    const unsigned na0 = ma0 & Da0, na1 = ma1 & Da1, nb0 = mb0 & Db0, nb1 = mb1 & Db1;
+    const bool ch = ((na0 ^ a0) | (na1 ^ a1) | (nb0 ^ b0) | (nb1 ^ b1)) != 0;
+    a0 = na0;
+    a1 = na1;
+    b0 = nb0;
+    b1 = nb1;
     if (!__any_sync(FULL, ch)) break;
     changed = true;
   }
@@ -1203,7 +1339,7 @@ template <int CONN>
 __global__ void __launch_bounds__(kCtaThreads)
     tile_engine_bin_kernel(EngineArgs a, unsigned long long *counters) {
   const int lane = threadIdx.x & 31;
-  const bool l0 = lane == 0;
+  const bool l0 = lane == 0, l31 = lane == 31;
   unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0;
   unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
   int next_tile = -1;
@@ -1221,14 +1357,17 @@ __global__ void __launch_bounds__(kCtaThreads)
     next_tile = -1;
     if (t < 0) break;
     const int tx = t % a.ntx, ty = t / a.ntx;
-    const int x0 = tx * TS, y0 = ty * TS;
+    const int x0 = tx * TSB, y0 = ty * TSB;
     long long c_load = l0 ? clock64() : 0;
     if (l0) ph[0] += c_load - c_pop;
-    unsigned j = bin_row((const uint8_t *)a.J, a.W, x0, y0 + lane, a.H, a.vec, true);
-    const unsigned m = bin_row((const uint8_t *)a.I, a.W, x0, y0 + lane, a.H, a.vec, false);
+    const uint8_t *Jb = (const uint8_t *)a.J, *Ib = (const uint8_t *)a.I;
+    unsigned a0, a1, b0, b1, ma0, ma1, mb0, mb1;
     BinHalo h;
-    bin_load_halo(a, x0, y0, lane, h);
-    unsigned ob = j;  // my row as last published
+    bin_tile_load(a, x0, y0, lane, a0, a1, b0, b1, ma0, ma1, mb0, mb1,
+                  [&]() { bin_load_halo(a, x0, y0, lane, h); });
+    (void)Jb;
+    (void)Ib;
+    unsigned oa0 = a0, oa1 = a1, ob0 = b0, ob1 = b1;  // as last published
     if (l0) ph[1] += clock64() - c_load;
     bool rerun = false;
     for (;;) {
@@ -1236,52 +1375,67 @@ __global__ void __launch_bounds__(kCtaThreads)
       n_reruns += l0 && rerun;
       long long c_fix = l0 ? clock64() : 0;
       bool changed = false;
-      const int steps = bin_fixpoint<CONN>(j, m, h, lane, changed);
+      const int steps = bin_fixpoint<CONN>(a0, a1, b0, b1, ma0, ma1, mb0, mb1, h, lane, changed);
       if (l0) n_steps += steps;
       changed = __any_sync(FULL, changed);
       long long c_st = l0 ? clock64() : 0;
       if (l0) ph[2] += c_st - c_fix;
       if (changed) {
-        const int gy = y0 + lane;
-        if (gy < a.H && j != ob) {
-          unsigned w[8];
-          bin_unpack(j, w);
-          uint8_t *p = (uint8_t *)a.J + (size_t)gy * a.W + x0;
-          if (a.vec && x0 + TS <= a.W) {
-            reinterpret_cast<uint4 *>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            reinterpret_cast<uint4 *>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
-          } else {
-            for (int x = 0; x < TS && x0 + x < a.W; x++) p[x] = (uint8_t)(w[x >> 2] >> (8 * (x & 3)));
-          }
-        }
+        if (a0 != oa0 || a1 != oa1) bin_store64(a, x0, y0 + lane, a0, a1);
+        if (b0 != ob0 || b1 != ob1) bin_store64(a, x0, y0 + lane + 32, b0, b1);
         if (a.dirty && l0) a.dirty[ty] = 1;
-        // neighbours a newly set border cell can still raise (halo J = 0, I = 1)
-        const unsigned cv = j & ~ob;
-        const unsigned Dr = CONN == 8 ? (cv | (cv << 1) | (cv >> 1)) : cv;
-        const unsigned need_row = Dr & h.rowI & ~h.row;
-        const unsigned cl = cv & 1u, cr = cv >> 31;
-        unsigned dl = cl, dr = cr;
+        // newly set border cells; a neighbour needs a re-run where such a
+        // cell (dilated along the border for 8-conn) meets a halo cell with
+        // J = 0, I = 1
+        const unsigned ca0 = a0 & ~oa0, ca1 = a1 & ~oa1, cb0 = b0 & ~ob0, cb1 = b1 & ~ob1;
+        unsigned need_row = 0;
+        {
+          const unsigned c0 = l0 ? ca0 : cb0, c1 = l0 ? ca1 : cb1;  // lane 0: top, 31: bottom
+          unsigned d0 = c0, d1 = c1;
+          if (CONN == 8) {
+            d0 = c0 | (c0 << 1) | (c0 >> 1) | (c1 << 31);
+            d1 = c1 | (c1 << 1) | (c0 >> 31) | (c1 >> 1);
+          }
+          need_row = (d0 & h.rowI0 & ~h.row0) | (d1 & h.rowI1 & ~h.row1);
+        }
+        const unsigned cla = ca0 & 1u, clb = cb0 & 1u, cra = ca1 >> 31, crb = cb1 >> 31;
+        unsigned dla = cla, dlb = clb, dra = cra, drb = crb;
         if (CONN == 8) {
-          unsigned lu = __shfl_up_sync(FULL, cl, 1), ld = __shfl_down_sync(FULL, cl, 1);
-          unsigned ru = __shfl_up_sync(FULL, cr, 1), rd = __shfl_down_sync(FULL, cr, 1);
-          if (lane == 0) lu = ru = 0;
-          if (lane == 31) ld = rd = 0;
-          dl |= lu | ld;
-          dr |= ru | rd;
+          unsigned u, d;
+          const unsigned clb0 = __shfl_sync(FULL, clb, 0), crb0 = __shfl_sync(FULL, crb, 0);
+          const unsigned cla31 = __shfl_sync(FULL, cla, 31), cra31 = __shfl_sync(FULL, cra, 31);
+          u = __shfl_up_sync(FULL, cla, 1); d = __shfl_down_sync(FULL, cla, 1);
+          if (l0) u = 0;
+          if (l31) d = clb0;
+          dla |= u | d;
+          u = __shfl_up_sync(FULL, clb, 1); d = __shfl_down_sync(FULL, clb, 1);
+          if (l0) u = cla31;
+          if (l31) d = 0;
+          dlb |= u | d;
+          u = __shfl_up_sync(FULL, cra, 1); d = __shfl_down_sync(FULL, cra, 1);
+          if (l0) u = 0;
+          if (l31) d = crb0;
+          dra |= u | d;
+          u = __shfl_up_sync(FULL, crb, 1); d = __shfl_down_sync(FULL, crb, 1);
+          if (l0) u = cra31;
+          if (l31) d = 0;
+          drb |= u | d;
         }
         unsigned dirs = 0;
-        if (__any_sync(FULL, l0 && need_row)) dirs |= 1u << 1;          // N
-        if (__any_sync(FULL, lane == 31 && need_row)) dirs |= 1u << 7;  // S
-        if (__any_sync(FULL, dl & h.lI & ~h.l)) dirs |= 1u << 3;          // W
-        if (__any_sync(FULL, dr & h.rI & ~h.r)) dirs |= 1u << 5;          // E
+        if (__any_sync(FULL, l0 && need_row)) dirs |= 1u << 1;   // N
+        if (__any_sync(FULL, l31 && need_row)) dirs |= 1u << 7;  // S
+        if (__any_sync(FULL, (dla & h.lIa & ~h.la) | (dlb & h.lIb & ~h.lb))) dirs |= 1u << 3;  // W
+        if (__any_sync(FULL, (dra & h.rIa & ~h.ra) | (drb & h.rIb & ~h.rb))) dirs |= 1u << 5;  // E
         if (CONN == 8) {
-          const bool cwl = cl & h.clI & ~h.cl, cwr = cr & h.crI & ~h.cr;
-          if (__any_sync(FULL, l0 && cwl)) dirs |= 1u << 0;
-          if (__any_sync(FULL, l0 && cwr)) dirs |= 1u << 2;
-          if (__any_sync(FULL, lane == 31 && cwl)) dirs |= 1u << 6;
-          if (__any_sync(FULL, lane == 31 && cwr)) dirs |= 1u << 8;
+          if (__any_sync(FULL, l0 && (cla & h.clI & ~h.cl))) dirs |= 1u << 0;
+          if (__any_sync(FULL, l0 && (cra & h.crI & ~h.cr))) dirs |= 1u << 2;
+          if (__any_sync(FULL, l31 && (clb & h.clI & ~h.cl))) dirs |= 1u << 6;
+          if (__any_sync(FULL, l31 && (crb & h.crI & ~h.cr))) dirs |= 1u << 8;
         }
-        ob = j;
+        oa0 = a0;
+        oa1 = a1;
+        ob0 = b0;
+        ob1 = b1;
         fence_acq_rel();  // publish the tile before any neighbour is (re)queued
         __syncwarp();
         bool own = false;
@@ -1467,11 +1621,21 @@ static bool use_reg_engine(const EngineOpts &o) {
   return o.qcap <= 0 && o.sweeps_set == 0;
 }
 
+static bool use_bin_engine(bool binary, const EngineOpts &o) {
+  return binary && o.engine != ENGINE_SMEM && o.engine != ENGINE_REG && o.qcap <= 0 &&
+         o.sweeps_set == 0;
+}
+
+int tile_side(int dtype, const EngineOpts &o) {
+  return use_bin_engine(dtype == IWPP_BIN, o) ? TSB : TS;
+}
+
 template <typename T, int CONN>
 static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
                          unsigned long long *counters, const EngineOpts &o, cudaStream_t st,
                          bool binary = false) {
-  int ntx = (W + TS - 1) / TS, nty = (H + TS - 1) / TS;
+  const int ts = use_bin_engine(binary, o) ? TSB : TS;
+  int ntx = (W + ts - 1) / ts, nty = (H + ts - 1) / ts;
   unsigned ntiles = (unsigned)ntx * nty;
   size_t smem = sizeof(WarpSmem<T>) * kWarpsPerCta;
   auto kern = tile_engine_kernel<T, CONN>;
@@ -1505,8 +1669,7 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   bool vec = ((size_t)W * sizeof(T)) % 16 == 0 && (uintptr_t)J % 16 == 0 && (uintptr_t)I % 16 == 0;
   EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, o.dirty, q};
   if (o.ev_begin) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_begin, st));
-  if (binary && o.engine != ENGINE_SMEM && o.engine != ENGINE_REG && o.qcap <= 0 &&
-      o.sweeps_set == 0) {
+  if (use_bin_engine(binary, o)) {
     static int bin_blocks = 0;
     if (bin_blocks == 0) {
       int per_sm = 0;

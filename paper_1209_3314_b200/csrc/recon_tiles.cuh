@@ -7,6 +7,7 @@ namespace recon {
 
 // One warp owns one TS x TS tile at a time (plus a 1-pixel halo).
 constexpr int TS = 32;                   // tile side
+constexpr int TSB = 64;                  // the binary engine's tile side (the largest)
 constexpr int PW = TS + 2;               // logical tile side with the halo
 constexpr int PS = PW + 1;               // shared-memory row stride (odd: conflict-free)
 constexpr int PN = PW * PW;              // logical cells
@@ -66,6 +67,9 @@ size_t tile_queue_bytes(unsigned ntiles);
 TileQueue carve_tile_queue(Carver &c, unsigned ntiles);
 int run_tile_engine(void *J, const void *I, int W, int H, int dtype, int conn, TileQueue q,
                     unsigned long long *counters, const EngineOpts &o, cudaStream_t st);
+// side of the square tiles the engine run_tile_engine picks for (dtype, o)
+// works on: sel_lo / sel_hi and the dirty flags count rows of these tiles
+int tile_side(int dtype, const EngineOpts &o);
 
 inline unsigned num_tiles(int64_t W, int64_t H) {
   return (unsigned)(((W + TS - 1) / TS) * ((H + TS - 1) / TS));

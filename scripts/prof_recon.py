@@ -21,7 +21,8 @@ elif case == "imfill":
 dJ, dI = torch.from_numpy(J).cuda(), torch.from_numpy(I).cuda()
 L = _lib.lib()
 H, W = J.shape
-ws = _lib.workspace(L.iwpp_recon_workspace_bytes(W, H, 0, conn))
+DT = int(os.environ.get("DTYPE", "0"))
+ws = _lib.workspace(L.iwpp_recon_workspace_bytes(W, H, DT, conn))
 out = dJ.clone()
 o = _lib.ReconOpts(); o.engine = int(os.environ.get("ENGINE", "0")); o.sweeps = int(os.environ.get("GSW", "0")); o.max_blocks = mb; o.check_contract = 0; o.queue_capacity = 0; o.tile_sweeps = tsw; o.halo_sweep_threshold = hth
 st = _lib.Stats()
@@ -30,11 +31,11 @@ for r in range(reps + 2):
     out.copy_(dJ)
     a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
     a.record()
-    _lib.check(L.iwpp_recon(_lib.ptr(out), _lib.ptr(dI), W, H, 0, conn, _lib.ptr(ws), ws.numel(), _lib.ctypes.byref(o), None, _lib.stream_ptr()))
+    _lib.check(L.iwpp_recon(_lib.ptr(out), _lib.ptr(dI), W, H, DT, conn, _lib.ptr(ws), ws.numel(), _lib.ctypes.byref(o), None, _lib.stream_ptr()))
     b.record(); torch.cuda.synchronize()
     if r >= 2: ts.append(a.elapsed_time(b))
 out.copy_(dJ)
-_lib.check(L.iwpp_recon(_lib.ptr(out), _lib.ptr(dI), W, H, 0, conn, _lib.ptr(ws), ws.numel(), _lib.ctypes.byref(o), _lib.ctypes.byref(st), _lib.stream_ptr()))
+_lib.check(L.iwpp_recon(_lib.ptr(out), _lib.ptr(dI), W, H, DT, conn, _lib.ptr(ws), ws.numel(), _lib.ctypes.byref(o), _lib.ctypes.byref(st), _lib.stream_ptr()))
 cnt = (_lib.ctypes.c_uint64 * 16)()
 L.iwpp_recon_engine_counters(_lib.ptr(ws), W, H, cnt, 16, _lib.stream_ptr())
 phs = list(cnt)[8:14]; tot = sum(phs) or 1
