@@ -107,6 +107,7 @@ size_t iwpp_recon_workspace_bytes(int64_t W, int64_t H, int dtype, int conn) {
   (void)conn;
   size_t b = recon_ws_bytes(W, H);
   if (dtype == IWPP_F32) b += align_up((size_t)W * H * 4, 256) + 256;  // the mask as ordered ints
+  if (dtype == IWPP_BIN) b += 2 * align_up(recon::bin_plane_words(W, H) * 4, 256) + 256;  // bit planes
   return b;
 }
 
@@ -171,8 +172,20 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
     eo.ev_end = opts->ev_end;
     eo.rows_mode = opts->slab_rows & 3;
   }
-  if ((rc = recon::run_tile_engine(J, I, (int)W, (int)H, dtype, conn, w.q, w.counters, eo, st)))
+  if (dtype == IWPP_BIN && recon::tile_side(IWPP_BIN, eo) != recon::TSB)
+    dtype = IWPP_U8;  // a byte engine was asked for: 0 / 255 is ordinary grey data
+  if (dtype == IWPP_BIN) {  // the bit-plane engine: pack, propagate, unpack
+    const size_t nw = recon::bin_plane_words(W, H);
+    uint32_t *Jb = c.take<uint32_t>(nw), *Ib = c.take<uint32_t>(nw);
+    if ((rc = recon::bin_pack(J, (int)W, (int)H, Jb, st))) return rc;
+    if ((rc = recon::bin_pack(I, (int)W, (int)H, Ib, st))) return rc;
+    if ((rc = recon::run_tile_engine(Jb, Ib, (int)W, (int)H, IWPP_BIN, conn, w.q, w.counters, eo, st)))
+      return rc;
+    if ((rc = recon::bin_unpack(Jb, (int)W, (int)H, J, st))) return rc;
+  } else if ((rc = recon::run_tile_engine(J, I, (int)W, (int)H, dtype, conn, w.q, w.counters, eo,
+                                          st))) {
     return rc;
+  }
   if (opts && opts->check_contract) {
     if ((rc = recon::check_le(J, I, (size_t)W * H, dtype, &w.counters[recon::CNT_VIOL], st)))
       return rc;
@@ -185,7 +198,9 @@ size_t iwpp_recon_host_workspace_bytes(int64_t W, int64_t H, int dtype, int conn
   (void)conn;
   size_t img = align_up((size_t)W * H * elem_size(dtype), 256);
   size_t nty = (size_t)((H + recon::TS - 1) / recon::TS);
-  return 2 * img + align_up(nty, 256) + recon_ws_bytes(W, H) + 512;
+  // the device call runs on the copies (f32 is converted in place first)
+  const size_t inner = iwpp_recon_workspace_bytes(W, H, dtype == IWPP_F32 ? IWPP_I32 : dtype, conn);
+  return 2 * img + align_up(nty, 256) + inner + 512;
 }
 
 }  // extern "C"
@@ -437,7 +452,7 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   size_t rest_bytes = workspace_bytes - align_up(c.off, 256);
   std::vector<int64_t> bnd;
   const bool pipelined =
-      dtype != IWPP_F32 &&
+      dtype != IWPP_F32 && dtype != IWPP_BIN &&
       !(opts && (opts->sweeps > 0 || opts->slab_rows || opts->pipeline_rows < 0)) &&
       host_slabs(W, H, es, opts ? opts->pipeline_rows : 0, bnd);
   if (pipelined)
@@ -465,6 +480,7 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   }
   if ((rc = iwpp_recon(dJ, dI, W, H, edtype, conn, rest, rest_bytes, &o, nullptr, stream))) return rc;
   if (dtype == IWPP_F32 && (rc = recon::ord_to_f32(dJ, dJ, (size_t)W * H, st))) return rc;
+  (void)0;
   IWPP_CUDA_TRY(cudaMemcpyAsync(out, dJ, nb, cudaMemcpyDeviceToHost, st));
   IWPP_CUDA_TRY(cudaStreamSynchronize(st));
   if (viol) return set_error(IWPP_E_CONTRACT, "marker exceeds mask somewhere (%llu cells)", viol);

@@ -50,6 +50,7 @@
 // is bit-exact with recon_fh.
 
 #include <climits>
+#include <cstdlib>
 
 #include "iwpp_common.cuh"
 #include "recon_tiles.cuh"
@@ -80,6 +81,7 @@ struct EngineArgs {
   int sweeps;            // sweep passes on a tile's first visit
   int vec;               // rows are 16-byte aligned
   uint8_t *dirty;        // per tile row: written by this run (nullable)
+  int WW;                // binary engine: words per bit-plane row
   TileQueue q;
 };
 
@@ -132,6 +134,8 @@ __device__ __forceinline__ void ring_push(const TileQueue &q, unsigned t) {
 // engine has terminated (no tile queued or running: nothing can be pushed
 // any more, and a filled slot would imply a queued tile).  Idle workers back
 // off to ~1 us so they do not steal issue slots from busy ones.
+constexpr int kBinCtasPerSm = 4;
+
 #ifndef IWPP_POP_MAX_SLEEP_NS
 #define IWPP_POP_MAX_SLEEP_NS 2048
 #endif
@@ -1116,159 +1120,61 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
   }
 }
 
-// --- binary engine (u8 storage, values 0 / 255) -------------------------------
+// --- binary engine (bit planes) ------------------------------------------------
 //
-// The "binary" element kind (grid.py binary, imfill): one bit per pixel.  A
-// warp owns a 64 x 64 tile -- lane = rows lane and lane + 32, two 32-bit
-// words per row -- so a Jacobi step
+// The "binary" element kind (grid.py binary, imfill).  iwpp_recon packs the
+// 0 / 255 marker and mask into bit planes (one bit per pixel, ceil(W/32)
+// words per row) and unpacks the result afterwards, so the engine moves
+// 1/8 of the bytes and does no byte arithmetic.  A warp owns a 64 x 64 tile
+// -- lane = rows lane and lane + 32, two words per row -- and a Jacobi step
 //     J <- I & (J | J_up | J_down | the same shifted by one column)
-// is a few dozen instructions for 4096 pixels.  Binary fills are long
-// narrow fronts that cross the image tile by tile; 64-pixel tiles halve the
-// number of tile hops on that critical path.  Same queue protocol as the
-// other engines, on a 64-pixel tile grid.
-// 32 bytes (8 words) -> 32 bits, bit x = byte x != 0
-__device__ __forceinline__ unsigned bin_pack(const unsigned *w) {
-  unsigned b = 0;
-#pragma unroll
-  for (int k = 0; k < 8; k++) {
-    const unsigned t = (w[k] | (w[k] << 1) | (w[k] << 2) | (w[k] << 3) | (w[k] << 4) |
-                        (w[k] << 5) | (w[k] << 6) | (w[k] << 7)) & 0x80808080u;  // any bit set
-    b |= ((t * 0x00204081u) >> 28) << (4 * k);
-  }
-  return b;
-}
-// 32 bits -> 32 bytes of 0 / 255
-__device__ __forceinline__ void bin_unpack(unsigned b, unsigned *w) {
-#pragma unroll
-  for (int k = 0; k < 8; k++) w[k] = ((((b >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu;
-}
+// is a few dozen instructions for 4096 pixels.  Binary fills are long narrow
+// fronts crossing the image tile by tile; 64-pixel tiles halve the tile hops
+// on that critical path.  Same queue protocol, on a 64-pixel tile grid.
 
-// 64 pixels of row gy from x0 -> two bit words (0 outside the image)
-__device__ __forceinline__ void bin_row64(const uint8_t *base, int W, int x0, int gy, int H, bool vec,
-                                          bool cg, unsigned &w0, unsigned &w1) {
-  unsigned w[8];
-  reg_load_row(base, W, x0, gy, H, vec, cg, w);
-  w0 = bin_pack(w);
-  reg_load_row(base, W, x0 + 32, gy, H, vec, cg, w);
-  w1 = bin_pack(w);
-}
-
-// rows gy and gy + 32 (64 pixels each from x0) -> bit words, with all eight
-// 16-byte loads in flight together (fast path: full, aligned tiles)
-__device__ __forceinline__ void bin_rows2(const uint8_t *base, int W, int x0, int gy, int H, bool vec,
-                                          bool cg, unsigned &a0, unsigned &a1, unsigned &b0,
-                                          unsigned &b1) {
-  if (vec && x0 + 64 <= W && gy + 32 < H && gy >= 0) {
-    const uint4 *pa = reinterpret_cast<const uint4 *>(base + (size_t)gy * W + x0);
-    const uint4 *pb = reinterpret_cast<const uint4 *>(base + (size_t)(gy + 32) * W + x0);
-    uint4 v[8];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-      v[k] = cg ? __ldcg(pa + k) : __ldg(pa + k);
-      v[4 + k] = cg ? __ldcg(pb + k) : __ldg(pb + k);
-    }
-    unsigned w[8];
-#pragma unroll
-    for (int r = 0; r < 4; r++) {
-      w[0] = v[2 * r].x; w[1] = v[2 * r].y; w[2] = v[2 * r].z; w[3] = v[2 * r].w;
-      w[4] = v[2 * r + 1].x; w[5] = v[2 * r + 1].y; w[6] = v[2 * r + 1].z; w[7] = v[2 * r + 1].w;
-      const unsigned bits = bin_pack(w);
-      if (r == 0) a0 = bits;
-      else if (r == 1) a1 = bits;
-      else if (r == 2) b0 = bits;
-      else b1 = bits;
-    }
-    return;
-  }
-  bin_row64(base, W, x0, gy, H, vec, cg, a0, a1);
-  bin_row64(base, W, x0, gy + 32, H, vec, cg, b0, b1);
-}
-
-// The whole tile (J and I rows lane and lane + 32) with all sixteen 16-byte
-// loads in flight together; the halo loads are issued before the packing so
-// their latency overlaps too.
-template <typename HaloFn>
-__device__ __forceinline__ void bin_tile_load(const EngineArgs &a, int x0, int y0, int lane,
-                                              unsigned &a0, unsigned &a1, unsigned &b0,
-                                              unsigned &b1, unsigned &ma0, unsigned &ma1,
-                                              unsigned &mb0, unsigned &mb1, HaloFn halo) {
-  const int gy = y0 + lane;
-  if (!(a.vec && x0 + 64 <= a.W && gy + 32 < a.H)) {
-    halo();
-    bin_rows2((const uint8_t *)a.J, a.W, x0, gy, a.H, a.vec, true, a0, a1, b0, b1);
-    bin_rows2((const uint8_t *)a.I, a.W, x0, gy, a.H, a.vec, false, ma0, ma1, mb0, mb1);
-    return;
-  }
-  const uint4 *ja = reinterpret_cast<const uint4 *>((const uint8_t *)a.J + (size_t)gy * a.W + x0);
-  const uint4 *jb = reinterpret_cast<const uint4 *>((const uint8_t *)a.J + (size_t)(gy + 32) * a.W + x0);
-  const uint4 *ia = reinterpret_cast<const uint4 *>((const uint8_t *)a.I + (size_t)gy * a.W + x0);
-  const uint4 *ib = reinterpret_cast<const uint4 *>((const uint8_t *)a.I + (size_t)(gy + 32) * a.W + x0);
-  uint4 v[16];
-#pragma unroll
-  for (int k = 0; k < 4; k++) {
-    v[k] = __ldcg(ja + k);
-    v[4 + k] = __ldcg(jb + k);
-    v[8 + k] = __ldg(ia + k);
-    v[12 + k] = __ldg(ib + k);
-  }
-  halo();
-  unsigned out[8];
-#pragma unroll
-  for (int r = 0; r < 8; r++) {
-    unsigned w[8] = {v[2 * r].x, v[2 * r].y, v[2 * r].z, v[2 * r].w,
-                     v[2 * r + 1].x, v[2 * r + 1].y, v[2 * r + 1].z, v[2 * r + 1].w};
-    out[r] = bin_pack(w);
-  }
-  a0 = out[0]; a1 = out[1]; b0 = out[2]; b1 = out[3];
-  ma0 = out[4]; ma1 = out[5]; mb0 = out[6]; mb1 = out[7];
-}
-
-__device__ __forceinline__ void bin_store64(const EngineArgs &a, int x0, int gy, unsigned w0,
-                                            unsigned w1) {
-  if (gy >= a.H) return;
-  uint8_t *p = (uint8_t *)a.J + (size_t)gy * a.W + x0;
-  unsigned w[8];
-#pragma unroll
-  for (int h = 0; h < 2; h++) {
-    const int xh = x0 + 32 * h;
-    if (xh >= a.W) break;
-    bin_unpack(h ? w1 : w0, w);
-    uint8_t *q = p + 32 * h;
-    if (a.vec && xh + 32 <= a.W) {
-      reinterpret_cast<uint4 *>(q)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-      reinterpret_cast<uint4 *>(q)[1] = make_uint4(w[4], w[5], w[6], w[7]);
-    } else {
-      for (int x = 0; x < 32 && xh + x < a.W; x++) q[x] = (uint8_t)(w[x >> 2] >> (8 * (x & 3)));
-    }
-  }
+__device__ __forceinline__ unsigned bitw(const uint32_t *P, int WW, int H, int wx, int gy, bool cg) {
+  if (gy < 0 || gy >= H || wx < 0 || wx >= WW) return 0u;
+  const uint32_t *p = P + (size_t)gy * WW + wx;
+  return cg ? __ldcg(p) : __ldg(p);
 }
 
 struct BinHalo {
-  unsigned row0, row1, rowI0, rowI1;  // lane 0: the row above (bits); lane 31: the row below
+  unsigned row0, row1, rowI0, rowI1;  // lane 0: the row above; lane 31: the row below
   unsigned la, ra, lIa, rIa;          // bits left / right of row lane (J, I)
   unsigned lb, rb, lIb, rIb;          // ... of row lane + 32
   unsigned cl, cr, clI, crI;          // lane 0: corners above; lane 31: corners below
 };
 
-__device__ __forceinline__ void bin_load_halo(const EngineArgs &a, int x0, int y0, int lane,
-                                              BinHalo &h) {
-  const uint8_t *J = (const uint8_t *)a.J, *I = (const uint8_t *)a.I;
-  const int ya = y0 + lane, yb = y0 + lane + 32;
+// the tile (rows lane, lane + 32; words wx0, wx0 + 1) and its halo: every
+// load issued before any is used
+__device__ __forceinline__ void bin_load(const EngineArgs &a, int x0, int y0, int lane, bool tile,
+                                         unsigned *jt, unsigned *mt, BinHalo &h) {
+  const uint32_t *J = (const uint32_t *)a.J, *I = (const uint32_t *)a.I;
+  const int WW = a.WW, wx = x0 >> 5, ya = y0 + lane, yb = ya + 32;
   const int hy = lane == 0 ? y0 - 1 : (lane == 31 ? y0 + TSB : -1);
-  h.la = reg_cell(J, a.W, a.H, x0 - 1, ya, true) != 0;
-  h.ra = reg_cell(J, a.W, a.H, x0 + TSB, ya, true) != 0;
-  h.lIa = reg_cell(I, a.W, a.H, x0 - 1, ya, false) != 0;
-  h.rIa = reg_cell(I, a.W, a.H, x0 + TSB, ya, false) != 0;
-  h.lb = reg_cell(J, a.W, a.H, x0 - 1, yb, true) != 0;
-  h.rb = reg_cell(J, a.W, a.H, x0 + TSB, yb, true) != 0;
-  h.lIb = reg_cell(I, a.W, a.H, x0 - 1, yb, false) != 0;
-  h.rIb = reg_cell(I, a.W, a.H, x0 + TSB, yb, false) != 0;
-  h.cl = reg_cell(J, a.W, a.H, x0 - 1, hy, true) != 0;
-  h.cr = reg_cell(J, a.W, a.H, x0 + TSB, hy, true) != 0;
-  h.clI = reg_cell(I, a.W, a.H, x0 - 1, hy, false) != 0;
-  h.crI = reg_cell(I, a.W, a.H, x0 + TSB, hy, false) != 0;
-  bin_row64(J, a.W, x0, hy, a.H, a.vec, true, h.row0, h.row1);
-  bin_row64(I, a.W, x0, hy, a.H, a.vec, false, h.rowI0, h.rowI1);
+  if (tile) {
+    jt[0] = bitw(J, WW, a.H, wx, ya, true);
+    jt[1] = bitw(J, WW, a.H, wx + 1, ya, true);
+    jt[2] = bitw(J, WW, a.H, wx, yb, true);
+    jt[3] = bitw(J, WW, a.H, wx + 1, yb, true);
+    mt[0] = bitw(I, WW, a.H, wx, ya, false);
+    mt[1] = bitw(I, WW, a.H, wx + 1, ya, false);
+    mt[2] = bitw(I, WW, a.H, wx, yb, false);
+    mt[3] = bitw(I, WW, a.H, wx + 1, yb, false);
+  }
+  const unsigned jla = bitw(J, WW, a.H, wx - 1, ya, true), jra = bitw(J, WW, a.H, wx + 2, ya, true);
+  const unsigned jlb = bitw(J, WW, a.H, wx - 1, yb, true), jrb = bitw(J, WW, a.H, wx + 2, yb, true);
+  const unsigned ila = bitw(I, WW, a.H, wx - 1, ya, false), ira = bitw(I, WW, a.H, wx + 2, ya, false);
+  const unsigned ilb = bitw(I, WW, a.H, wx - 1, yb, false), irb = bitw(I, WW, a.H, wx + 2, yb, false);
+  const unsigned jhl = bitw(J, WW, a.H, wx - 1, hy, true), jhr = bitw(J, WW, a.H, wx + 2, hy, true);
+  const unsigned ihl = bitw(I, WW, a.H, wx - 1, hy, false), ihr = bitw(I, WW, a.H, wx + 2, hy, false);
+  h.row0 = bitw(J, WW, a.H, wx, hy, true);
+  h.row1 = bitw(J, WW, a.H, wx + 1, hy, true);
+  h.rowI0 = bitw(I, WW, a.H, wx, hy, false);
+  h.rowI1 = bitw(I, WW, a.H, wx + 1, hy, false);
+  h.la = jla >> 31; h.ra = jra & 1u; h.lIa = ila >> 31; h.rIa = ira & 1u;
+  h.lb = jlb >> 31; h.rb = jrb & 1u; h.lIb = ilb >> 31; h.rIb = irb & 1u;
+  h.cl = jhl >> 31; h.cr = jhr & 1u; h.clI = ihl >> 31; h.crI = ihr & 1u;
 }
 
 // 3x3 (8-conn) / cross (4-conn) dilation of a 64-bit row (w0, w1) with the
@@ -1360,13 +1266,10 @@ __global__ void __launch_bounds__(kCtaThreads)
     const int x0 = tx * TSB, y0 = ty * TSB;
     long long c_load = l0 ? clock64() : 0;
     if (l0) ph[0] += c_load - c_pop;
-    const uint8_t *Jb = (const uint8_t *)a.J, *Ib = (const uint8_t *)a.I;
-    unsigned a0, a1, b0, b1, ma0, ma1, mb0, mb1;
+    unsigned jt[4], mt[4];
     BinHalo h;
-    bin_tile_load(a, x0, y0, lane, a0, a1, b0, b1, ma0, ma1, mb0, mb1,
-                  [&]() { bin_load_halo(a, x0, y0, lane, h); });
-    (void)Jb;
-    (void)Ib;
+    bin_load(a, x0, y0, lane, true, jt, mt, h);
+    unsigned a0 = jt[0], a1 = jt[1], b0 = jt[2], b1 = jt[3];
     unsigned oa0 = a0, oa1 = a1, ob0 = b0, ob1 = b1;  // as last published
     if (l0) ph[1] += clock64() - c_load;
     bool rerun = false;
@@ -1375,14 +1278,22 @@ __global__ void __launch_bounds__(kCtaThreads)
       n_reruns += l0 && rerun;
       long long c_fix = l0 ? clock64() : 0;
       bool changed = false;
-      const int steps = bin_fixpoint<CONN>(a0, a1, b0, b1, ma0, ma1, mb0, mb1, h, lane, changed);
+      const int steps = bin_fixpoint<CONN>(a0, a1, b0, b1, mt[0], mt[1], mt[2], mt[3], h, lane, changed);
       if (l0) n_steps += steps;
       changed = __any_sync(FULL, changed);
       long long c_st = l0 ? clock64() : 0;
       if (l0) ph[2] += c_st - c_fix;
       if (changed) {
-        if (a0 != oa0 || a1 != oa1) bin_store64(a, x0, y0 + lane, a0, a1);
-        if (b0 != ob0 || b1 != ob1) bin_store64(a, x0, y0 + lane + 32, b0, b1);
+        uint32_t *Jw = (uint32_t *)a.J;
+        const int wx = x0 >> 5, ya = y0 + lane, yb = ya + 32;
+        if (ya < a.H) {
+          if (a0 != oa0) Jw[(size_t)ya * a.WW + wx] = a0;
+          if (a1 != oa1) Jw[(size_t)ya * a.WW + wx + 1] = a1;
+        }
+        if (yb < a.H) {
+          if (b0 != ob0) Jw[(size_t)yb * a.WW + wx] = b0;
+          if (b1 != ob1) Jw[(size_t)yb * a.WW + wx + 1] = b1;
+        }
         if (a.dirty && l0) a.dirty[ty] = 1;
         // newly set border cells; a neighbour needs a re-run where such a
         // cell (dilated along the border for 8-conn) meets a halo cell with
@@ -1466,7 +1377,7 @@ __global__ void __launch_bounds__(kCtaThreads)
       done = __shfl_sync(FULL, done, 0);
       if (l0) ph[5] += clock64() - c_st;
       if (done) break;
-      bin_load_halo(a, x0, y0, lane, h);
+      bin_load(a, x0, y0, lane, false, jt, mt, h);  // the tile is ours: halo only
       rerun = true;
     }
   }
@@ -1476,6 +1387,84 @@ __global__ void __launch_bounds__(kCtaThreads)
     atomicAdd(&counters[CNT_STEPS], n_steps);
     for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
   }
+}
+
+// 0 / 255 bytes <-> bit planes: one thread per 32-pixel word (32-bit index
+// math; rows 16-byte aligned -> two 16-byte loads / stores per word)
+__device__ __forceinline__ unsigned pack_bits(const unsigned *w) {
+  unsigned b = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const unsigned t = (w[k] | (w[k] << 1) | (w[k] << 2) | (w[k] << 3) | (w[k] << 4) |
+                        (w[k] << 5) | (w[k] << 6) | (w[k] << 7)) & 0x80808080u;  // byte != 0
+    b |= ((t * 0x00204081u) >> 28) << (4 * k);
+  }
+  return b;
+}
+
+__global__ void bin_pack_kernel(const uint8_t *__restrict__ src, int W, int H,
+                                uint32_t *__restrict__ bits, int vec) {
+  const unsigned WW = (unsigned)(W + 31) >> 5;
+  const unsigned nw = WW * (unsigned)H;
+  for (unsigned wi = blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += gridDim.x * blockDim.x) {
+    const unsigned y = wi / WW, x0 = (wi - y * WW) * 32;
+    const uint8_t *p = src + (size_t)y * W + x0;
+    unsigned w[8];
+    if (vec && x0 + 32 <= (unsigned)W) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4 *>(p)), b = __ldg(reinterpret_cast<const uint4 *>(p) + 1);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        unsigned v = 0;
+        for (int e = 0; e < 4; e++)
+          if (x0 + 4 * k + e < (unsigned)W) v |= (unsigned)p[4 * k + e] << (8 * e);
+        w[k] = v;
+      }
+    }
+    bits[wi] = pack_bits(w);
+  }
+}
+
+__global__ void bin_unpack_kernel(const uint32_t *__restrict__ bits, int W, int H,
+                                  uint8_t *__restrict__ dst, int vec) {
+  const unsigned WW = (unsigned)(W + 31) >> 5;
+  const unsigned nw = WW * (unsigned)H;
+  for (unsigned wi = blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += gridDim.x * blockDim.x) {
+    const unsigned y = wi / WW, x0 = (wi - y * WW) * 32;
+    const unsigned b = bits[wi];
+    unsigned w[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) w[k] = ((((b >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu;
+    uint8_t *p = dst + (size_t)y * W + x0;
+    if (vec && x0 + 32 <= (unsigned)W) {
+      reinterpret_cast<uint4 *>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      reinterpret_cast<uint4 *>(p)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+      for (unsigned x = 0; x < 32 && x0 + x < (unsigned)W; x++) p[x] = (uint8_t)(w[x >> 2] >> (8 * (x & 3)));
+    }
+  }
+}
+
+size_t bin_plane_words(int64_t W, int64_t H) { return (size_t)((W + 31) / 32) * (size_t)H; }
+
+int bin_pack(const void *src, int W, int H, uint32_t *bits, cudaStream_t st) {
+  size_t threads = bin_plane_words(W, H);
+  size_t blocks = (threads + 255) / 256, cap = (size_t)device_sm_count() * 16;
+  const int vec = W % 16 == 0 && (uintptr_t)src % 16 == 0;
+  bin_pack_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, st>>>((const uint8_t *)src, W, H,
+                                                                           bits, vec);
+  IWPP_CUDA_TRY(cudaGetLastError());
+  return IWPP_OK;
+}
+int bin_unpack(const uint32_t *bits, int W, int H, void *dst, cudaStream_t st) {
+  size_t threads = bin_plane_words(W, H);
+  size_t blocks = (threads + 255) / 256, cap = (size_t)device_sm_count() * 16;
+  const int vec = W % 16 == 0 && (uintptr_t)dst % 16 == 0;
+  bin_unpack_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, st>>>(bits, W, H, (uint8_t *)dst,
+                                                                             vec);
+  IWPP_CUDA_TRY(cudaGetLastError());
+  return IWPP_OK;
 }
 
 // Initial GBQ: every tile, ordered by 2x2 colour class (then raster) so the
@@ -1667,7 +1656,7 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   unsigned qlimit = (o.qcap > 0 && o.qcap < RQ) ? (unsigned)o.qcap : (unsigned)RQ;
   unsigned hth = o.halo_thresh >= 0 ? (unsigned)o.halo_thresh : kHaloSweepThreshold;
   bool vec = ((size_t)W * sizeof(T)) % 16 == 0 && (uintptr_t)J % 16 == 0 && (uintptr_t)I % 16 == 0;
-  EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, o.dirty, q};
+  EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, o.dirty, (W + 31) / 32, q};
   if (o.ev_begin) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_begin, st));
   if (use_bin_engine(binary, o)) {
     static int bin_blocks = 0;
@@ -1675,6 +1664,11 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
       int per_sm = 0;
       IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_engine_bin_kernel<CONN>,
                                                                   kCtaThreads, 0));
+      // more resident warps than this only adds idle pollers on the tile
+      // ring (binary fills are narrow fronts): measured best at 4 CTAs/SM
+      int cap = kBinCtasPerSm;
+      if (const char *e = getenv("IWPP_BIN_CTAS")) cap = atoi(e);
+      if (per_sm > cap) per_sm = cap;
       bin_blocks = device_sm_count() * (per_sm < 1 ? 1 : per_sm);
     }
     int bb = bin_blocks;

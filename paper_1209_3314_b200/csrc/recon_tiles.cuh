@@ -70,6 +70,10 @@ int run_tile_engine(void *J, const void *I, int W, int H, int dtype, int conn, T
 // side of the square tiles the engine run_tile_engine picks for (dtype, o)
 // works on: sel_lo / sel_hi and the dirty flags count rows of these tiles
 int tile_side(int dtype, const EngineOpts &o);
+// binary kind: J / I as bit planes (ceil(W/32) words per row) for the engine
+size_t bin_plane_words(int64_t W, int64_t H);
+int bin_pack(const void *src, int W, int H, uint32_t *bits, cudaStream_t st);
+int bin_unpack(const uint32_t *bits, int W, int H, void *dst, cudaStream_t st);
 
 inline unsigned num_tiles(int64_t W, int64_t H) {
   return (unsigned)(((W + TS - 1) / TS) * ((H + TS - 1) / TS));
