@@ -176,13 +176,14 @@ int iwpp_edt_propagate(int64_t *vr, int64_t W, int64_t H, int conn,
                        size_t workspace_bytes, int64_t max_rounds,
                        iwpp_stats *stats, void *stream);
 /* Engine selection for tests/diagnostics (process-wide, not thread-safe):
- * 0 = auto (64-bit keys: the per-round frontier-queue engine below 2^25
- * cells, the temporally blocked engine above; range-checked with a CAS
- * re-run when W, H exceed the 32-bit d^2 range), 1 = force the
- * 32-bit-source CAS engine, 2 = force range-checked keys, 3 = force the
+ * 0 = auto (64-bit keys: the raster-frontier engine below 2^25 cells, the
+ * temporally blocked engine above; range-checked with a CAS re-run when
+ * W, H exceed the 32-bit d^2 range), 1 = force the 32-bit-source CAS
+ * engine, 2 = force range-checked keys, 3 = force the per-round
  * frontier-queue engine, 4 = force the blocked engine; 5 / 6 = the queue
  * engine with the paper's prefix-sum / naive global queue instead of the
- * block queue (PAPER.md:1563-1595 queue study).  Results never depend on it. */
+ * block queue (PAPER.md:1563-1595 queue study), 7 = force the raster engine.
+ * Results never depend on it. */
 int iwpp_edt_set_engine(int mode);
 /* finalize_distance_map (edt.py:272-281): dist = f32(sqrt(f64(d2))).
  * Returns IWPP_E_NO_BACKGROUND if any vr == -1.  d2 may be NULL. */

@@ -656,7 +656,7 @@ static int edt_solve(edt::EdtState &s, void *workspace, int64_t W, int64_t H, in
 extern "C" {
 
 int iwpp_edt_set_engine(int mode) {
-  if (mode < edt::ENGINE_AUTO || mode > edt::ENGINE_QUEUE_NAIVE)
+  if (mode < edt::ENGINE_AUTO || mode > edt::ENGINE_RASTER)
     return set_error(IWPP_E_CONTRACT, "unknown EDT engine mode %d", mode);
   edt::g_engine_override = mode;
   return IWPP_OK;

@@ -447,6 +447,220 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
   }
 }
 
+// ---- raster-frontier key engine ---------------------------------------------
+// rounds whose frontier is smaller than this run as queue rounds (below)
+#ifndef IWPP_RASTER_MIN
+#define IWPP_RASTER_MIN 262144
+#endif
+constexpr unsigned kRasterMinFrontier = IWPP_RASTER_MIN;
+//
+// The same two-phase rounds as edt_rounds_key_kernel, with no returned
+// atomic on a round's critical path and the frontier in raster order:
+//   phase 1: every frontier cell resyncs its building key (RED.MIN) and
+//            offers make_key(q, src) to each neighbour whose round-start key
+//            it beats: RED.MIN on q's building key and RED.OR of q's bit in
+//            the next-frontier bitmap.  q changed iff some offer beat its
+//            round-start key, so the bitmap is exactly the next frontier --
+//            no dedupe, no per-item reservation.  Neighbour keys are read
+//            through L1 (the round-start buffer is read-only within the
+//            round; every barrier's acquire invalidates L1).
+//   phase 2: the bitmap is compacted into the next frontier list: each CTA
+//            scans a contiguous run of words (block prefix sum, one global
+//            atomic per CTA) and clears them.  The list is raster-ordered
+//            within each run, so neighbouring lanes offer to neighbouring
+//            cells in the next round.
+// Two grid barriers per round.
+template <int CONN, bool CHECK>
+__global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W, int H, EdtState s,
+                                                                          long long max_rounds) {
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  __shared__ unsigned wsum[kRoundThreads / 32];
+  __shared__ unsigned blk_base, bq_n;
+  __shared__ uint32_t bq[kEdtBq];
+  const int WW = (W + 31) >> 5;
+  const unsigned nwords = (unsigned)WW * (unsigned)H;
+  uint32_t *Fb = s.fbits[0];
+  unsigned long long visits = 0;
+  unsigned long long *K = s.keys;
+  // this CTA's run of bitmap words (phase 2)
+  const unsigned per = (nwords + gridDim.x - 1) / gridDim.x;
+  const unsigned w_lo = blockIdx.x * per, w_hi = min(nwords, w_lo + per);
+  int r = 0;
+  for (;; r++) {
+    const unsigned n = ld_acquire(&s.cnt[r % 3]);
+    if (n == 0) break;
+    if (max_rounds >= 0 && r >= max_rounds) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) s.counters[EC_LIMIT] = 1;
+      break;
+    }
+    const int kr = r & 1, kw = kr ^ 1;
+    const uint32_t *cur = s.F[r & 1];
+    uint32_t *nxt = s.F[(r + 1) & 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      s.cnt[(r + 2) % 3] = 0;
+      visits += n;
+    }
+    if (n < kRasterMinFrontier) {
+      // a small frontier: the queue round (returned atomics, transition-rule
+      // pushes into a shared-memory block queue) -- one barrier
+      if (threadIdx.x == 0) bq_n = 0;
+      __syncthreads();
+      unsigned *ncnt = &s.cnt[(r + 1) % 3];
+      const unsigned stride = gridDim.x * blockDim.x;
+      for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+        const unsigned i = base + lane;
+        unsigned mask = 0;
+        int px = 0, py = 0;
+        if (i < n) {
+          const uint32_t pyx = __ldcg(cur + i);
+          py = (int)(pyx >> 16);
+          px = (int)(pyx & 0xffffu);
+          const size_t p = (size_t)py * W + px;
+          const unsigned long long kp = __ldcg(K + 2 * p + kr);
+          atomicMin(K + 2 * p + kw, kp);
+          if (kp != KINF) {
+            const uint32_t src = (uint32_t)kp;
+            unsigned long long rq[Nbr<CONN>::N], nk[Nbr<CONN>::N];
+            unsigned cand = 0;
+#pragma unroll
+            for (int k = 0; k < Nbr<CONN>::N; k++) {
+              const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+              const bool in = qx >= 0 && qx < W && qy >= 0 && qy < H;
+              rq[k] = in ? __ldcg(K + 2 * ((size_t)qy * W + qx) + kr) : 0ull;
+            }
+#pragma unroll
+            for (int k = 0; k < Nbr<CONN>::N; k++) {
+              const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+              bool ok = true;
+              if (CHECK) {
+                nk[k] = make_key_checked(qx, qy, src, ok);
+                if (!ok) s.counters[EC_RANGE] = 1;
+              } else {
+                nk[k] = make_key(qx, qy, src);
+              }
+              if (ok && nk[k] < rq[k]) cand |= 1u << k;
+            }
+#pragma unroll
+            for (int k = 0; k < Nbr<CONN>::N; k++) {
+              const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+              const unsigned on = (cand >> k) & 1u;
+              const unsigned long long old =
+                  gmem_atomic_min_if(K + 2 * ((size_t)qy * W + qx) + kw, nk[k], on);
+              if (on && old >= rq[k]) mask |= 1u << k;
+            }
+          }
+        }
+        const unsigned c = __popc(mask);
+        unsigned pos = warp_reserve(&bq_n, c, FULL);
+        while (mask) {
+          const int k = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+          const uint32_t item = ((uint32_t)qy << 16) | (uint32_t)qx;
+          if (pos < kEdtBq)
+            bq[pos] = item;
+          else
+            nxt[atomicAdd(ncnt, 1u)] = item;
+          pos++;
+        }
+      }
+      __syncthreads();
+      const unsigned m = min(bq_n, (unsigned)kEdtBq);
+      if (threadIdx.x == 0 && m) blk_base = atomicAdd(ncnt, m);
+      __syncthreads();
+      for (unsigned i = threadIdx.x; i < m; i += blockDim.x) nxt[blk_base + i] = bq[i];
+      grid_barrier(&s.bar[0], &s.bar[1], gridDim.x);
+      continue;
+    }
+    // phase 1: offers
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+      const unsigned i = base + lane;
+      int px = 0, py = 0;
+      unsigned long long kp = KINF;
+      if (i < n) {
+        const uint32_t pyx = __ldcg(cur + i);
+        py = (int)(pyx >> 16);
+        px = (int)(pyx & 0xffffu);
+        const size_t p = (size_t)py * W + px;
+        kp = K[2 * p + kr];
+        atomicMin(K + 2 * p + kw, kp);  // the building key lags on the frontier (RED)
+      }
+      const uint32_t src = (uint32_t)kp;
+      unsigned long long rq[Nbr<CONN>::N];
+#pragma unroll
+      for (int k = 0; k < Nbr<CONN>::N; k++) {
+        const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+        const bool in = kp != KINF && qx >= 0 && qx < W && qy >= 0 && qy < H;
+        rq[k] = in ? K[2 * ((size_t)qy * W + qx) + kr] : 0ull;
+      }
+#pragma unroll
+      for (int k = 0; k < Nbr<CONN>::N; k++) {
+        const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+        unsigned long long nk;
+        bool ok = true;
+        if (CHECK) {
+          nk = make_key_checked(qx, qy, src, ok);
+          if (kp != KINF && !ok) s.counters[EC_RANGE] = 1;
+        } else {
+          nk = make_key(qx, qy, src);
+        }
+        const bool push = ok && nk < rq[k];  // rq = 0 off the image / for inactive lanes
+        if (push) atomicMin(K + 2 * ((size_t)qy * W + qx) + kw, nk);
+        const unsigned waddr = push ? (unsigned)qy * (unsigned)WW + ((unsigned)qx >> 5) : 0xffffffffu;
+        const unsigned grp = __match_any_sync(FULL, waddr);
+        const unsigned orb = __reduce_or_sync(grp, push ? (1u << (qx & 31)) : 0u);
+        if (push && lane == (unsigned)(__ffs(grp) - 1)) atomicOr(Fb + waddr, orb);
+      }
+    }
+    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x);
+    // phase 2: compact this CTA's words of the bitmap into the next list,
+    // one 512-word chunk at a time (block prefix sum, one global atomic per
+    // non-empty chunk), clearing them
+    for (unsigned wb = w_lo; wb < w_hi; wb += blockDim.x) {
+      const unsigned wi = wb + threadIdx.x;
+      unsigned w = wi < w_hi ? __ldcg(Fb + wi) : 0u;
+      const unsigned c = __popc(w);
+      unsigned incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= (unsigned)o) incl += v;
+      }
+      if (lane == 31) wsum[warp] = incl;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned t = 0;
+        for (int k = 0; k < kRoundThreads / 32; k++) {
+          const unsigned v = wsum[k];
+          wsum[k] = t;  // exclusive prefix over warps
+          t += v;
+        }
+        blk_base = t ? atomicAdd(&s.cnt[(r + 1) % 3], t) : 0u;
+      }
+      __syncthreads();
+      unsigned o = blk_base + wsum[warp] + incl - c;
+      if (w) {
+        Fb[wi] = 0u;
+        const unsigned y = wi / (unsigned)WW, x0 = (wi - y * (unsigned)WW) * 32;
+        while (w) {
+          const int bb = __ffs(w) - 1;
+          w &= w - 1;
+          nxt[o++] = (y << 16) | (x0 + bb);
+        }
+      }
+      __syncthreads();
+    }
+    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s.counters[EC_ROUNDS] = (unsigned long long)r;
+    s.counters[EC_VISITS] = visits;
+    s.counters[EC_FINAL] = (unsigned long long)(r & 1);
+  }
+}
+
 __global__ void edt_finalize_key_kernel(EdtState s, int W, int H, int64_t *vr, float *dist,
                                         int64_t *d2) {
   const int fb = (int)s.counters[EC_FINAL];
@@ -506,9 +720,14 @@ static EdtState carve_any(Carver &c, int64_t W, int64_t H, bool cas) {
   // block engine: two planes over the same 2n keys, frontier bitmaps, regions
   const bool force_queue = g_engine_override == ENGINE_QUEUE ||
                            g_engine_override == ENGINE_QUEUE_PF ||
-                           g_engine_override == ENGINE_QUEUE_NAIVE;
+                           g_engine_override == ENGINE_QUEUE_NAIVE ||
+                           g_engine_override == ENGINE_RASTER;
   s.block = s.keymode && !force_queue &&
             (g_engine_override == ENGINE_BLOCK || (int64_t)n >= kBlockMinCells);
+  // below kBlockMinCells the default is the raster-frontier engine (with
+  // queue rounds for small frontiers); 3 / 5 / 6 force the plain queue engine
+  s.raster = s.keymode && !s.block && g_engine_override != ENGINE_QUEUE &&
+             g_engine_override != ENGINE_QUEUE_PF && g_engine_override != ENGINE_QUEUE_NAIVE;
   s.plane[0] = keys;
   s.plane[1] = keys + n;
   const size_t words = (size_t)((W + 31) / 32) * H;
@@ -597,6 +816,28 @@ int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_round
                   cudaStream_t st) {
   const int qm = g_engine_override == ENGINE_QUEUE_PF ? QM_PF
                  : g_engine_override == ENGINE_QUEUE_NAIVE ? QM_NAIVE : QM_BQ;
+  if (s.raster) {  // the raster-frontier engine
+    void *rk = s.keycheck ? (conn == 8 ? (void *)edt_rounds_raster_kernel<8, true>
+                                       : (void *)edt_rounds_raster_kernel<4, true>)
+                          : (conn == 8 ? (void *)edt_rounds_raster_kernel<8, false>
+                                       : (void *)edt_rounds_raster_kernel<4, false>);
+    static int rblocks[4] = {0, 0, 0, 0};
+    int &rb = rblocks[(conn == 8) + 2 * s.keycheck];
+    if (rb == 0) {
+      int per_sm = 0;
+      IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rk, kRoundThreads, 0));
+      if (per_sm < 1) per_sm = 1;
+      if (per_sm > kRoundBlocksPerSm) per_sm = kRoundBlocksPerSm;
+      rb = device_sm_count() * per_sm;
+    }
+    // the next-frontier bitmap starts empty
+    IWPP_CUDA_TRY(cudaMemsetAsync(s.fbits[0], 0, sizeof(uint32_t) * ((W + 31) / 32) * (size_t)H, st));
+    int w = W, h = H;
+    EdtState ss = s;
+    void *args[] = {&w, &h, &ss, &max_rounds};
+    IWPP_CUDA_TRY(cudaLaunchCooperativeKernel(rk, dim3(rb), dim3(kRoundThreads), args, 0, st));
+    return IWPP_OK;
+  }
   void *kern = s.keymode
                    ? (s.keycheck ? (conn == 8 ? (void *)edt_rounds_key_kernel<8, true>
                                               : (void *)edt_rounds_key_kernel<4, true>)

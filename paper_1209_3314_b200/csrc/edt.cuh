@@ -26,6 +26,7 @@ struct EdtState {
   unsigned long long *counters;
   // block engine (edt_block.cu)
   int block;                 // keymode runs on the temporally blocked engine
+  int raster;                // keymode runs on the raster-frontier engine
   unsigned long long *plane[2];  // block engine: two key planes (no interleave)
   uint32_t *fbits[2];        // frontier bitmaps (row-major, ceil(W/32) words per row)
   unsigned *rplane;          // per region: (pass << 1) | plane holding its current keys
@@ -50,7 +51,8 @@ inline bool cas_supported(int64_t W, int64_t H) {
 enum {
   ENGINE_AUTO = 0, ENGINE_CAS = 1, ENGINE_KEYCHECK = 2, ENGINE_QUEUE = 3, ENGINE_BLOCK = 4,
   ENGINE_QUEUE_PF = 5,    // queue engine, next frontier by warp reservations in global memory
-  ENGINE_QUEUE_NAIVE = 6  // queue engine, one global atomic per pushed item
+  ENGINE_QUEUE_NAIVE = 6, // queue engine, one global atomic per pushed item
+  ENGINE_RASTER = 7       // raster-frontier engine (bitmap + compaction, no returned atomics)
 };
 // auto: the temporally blocked engine from this many cells up (measured on
 // B200: it wins on whole-slide images, the frontier queue on 4K tiles)
@@ -83,19 +85,21 @@ __device__ __forceinline__ unsigned long long make_key_checked(int qx, int qy, u
 
 // Software grid barrier for the persistent cooperative kernels.
 __device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen, unsigned nblocks) {
+  // Arrival is an acq_rel RMW (publishes this block's writes, and the last
+  // arriver acquires everyone's); the release is a release add on the
+  // generation, which the waiters acquire.  No sequentially consistent
+  // fences (MEMBAR.SC) on the round's critical path.
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned g = ld_acquire(gen);
-    __threadfence();
-    unsigned arrived = atomicAdd(count, 1u);
+    const unsigned g = ld_acquire(gen);
+    unsigned arrived;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(count) : "memory");
     if (arrived == nblocks - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
-      atomicAdd(gen, 1u);
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(count) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gen) : "memory");
     } else {
       while (ld_acquire(gen) == g) __nanosleep(16);
     }
-    __threadfence();
   }
   __syncthreads();
 }

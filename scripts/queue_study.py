@@ -49,7 +49,8 @@ print(f"{'mask':8s} {'engine':32s} {'ms':>8s} {'rounds':>7s} {'visits':>10s} {'u
 masks = {"nuclei": oracle.gen_nuclei_mask(4096, 4096, 30.0, 7),
          "blob": oracle.gen_synthetic_mask(4096, 4096, 50, 7)}
 engines = [(3, "frontier queue, block queue"), (5, "frontier queue, prefix-sum (PF)"),
-           (6, "frontier queue, naive atomics"), (4, "temporally blocked (8 rounds/sync)")]
+           (6, "frontier queue, naive atomics"), (7, "raster frontier (default)"),
+           (4, "temporally blocked (8 rounds/sync)")]
 for name, m in masks.items():
     img = gw.Image2D(4096, 4096, "binary", torch.from_numpy(m).cuda())
     ref_vr = None

@@ -189,7 +189,7 @@ def engine_mode(gw):
     set_mode(0)
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("conn", [4, 8])
 def test_engine_variants_vs_oracle(gw, engine_mode, mode, conn):
     engine_mode(mode)
