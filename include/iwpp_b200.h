@@ -176,9 +176,8 @@ int iwpp_edt_propagate(int64_t *vr, int64_t W, int64_t H, int conn,
                        size_t workspace_bytes, int64_t max_rounds,
                        iwpp_stats *stats, void *stream);
 /* Engine selection for tests/diagnostics (process-wide, not thread-safe):
- * 0 = auto (64-bit keys: the raster-frontier engine below 2^25 cells, the
- * temporally blocked engine above; range-checked with a CAS re-run when
- * W, H exceed the 32-bit d^2 range), 1 = force the 32-bit-source CAS
+ * 0 = auto (64-bit keys on the raster-frontier engine; range-checked with a
+ * CAS re-run when W, H exceed the 32-bit d^2 range), 1 = force the 32-bit-source CAS
  * engine, 2 = force range-checked keys, 3 = force the per-round
  * frontier-queue engine, 4 = force the blocked engine; 5 / 6 = the queue
  * engine with the paper's prefix-sum / naive global queue instead of the

@@ -722,10 +722,11 @@ static EdtState carve_any(Carver &c, int64_t W, int64_t H, bool cas) {
                            g_engine_override == ENGINE_QUEUE_PF ||
                            g_engine_override == ENGINE_QUEUE_NAIVE ||
                            g_engine_override == ENGINE_RASTER;
-  s.block = s.keymode && !force_queue &&
-            (g_engine_override == ENGINE_BLOCK || (int64_t)n >= kBlockMinCells);
-  // below kBlockMinCells the default is the raster-frontier engine (with
-  // queue rounds for small frontiers); 3 / 5 / 6 force the plain queue engine
+  // the default is the raster-frontier engine (queue rounds for small
+  // frontiers) at every size -- on B200 it beat the blocked engine on the
+  // 64K^2 whole slide too (287 vs 319 ms); 4 forces the blocked engine
+  s.block = s.keymode && !force_queue && g_engine_override == ENGINE_BLOCK;
+  // 3 / 5 / 6 force the plain queue engine
   s.raster = s.keymode && !s.block && g_engine_override != ENGINE_QUEUE &&
              g_engine_override != ENGINE_QUEUE_PF && g_engine_override != ENGINE_QUEUE_NAIVE;
   s.plane[0] = keys;

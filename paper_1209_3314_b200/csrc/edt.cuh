@@ -54,9 +54,7 @@ enum {
   ENGINE_QUEUE_NAIVE = 6, // queue engine, one global atomic per pushed item
   ENGINE_RASTER = 7       // raster-frontier engine (bitmap + compaction, no returned atomics)
 };
-// auto: the temporally blocked engine from this many cells up (measured on
-// B200: it wins on whole-slide images, the frontier queue on 4K tiles)
-constexpr int64_t kBlockMinCells = (int64_t)1 << 25;
+
 extern int g_engine_override;
 // The key engine needs every squared distance to fit 32 bits.
 inline bool key_mode_ok(int64_t W, int64_t H) {
