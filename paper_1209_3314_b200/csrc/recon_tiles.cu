@@ -50,7 +50,11 @@
 // is bit-exact with recon_fh.
 
 #include <climits>
+#include <cstdio>
+#include <cstring>
 #include <cstdlib>
+
+#include <cuda.h>  // CUtensorMap (the encoder is fetched from the driver at run time)
 
 #include "iwpp_common.cuh"
 #include "recon_tiles.cuh"
@@ -956,10 +960,94 @@ __device__ __forceinline__ int reg_fixpoint(unsigned *j, const unsigned *m, cons
   return steps;
 }
 
+// --- TMA staging of a tile (register engine, u8) --------------------------------
+//
+// One elected lane loads the tile plus its one-pixel halo of J and of I as
+// two 64 x 34-byte boxes with cp.async.bulk.tensor (out-of-image cells come
+// back as 0, the u8 sentinel), completion on a per-warp mbarrier; the lanes
+// then read their rows from shared memory.  A box's start column must be
+// 16-byte aligned, so box column c is image column x0 - 16 + c (the tile at
+// c = 16..47, the halo at 15 and 48); row r is image row y0 - 1 + r.
+constexpr int kBoxW = 64, kBoxH = TS + 2, kBoxBytes = kBoxW * kBoxH, kBoxX = 16;
+
+struct alignas(128) TmaWarpSmem {
+  uint8_t J[kBoxBytes];
+  uint8_t pad0[(128 - kBoxBytes % 128) % 128];
+  uint8_t I[kBoxBytes];
+  uint8_t pad1[(128 - kBoxBytes % 128) % 128];
+  unsigned long long bar;
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_box(const CUtensorMap *map, void *dst, unsigned long long *bar,
+                                             int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// lane 0: issue the J (and, for a fresh tile, I) boxes of tile (x0, y0);
+// every lane then waits for them.  `phase` toggles per use.
+__device__ __forceinline__ void tma_stage(const CUtensorMap *mJ, const CUtensorMap *mI, TmaWarpSmem &t,
+                                          int x0, int y0, bool withI, unsigned &phase, int lane) {
+  __syncwarp();  // the previous boxes have been read (WAR on the staging buffers)
+  if (lane == 0) {
+    // other SMs' stores, acquired through the tile state, must be visible
+    // to the async proxy that performs the box reads
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mbar_expect_tx(&t.bar, withI ? 2u * kBoxBytes : (unsigned)kBoxBytes);
+    tma_load_box(mJ, t.J, &t.bar, x0 - kBoxX, y0 - 1);
+    if (withI) tma_load_box(mI, t.I, &t.bar, x0 - kBoxX, y0 - 1);
+  }
+  mbar_wait(&t.bar, phase);
+  phase ^= 1u;
+}
+
+// rows from the staged boxes: my row's words + halo bytes; lanes 0 / 31 also
+// take the halo row above / below and its corners
+__device__ __forceinline__ void tma_row(const uint8_t *box, int r, unsigned *w) {
+  const uint4 *p = reinterpret_cast<const uint4 *>(box + r * kBoxW + kBoxX);
+  const uint4 a = p[0], b = p[1];
+  w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+  w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+}
+
 template <int CONN>
 __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
-    tile_engine_reg_kernel(EngineArgs a, unsigned long long *counters) {
+    tile_engine_reg_kernel(EngineArgs a, unsigned long long *counters, const CUtensorMap *tmaps,
+                           int use_tma) {
   __shared__ RegWarpSmem wsm[kWarpsPerCta];
+  __shared__ TmaWarpSmem tsm[kWarpsPerCta];
+  TmaWarpSmem &ts = tsm[threadIdx.x >> 5];
+  const CUtensorMap *tmJ = tmaps, *tmI = tmaps + 1;  // in global memory (workspace)
+  unsigned tphase = 0;
+  if (use_tma && (threadIdx.x & 31) == 0) {
+    mbar_init(&ts.bar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // the descriptors were written by a copy before this launch
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmJ) : "memory");
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmI) : "memory");
+  }
+  __syncwarp();
   const int lane = threadIdx.x & 31;
   const bool l0 = lane == 0;
   const bool edge = lane == 0 || lane == 31;
@@ -988,18 +1076,43 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
 
     unsigned j[8], m[8];
     RegHalo h;
-    reg_load_row((const uint8_t *)a.J, a.W, x0, y0 + lane, a.H, a.vec, true, j);
-    reg_load_row((const uint8_t *)a.I, a.W, x0, y0 + lane, a.H, a.vec, false, m);
-    reg_load_halo(a, x0, y0, lane, h);
-    // the border as last published (lanes 0 / 31: whole rows; every lane: its ends)
-    if (edge) {
-      const int hy = lane == 0 ? y0 - 1 : y0 + TS;
-      unsigned hI[8];
-      reg_load_row((const uint8_t *)a.I, a.W, x0, hy, a.H, a.vec, false, hI);
+    if (use_tma) {
+      tma_stage(tmJ, tmI, ts, x0, y0, true, tphase, lane);
+      const int hr = lane == 0 ? 0 : TS + 1;  // halo row (lanes 0 / 31)
+      tma_row(ts.J, lane + 1, j);
+      tma_row(ts.I, lane + 1, m);
+      tma_row(ts.J, hr, h.row);
+      h.l = ts.J[(lane + 1) * kBoxW + kBoxX - 1];
+      h.r = ts.J[(lane + 1) * kBoxW + kBoxX + TS];
+      h.lI = ts.I[(lane + 1) * kBoxW + kBoxX - 1];
+      h.rI = ts.I[(lane + 1) * kBoxW + kBoxX + TS];
+      h.cl = ts.J[hr * kBoxW + kBoxX - 1];
+      h.cr = ts.J[hr * kBoxW + kBoxX + TS];
+      h.clI = ts.I[hr * kBoxW + kBoxX - 1];
+      h.crI = ts.I[hr * kBoxW + kBoxX + TS];
+      if (edge) {
+        unsigned hI[8];
+        tma_row(ts.I, hr, hI);
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        ws.rowI[sel][k] = hI[k];
-        ws.ob[sel][k] = j[k];
+        for (int k = 0; k < 8; k++) {
+          ws.rowI[sel][k] = hI[k];
+          ws.ob[sel][k] = j[k];
+        }
+      }
+    } else {
+      reg_load_row((const uint8_t *)a.J, a.W, x0, y0 + lane, a.H, a.vec, true, j);
+      reg_load_row((const uint8_t *)a.I, a.W, x0, y0 + lane, a.H, a.vec, false, m);
+      reg_load_halo(a, x0, y0, lane, h);
+      // the border as last published (lanes 0 / 31: whole rows; every lane: its ends)
+      if (edge) {
+        const int hy = lane == 0 ? y0 - 1 : y0 + TS;
+        unsigned hI[8];
+        reg_load_row((const uint8_t *)a.I, a.W, x0, hy, a.H, a.vec, false, hI);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          ws.rowI[sel][k] = hI[k];
+          ws.ob[sel][k] = j[k];
+        }
       }
     }
     unsigned obl = j[0] & 0xffu, obr = j[7] >> 24;
@@ -1076,7 +1189,10 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
           for (int k = 0; k < 8; k++) ws.ob[sel][k] = j[k];
         obl = jl;
         obr = jr;
-        fence_acq_rel();  // publish the tile before any neighbour is (re)queued
+        // publish the tile before any neighbour is (re)queued.  With no
+        // neighbour to activate no fence is needed: a neighbour that this
+        // border cannot raise never needs to see it (need_h was false)
+        if (dirs) fence_acq_rel();
         __syncwarp();
         bool own = false;
         unsigned ntile = 0;
@@ -1108,7 +1224,17 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
       done = __shfl_sync(FULL, done, 0);
       if (l0) ph[5] += clock64() - c_st;
       if (done) break;
-      reg_load_halo(a, x0, y0, lane, h);  // the interior is ours and current
+      if (use_tma) {  // the interior is ours and current: refresh the J halo only
+        tma_stage(tmJ, tmI, ts, x0, y0, false, tphase, lane);
+        const int hr = lane == 0 ? 0 : TS + 1;
+        tma_row(ts.J, hr, h.row);
+        h.l = ts.J[(lane + 1) * kBoxW + kBoxX - 1];
+        h.r = ts.J[(lane + 1) * kBoxW + kBoxX + TS];
+        h.cl = ts.J[hr * kBoxW + kBoxX - 1];
+        h.cr = ts.J[hr * kBoxW + kBoxX + TS];
+      } else {
+        reg_load_halo(a, x0, y0, lane, h);  // the interior is ours and current
+      }
       rerun = true;
     }
   }
@@ -1347,7 +1473,10 @@ __global__ void __launch_bounds__(kCtaThreads)
         oa1 = a1;
         ob0 = b0;
         ob1 = b1;
-        fence_acq_rel();  // publish the tile before any neighbour is (re)queued
+        // publish the tile before any neighbour is (re)queued.  With no
+        // neighbour to activate no fence is needed: a neighbour that this
+        // border cannot raise never needs to see it (need_h was false)
+        if (dirs) fence_acq_rel();
         __syncwarp();
         bool own = false;
         unsigned ntile = 0;
@@ -1593,10 +1722,42 @@ TileQueue carve_tile_queue(Carver &c, unsigned ntiles) {
   q.ring = c.take<unsigned long long>(cap);
   q.mask = cap - 1;
   unsigned *ctr = c.take<unsigned>(4);
+  q.tmaps = c.take<unsigned char>(2 * 128);  // 256-byte aligned by the carver
   q.head = ctr;
   q.tail = ctr + 1;
   q.pending = ctr + 2;
   return q;
+}
+
+// A 2D u8 tensor map of a (H, W) image with 48 x 34 boxes (TMA staging of
+// the register engine).  The encoder comes from the driver at run time (no
+// link-time libcuda dependency).  Needs 16-byte aligned rows.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static bool make_u8_box_map(CUtensorMap *map, const void *base, int W, int H) {
+  static EncodeTiledFn encode = nullptr;
+  static int tried = 0;
+  if (!tried) {
+    tried = 1;
+    if (!getenv("IWPP_NO_TMA")) {
+      void *fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        encode = (EncodeTiledFn)fn;
+    }
+  }
+  if (!encode || W % 16 != 0 || (uintptr_t)base % 16 != 0) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)H};
+  const cuuint64_t strides[1] = {(cuuint64_t)W};
+  const cuuint32_t box[2] = {(cuuint32_t)kBoxW, (cuuint32_t)kBoxH};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // the register engine covers u8 (and binary); the shared-memory engine stays
@@ -1686,7 +1847,14 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
     int rb = reg_blocks;
     if (o.max_blocks > 0 && rb > o.max_blocks) rb = o.max_blocks;
     if ((unsigned)rb > max_b) rb = (int)max_b;
-    tile_engine_reg_kernel<CONN><<<rb, kCtaThreads, 0, st>>>(a, counters);
+    // the two box descriptors go to the workspace (global memory)
+    alignas(128) static thread_local CUtensorMap maps[2];
+    const int use_tma = vec && q.tmaps && make_u8_box_map(&maps[0], J, W, H) &&
+                        make_u8_box_map(&maps[1], I, W, H);
+    if (use_tma) IWPP_CUDA_TRY(cudaMemcpyAsync(q.tmaps, maps, sizeof maps, cudaMemcpyHostToDevice, st));
+    if (getenv("IWPP_TRACE")) fprintf(stderr, "[iwpp] reg engine %dx%d use_tma=%d vec=%d\n", W, H, use_tma, (int)vec);
+    tile_engine_reg_kernel<CONN><<<rb, kCtaThreads, 0, st>>>(a, counters, (const CUtensorMap *)q.tmaps,
+                                                            use_tma);
   } else {
     kern<<<blocks, kCtaThreads, smem, st>>>(a, counters);
   }

@@ -38,6 +38,7 @@ struct TileQueue {
   unsigned long long *ring;  // (pos << 32) | tile
   unsigned mask;             // ring capacity - 1
   unsigned *head, *tail, *pending;
+  void *tmaps;               // 2 TMA descriptors (register engine), in device memory
 };
 
 struct EngineOpts {
