@@ -245,7 +245,9 @@ static bool host_slabs(int64_t W, int64_t H, size_t es, int64_t rows, std::vecto
   b.clear();
   bool taper = rows <= 0;
   if (rows <= 0) {
-    rows = (int64_t)((size_t)(4u << 20) / ((size_t)W * es));
+    double mb = 4.0;
+    if (const char *e = getenv("IWPP_SLAB_MB")) mb = atof(e);  // diagnostics
+    rows = (int64_t)(mb * (1 << 20) / ((double)W * es));
     if (rows < 8 * TS) rows = 8 * TS;
   }
   rows = (rows + TS - 1) / TS * TS;
@@ -255,7 +257,17 @@ static bool host_slabs(int64_t W, int64_t H, size_t es, int64_t rows, std::vecto
   int64_t tail = 0;
   std::vector<int64_t> last;
   if (taper) {
-    for (int64_t part : {rows / 4, rows / 2}) {
+    std::vector<int64_t> parts = {rows / 4, rows / 2};
+    if (const char *e = getenv("IWPP_TAPER")) {  // diagnostics: divisors, smallest slab first
+      parts.clear();
+      for (const char *q = e; *q;) {
+        int d = atoi(q);
+        if (d > 0) parts.push_back(rows / d);
+        while (*q && *q != ',') q++;
+        if (*q == ',') q++;
+      }
+    }
+    for (int64_t part : parts) {
       part = std::max<int64_t>(TS, part / TS * TS);
       if (H - tail - part >= rows) {
         last.push_back(part);
