@@ -890,17 +890,17 @@ template <int CONN>
 __device__ __forceinline__ int reg_fixpoint(unsigned *j, const unsigned *m, const RegHalo &h,
                                             int lane, bool &changed) {
   constexpr unsigned LO8 = 0x00FF00FFu;
-  unsigned e[8], o[8], ie[8], io[8], he[8], ho[8];
+  unsigned e[8], o[8], ie[8], io[8];
 #pragma unroll
   for (int k = 0; k < 8; k++) {
     e[k] = j[k] & LO8;
     o[k] = (j[k] >> 8) & LO8;
     ie[k] = m[k] & LO8;
     io[k] = (m[k] >> 8) & LO8;
-    he[k] = h.row[k] & LO8;
-    ho[k] = (h.row[k] >> 8) & LO8;
   }
-  // the halo columns' values (vertical maxima for 8-conn) are constant
+  // The halo is constant during the iteration: its whole effect on the
+  // tile's fixed point is the lower bound min(I, halo dilation) on the edge
+  // pixels.  Apply it once; the steps below then see a closed tile.
   unsigned hlv = h.l, hrv = h.r;
   if (CONN == 8) {
     unsigned lu = __shfl_up_sync(FULL, h.l, 1), ld = __shfl_down_sync(FULL, h.l, 1);
@@ -910,16 +910,34 @@ __device__ __forceinline__ int reg_fixpoint(unsigned *j, const unsigned *m, cons
     hlv = max(h.l, max(lu, ld));
     hrv = max(h.r, max(ru, rd));
   }
+  e[0] = max2(e[0], min2(ie[0], hlv));
+  o[7] = max2(o[7], min2(io[7], hrv << 16));
+  if (lane == 0 || lane == 31) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const unsigned he = h.row[k] & LO8, ho = (h.row[k] >> 8) & LO8;
+      unsigned dE = he, dO = ho;
+      if (CONN == 8) {
+        const unsigned hoP = k ? (h.row[k - 1] >> 8) & LO8 : (h.cl << 16);
+        const unsigned heN = k < 7 ? h.row[k + 1] & LO8 : h.cr;
+        dE = max2(he, max2(__funnelshift_l(hoP, ho, 16), ho));
+        dO = max2(ho, max2(he, __funnelshift_r(he, heN, 16)));
+      }
+      e[k] = max2(e[k], min2(ie[k], dE));
+      o[k] = max2(o[k], min2(io[k], dO));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; k++) changed |= ((e[k] | (o[k] << 8)) != j[k]);
   int steps = 0;
   for (;;) {
     steps++;
     unsigned ve[8], vo[8];
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      unsigned ue = __shfl_up_sync(FULL, e[k], 1), de = __shfl_down_sync(FULL, e[k], 1);
-      unsigned uo = __shfl_up_sync(FULL, o[k], 1), dn = __shfl_down_sync(FULL, o[k], 1);
-      if (lane == 0) { ue = he[k]; uo = ho[k]; }
-      if (lane == 31) { de = he[k]; dn = ho[k]; }
+      // lanes 0 / 31 see themselves: harmless under max
+      const unsigned ue = __shfl_up_sync(FULL, e[k], 1), de = __shfl_down_sync(FULL, e[k], 1);
+      const unsigned uo = __shfl_up_sync(FULL, o[k], 1), dn = __shfl_down_sync(FULL, o[k], 1);
       ve[k] = CONN == 8 ? max2(e[k], max2(ue, de)) : max2(ue, de);
       vo[k] = CONN == 8 ? max2(o[k], max2(uo, dn)) : max2(uo, dn);
     }
@@ -928,8 +946,8 @@ __device__ __forceinline__ int reg_fixpoint(unsigned *j, const unsigned *m, cons
       // 3x3 max = horizontal max of the vertical maxima
 #pragma unroll
       for (int k = 0; k < 8; k++) {
-        const unsigned lE = __funnelshift_l(k ? vo[k - 1] : (hlv << 16), vo[k], 16);
-        const unsigned rO = __funnelshift_r(ve[k], k < 7 ? ve[k + 1] : hrv, 16);
+        const unsigned lE = __funnelshift_l(k ? vo[k - 1] : 0u, vo[k], 16);
+        const unsigned rO = __funnelshift_r(ve[k], k < 7 ? ve[k + 1] : 0u, 16);
         const unsigned dE = max2(ve[k], max2(lE, vo[k]));
         const unsigned dO = max2(vo[k], max2(ve[k], rO));
         const unsigned nE = min2(ie[k], dE), nO = min2(io[k], dO);  // D >= J (centre included)
@@ -938,11 +956,11 @@ __device__ __forceinline__ int reg_fixpoint(unsigned *j, const unsigned *m, cons
         o[k] = nO;
       }
     } else {
-      unsigned prevo = h.l << 16;
+      unsigned prevo = 0;
 #pragma unroll
       for (int k = 0; k < 8; k++) {
         const unsigned lE = __funnelshift_l(prevo, o[k], 16);
-        const unsigned rO = __funnelshift_r(e[k], k < 7 ? e[k + 1] : h.r, 16);
+        const unsigned rO = __funnelshift_r(e[k], k < 7 ? e[k + 1] : 0u, 16);
         const unsigned dE = max2(max2(ve[k], e[k]), max2(lE, o[k]));
         const unsigned dO = max2(max2(vo[k], o[k]), max2(e[k], rO));
         prevo = o[k];  // the old odd word, for word k + 1
@@ -1235,6 +1253,317 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
       } else {
         reg_load_halo(a, x0, y0, lane, h);  // the interior is ours and current
       }
+      rerun = true;
+    }
+  }
+  if (l0) {
+    atomicAdd(&counters[CNT_TILES], n_tiles);
+    atomicAdd(&counters[CNT_RERUNS], n_reruns);
+    atomicAdd(&counters[CNT_STEPS], n_steps);
+    for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
+  }
+}
+
+// --- register engine, 16 / 32-bit kinds (u16, int32; f32 via the ordered map) ---
+//
+// Same design as the u8 register engine: one warp per 32 x 32 tile, lane =
+// row, the row's 32 values in registers (widened to int), Jacobi steps
+// J <- min(I, max over the 3 x 3 / cross neighbourhood) to the tile's fixed
+// point, the same queue protocol.  The tile and its halo are staged in
+// shared memory first (TMA box when rows are 16-byte aligned, else a
+// cooperative copy); the halo rows / columns and the last published border
+// (the activation test's inputs) are read from that box, so registers hold
+// only the 2 x 32 row values.
+template <typename T>
+struct R32 {
+  static constexpr int OFF = 16 / (int)sizeof(T);  // box columns left of the tile
+  static constexpr int BW = TS + 2 * OFF;          // box width (elements, 16-byte rows)
+  static constexpr int LO = (int)Elem<T>::lo;      // the sentinel (outside the image)
+};
+
+template <typename T>
+struct alignas(128) Box32Smem {
+  static constexpr int BYTES = (TS + 2) * R32<T>::BW * (int)sizeof(T);
+  T J[TS + 2][R32<T>::BW];
+  uint8_t pad0[(128 - BYTES % 128) % 128];  // TMA destinations are 128-byte aligned
+  T I[TS + 2][R32<T>::BW];
+  uint8_t pad1[(128 - BYTES % 128) % 128];
+  unsigned long long bar;
+};
+
+// stage the J (and I) box of tile (x0, y0); cells outside the image hold LO
+template <typename T>
+__device__ __forceinline__ void box32_stage(const EngineArgs &a, const CUtensorMap *maps, int use_tma,
+                                            Box32Smem<T> &b, int x0, int y0, bool withI,
+                                            unsigned &phase, int lane) {
+  constexpr int OFF = R32<T>::OFF, BW = R32<T>::BW;
+  constexpr int BYTES = (TS + 2) * BW * (int)sizeof(T);
+  __syncwarp();  // the previous box contents have been read
+  const bool edge = x0 - OFF < 0 || y0 - 1 < 0 || x0 + TS + OFF > a.W || y0 + TS + 1 > a.H;
+  if (use_tma) {
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      mbar_expect_tx(&b.bar, withI ? 2u * BYTES : (unsigned)BYTES);
+      tma_load_box(maps, &b.J[0][0], &b.bar, x0 - OFF, y0 - 1);
+      if (withI) tma_load_box(maps + 1, &b.I[0][0], &b.bar, x0 - OFF, y0 - 1);
+    }
+    mbar_wait(&b.bar, phase);
+    phase ^= 1u;
+    if (edge && Elem<T>::lo != 0) {  // TMA fills with 0: patch the sentinel in
+      for (int i = lane; i < (TS + 2) * BW; i += 32) {
+        const int r = i / BW, c = i - r * BW, gx = x0 - OFF + c, gy = y0 - 1 + r;
+        if (gx < 0 || gx >= a.W || gy < 0 || gy >= a.H) {
+          b.J[r][c] = Elem<T>::lo;
+          if (withI) b.I[r][c] = Elem<T>::lo;
+        }
+      }
+    }
+  } else {
+    const T *J = (const T *)a.J, *I = (const T *)a.I;
+    for (int i = lane; i < (TS + 2) * BW; i += 32) {
+      const int r = i / BW, c = i - r * BW, gx = x0 - OFF + c, gy = y0 - 1 + r;
+      const bool in = gx >= 0 && gx < a.W && gy >= 0 && gy < a.H;
+      const size_t g = (size_t)gy * a.W + gx;
+      b.J[r][c] = in ? ld_cg(J + g) : Elem<T>::lo;
+      if (withI) b.I[r][c] = in ? __ldg(I + g) : Elem<T>::lo;
+    }
+  }
+  __syncwarp();
+}
+
+template <int CONN, typename T>
+__device__ __forceinline__ int reg32_fixpoint(int *j, const int *m, const Box32Smem<T> &b, int lane,
+                                              bool &changed) {
+  constexpr int OFF = R32<T>::OFF, LO = R32<T>::LO;
+  const int row = lane + 1;
+  // The halo is constant during the iteration, so its whole effect on the
+  // tile's fixed point is the lower bound min(I, halo dilation) on the edge
+  // pixels: apply it once, then iterate with the tile closed (shuffles only).
+  {
+    int hl = (int)b.J[row][OFF - 1], hr = (int)b.J[row][OFF + TS];
+    if (CONN == 8) {
+      hl = max(hl, max((int)b.J[row - 1][OFF - 1], (int)b.J[row + 1][OFF - 1]));
+      hr = max(hr, max((int)b.J[row - 1][OFF + TS], (int)b.J[row + 1][OFF + TS]));
+    }
+    bool ch = false;
+    int nj = max(j[0], min(m[0], hl));
+    ch |= nj != j[0];
+    j[0] = nj;
+    nj = max(j[TS - 1], min(m[TS - 1], hr));
+    ch |= nj != j[TS - 1];
+    j[TS - 1] = nj;
+    if (lane == 0 || lane == 31) {
+      const int hrow = lane == 0 ? 0 : TS + 1;
+#pragma unroll
+      for (int k = 0; k < TS; k++) {
+        int h = (int)b.J[hrow][OFF + k];
+        if (CONN == 8) h = max(h, max((int)b.J[hrow][OFF + k - 1], (int)b.J[hrow][OFF + k + 1]));
+        nj = max(j[k], min(m[k], h));
+        ch |= nj != j[k];
+        j[k] = nj;
+      }
+    }
+    changed |= ch;
+  }
+  int steps = 0;
+  for (;;) {
+    steps++;
+    bool ch = false;
+    // rows lane-1 / lane+1 (lanes 0 / 31 see themselves: harmless under max)
+    auto vert = [&](int k) -> int {
+      const int u = __shfl_up_sync(FULL, j[k], 1), d = __shfl_down_sync(FULL, j[k], 1);
+      return CONN == 8 ? max(j[k], max(u, d)) : max(u, d);
+    };
+    if (CONN == 8) {
+      int left = LO, vc = vert(0);  // left: max over the 3 rows at k-1, Gauss-Seidel in the row
+#pragma unroll
+      for (int k = 0; k < TS; k++) {
+        const int vn = k + 1 < TS ? vert(k + 1) : LO;
+        const int nj = min(m[k], max(vc, max(left, vn)));  // >= j[k]: the centre is included
+        ch |= nj != j[k];
+        j[k] = nj;
+        left = max(vc, nj);
+        vc = vn;
+      }
+    } else {
+      int prev = LO;  // the updated left neighbour (Gauss-Seidel in the row)
+#pragma unroll
+      for (int k = 0; k < TS; k++) {
+        const int right = k + 1 < TS ? j[k + 1] : LO;
+        const int D = max(max(prev, right), vert(k));
+        const int nj = max(j[k], min(m[k], D));
+        ch |= nj != j[k];
+        j[k] = nj;
+        prev = nj;
+      }
+    }
+    if (!__any_sync(FULL, ch)) break;
+    changed = true;
+  }
+  return steps;
+}
+
+template <typename T, int CONN>
+__global__ void __launch_bounds__(kCtaThreads, 3)
+    tile_engine_reg32_kernel(EngineArgs a, unsigned long long *counters, const CUtensorMap *tmaps,
+                             int use_tma) {
+  constexpr int OFF = R32<T>::OFF, LO = R32<T>::LO;
+  __shared__ Box32Smem<T> bsm[kWarpsPerCta];
+  Box32Smem<T> &b = bsm[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const bool l0 = lane == 0, l31 = lane == 31;
+  unsigned phase = 0;
+  if (use_tma && l0) {
+    mbar_init(&b.bar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmaps) : "memory");
+    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmaps + 1) : "memory");
+  }
+  __syncwarp();
+  unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0;
+  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  int next_tile = -1;
+  for (;;) {
+    long long c_pop = l0 ? clock64() : 0;
+    int t = -1;
+    if (l0) {
+      t = next_tile >= 0 ? next_tile : ring_pop(a.q);
+      if (t >= 0) {
+        atomicExch(&a.q.state[t], ST_R);
+        fence_acq_rel();
+      }
+    }
+    t = __shfl_sync(FULL, t, 0);
+    next_tile = -1;
+    if (t < 0) break;
+    const int tx = t % a.ntx, ty = t / a.ntx;
+    const int x0 = tx * TS, y0 = ty * TS;
+    long long c_load = l0 ? clock64() : 0;
+    if (l0) ph[0] += c_load - c_pop;
+    box32_stage<T>(a, tmaps, use_tma, b, x0, y0, true, phase, lane);
+    int j[TS], m[TS];
+#pragma unroll
+    for (int k = 0; k < TS; k++) {
+      j[k] = (int)b.J[lane + 1][OFF + k];
+      m[k] = (int)b.I[lane + 1][OFF + k];
+    }
+    if (l0) ph[1] += clock64() - c_load;
+    bool rerun = false;
+    for (;;) {
+      n_tiles += l0;
+      n_reruns += l0 && rerun;
+      long long c_fix = l0 ? clock64() : 0;
+      bool changed = false;
+      const int steps = reg32_fixpoint<CONN, T>(j, m, b, lane, changed);
+      if (l0) n_steps += steps;
+      changed = __any_sync(FULL, changed);
+      long long c_st = l0 ? clock64() : 0;
+      if (l0) ph[2] += c_st - c_fix;
+      if (changed) {
+        const int gy = y0 + lane;
+        if (gy < a.H) {  // store my row
+          T *p = (T *)a.J + (size_t)gy * a.W + x0;
+          if (a.vec && x0 + TS <= a.W) {
+            constexpr int E = 16 / (int)sizeof(T);
+#pragma unroll
+            for (int v = 0; v < TS / E; v++) {
+              uint4 w;
+              T *e = reinterpret_cast<T *>(&w);
+#pragma unroll
+              for (int q = 0; q < E; q++) e[q] = (T)j[v * E + q];
+              reinterpret_cast<uint4 *>(p)[v] = w;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < TS; k++)
+              if (x0 + k < a.W) p[k] = (T)j[k];
+          }
+        }
+        if (a.dirty && l0) a.dirty[ty] = 1;
+        // the box still holds the border as last published (loaded at the
+        // start of the activation / refreshed on re-runs)
+        const int row = lane + 1, ob_row = l0 ? 1 : TS, h_row = l0 ? 0 : TS + 1;
+        bool need_row = false;
+        if (l0 || l31) {
+          int cp = LO, cc = j[0] != (int)b.J[ob_row][OFF] ? j[0] : LO;
+#pragma unroll
+          for (int k = 0; k < TS; k++) {
+            const int cn = k + 1 < TS ? (j[k + 1] != (int)b.J[ob_row][OFF + k + 1] ? j[k + 1] : LO) : LO;
+            const int D = CONN == 8 ? max(cc, max(cp, cn)) : cc;
+            const int hJ = (int)b.J[h_row][OFF + k], hI = (int)b.I[h_row][OFF + k];
+            need_row |= hJ < hI && hJ < D;
+            cp = cc;
+            cc = cn;
+          }
+        }
+        const int cl = j[0] != (int)b.J[row][OFF] ? j[0] : LO;
+        const int cr = j[TS - 1] != (int)b.J[row][OFF + TS - 1] ? j[TS - 1] : LO;
+        int dl = cl, dr = cr;
+        if (CONN == 8) {
+          int u = __shfl_up_sync(FULL, cl, 1), d = __shfl_down_sync(FULL, cl, 1);
+          if (l0) u = LO;
+          if (l31) d = LO;
+          dl = max(cl, max(u, d));
+          u = __shfl_up_sync(FULL, cr, 1);
+          d = __shfl_down_sync(FULL, cr, 1);
+          if (l0) u = LO;
+          if (l31) d = LO;
+          dr = max(cr, max(u, d));
+        }
+        const int hlJ = (int)b.J[row][OFF - 1], hlI = (int)b.I[row][OFF - 1];
+        const int hrJ = (int)b.J[row][OFF + TS], hrI = (int)b.I[row][OFF + TS];
+        unsigned dirs = 0;
+        if (__any_sync(FULL, l0 && need_row)) dirs |= 1u << 1;   // N
+        if (__any_sync(FULL, l31 && need_row)) dirs |= 1u << 7;  // S
+        if (__any_sync(FULL, hlJ < hlI && hlJ < dl)) dirs |= 1u << 3;  // W
+        if (__any_sync(FULL, hrJ < hrI && hrJ < dr)) dirs |= 1u << 5;  // E
+        if (CONN == 8) {
+          const int cJl = (int)b.J[h_row][OFF - 1], cIl = (int)b.I[h_row][OFF - 1];
+          const int cJr = (int)b.J[h_row][OFF + TS], cIr = (int)b.I[h_row][OFF + TS];
+          const bool cwl = cJl < cIl && cJl < cl, cwr = cJr < cIr && cJr < cr;
+          if (__any_sync(FULL, l0 && cwl)) dirs |= 1u << 0;
+          if (__any_sync(FULL, l0 && cwr)) dirs |= 1u << 2;
+          if (__any_sync(FULL, l31 && cwl)) dirs |= 1u << 6;
+          if (__any_sync(FULL, l31 && cwr)) dirs |= 1u << 8;
+        }
+        // the published border becomes the reference for the next check
+        __syncwarp();
+        b.J[row][OFF] = (T)j[0];
+        b.J[row][OFF + TS - 1] = (T)j[TS - 1];
+        if (l0 || l31)
+#pragma unroll
+          for (int k = 0; k < TS; k++) b.J[ob_row][OFF + k] = (T)j[k];
+        if (dirs) fence_acq_rel();  // publish before any neighbour is (re)queued
+        __syncwarp();
+        bool own = false;
+        unsigned ntile = 0;
+        if (lane < 9 && ((dirs >> lane) & 1u)) {
+          int ntxi = tx + (lane % 3) - 1, ntyi = ty + (lane / 3) - 1;
+          if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty) {
+            ntile = (unsigned)(ntyi * a.ntx + ntxi);
+            own = activate_claim(a.q, ntile);
+          }
+        }
+        unsigned ownmask = __ballot_sync(FULL, own);
+        int keep = (ownmask && next_tile < 0) ? __ffs(ownmask) - 1 : -1;
+        if (own && lane != keep) ring_push(a.q, ntile);
+        if (keep >= 0) next_tile = __shfl_sync(FULL, (int)ntile, keep);
+      }
+      int done = 0;
+      if (l0) {
+        unsigned old = atomicCAS(&a.q.state[t], ST_R, 0u);
+        if (old == ST_R) {
+          atomicSub(a.q.pending, 1u);
+          done = 1;
+        } else {
+          atomicExch(&a.q.state[t], ST_R);  // consume the request (acquire)
+          fence_acq_rel();
+        }
+      }
+      done = __shfl_sync(FULL, done, 0);
+      if (l0) ph[5] += clock64() - c_st;
+      if (done) break;
+      box32_stage<T>(a, tmaps, use_tma, b, x0, y0, false, phase, lane);  // J halo (+ our rows)
       rerun = true;
     }
   }
@@ -1737,7 +2066,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static bool make_u8_box_map(CUtensorMap *map, const void *base, int W, int H) {
+static bool make_box_map(CUtensorMap *map, const void *base, int W, int H, int esize, int boxW) {
   static EncodeTiledFn encode = nullptr;
   static int tried = 0;
   if (!tried) {
@@ -1750,12 +2079,15 @@ static bool make_u8_box_map(CUtensorMap *map, const void *base, int W, int H) {
         encode = (EncodeTiledFn)fn;
     }
   }
-  if (!encode || W % 16 != 0 || (uintptr_t)base % 16 != 0) return false;
+  if (!encode || ((size_t)W * esize) % 16 != 0 || (uintptr_t)base % 16 != 0) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)H};
-  const cuuint64_t strides[1] = {(cuuint64_t)W};
-  const cuuint32_t box[2] = {(cuuint32_t)kBoxW, (cuuint32_t)kBoxH};
+  const cuuint64_t strides[1] = {(cuuint64_t)W * esize};
+  const cuuint32_t box[2] = {(cuuint32_t)boxW, (cuuint32_t)kBoxH};
   const cuuint32_t estr[2] = {1, 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box,
+  const CUtensorMapDataType dt = esize == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                              : CU_TENSOR_MAP_DATA_TYPE_INT32;
+  return encode(map, dt, 2, const_cast<void *>(base), dims, strides, box,
                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -1765,7 +2097,6 @@ static bool make_u8_box_map(CUtensorMap *map, const void *base, int W, int H) {
 // for the forced-overflow path, in-tile sweep counts)
 template <typename T>
 static bool use_reg_engine(const EngineOpts &o) {
-  if (sizeof(T) != 1) return false;
   if (o.engine == ENGINE_SMEM) return false;
   if (o.engine == ENGINE_REG) return true;
   return o.qcap <= 0 && o.sweeps_set == 0;
@@ -1836,6 +2167,24 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
     if (o.max_blocks > 0 && bb > o.max_blocks) bb = o.max_blocks;
     if ((unsigned)bb > max_b) bb = (int)max_b;
     tile_engine_bin_kernel<CONN><<<bb, kCtaThreads, 0, st>>>(a, counters);
+  } else if (sizeof(T) > 1 && use_reg_engine<T>(o)) {  // 16 / 32-bit register engine
+    static int r32_blocks = 0;
+    if (r32_blocks == 0) {
+      int per_sm = 0;
+      IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, tile_engine_reg32_kernel<T, CONN>, kCtaThreads, 0));
+      r32_blocks = device_sm_count() * (per_sm < 1 ? 1 : per_sm);
+    }
+    int rb = r32_blocks;
+    if (o.max_blocks > 0 && rb > o.max_blocks) rb = o.max_blocks;
+    if ((unsigned)rb > max_b) rb = (int)max_b;
+    alignas(128) static thread_local CUtensorMap maps32[2];
+    const int use_tma = q.tmaps && make_box_map(&maps32[0], J, W, H, sizeof(T), R32<T>::BW) &&
+                        make_box_map(&maps32[1], I, W, H, sizeof(T), R32<T>::BW);
+    if (use_tma)
+      IWPP_CUDA_TRY(cudaMemcpyAsync(q.tmaps, maps32, sizeof maps32, cudaMemcpyHostToDevice, st));
+    tile_engine_reg32_kernel<T, CONN><<<rb, kCtaThreads, 0, st>>>(a, counters,
+                                                                  (const CUtensorMap *)q.tmaps, use_tma);
   } else if (use_reg_engine<T>(o)) {
     static int reg_blocks = 0;
     if (reg_blocks == 0) {
@@ -1849,8 +2198,8 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
     if ((unsigned)rb > max_b) rb = (int)max_b;
     // the two box descriptors go to the workspace (global memory)
     alignas(128) static thread_local CUtensorMap maps[2];
-    const int use_tma = vec && q.tmaps && make_u8_box_map(&maps[0], J, W, H) &&
-                        make_u8_box_map(&maps[1], I, W, H);
+    const int use_tma = vec && q.tmaps && make_box_map(&maps[0], J, W, H, 1, kBoxW) &&
+                        make_box_map(&maps[1], I, W, H, 1, kBoxW);
     if (use_tma) IWPP_CUDA_TRY(cudaMemcpyAsync(q.tmaps, maps, sizeof maps, cudaMemcpyHostToDevice, st));
     if (getenv("IWPP_TRACE")) fprintf(stderr, "[iwpp] reg engine %dx%d use_tma=%d vec=%d\n", W, H, use_tma, (int)vec);
     tile_engine_reg_kernel<CONN><<<rb, kCtaThreads, 0, st>>>(a, counters, (const CUtensorMap *)q.tmaps,

@@ -18,10 +18,16 @@ elif case == "same":
 elif case == "imfill":
     bw = oracle.gen_synthetic_mask(4096, 4096, 50, 7)
     J, I = oracle.imfill_pair(np.tile(bw, (n // 4096, n // 4096)))
+DT = int(os.environ.get("DTYPE", "0"))
+if DT == 1:
+    J, I = J.astype(np.uint16) * 200, I.astype(np.uint16) * 200
+elif DT == 2:
+    J, I = J.astype(np.int32) * 1000 - 7, I.astype(np.int32) * 1000 - 7
+elif DT == 3:
+    J, I = J.astype(np.float32) * 0.5 - 3, I.astype(np.float32) * 0.5 - 3
 dJ, dI = torch.from_numpy(J).cuda(), torch.from_numpy(I).cuda()
 L = _lib.lib()
 H, W = J.shape
-DT = int(os.environ.get("DTYPE", "0"))
 ws = _lib.workspace(L.iwpp_recon_workspace_bytes(W, H, DT, conn))
 out = dJ.clone()
 o = _lib.ReconOpts(); o.engine = int(os.environ.get("ENGINE", "0")); o.sweeps = int(os.environ.get("GSW", "0")); o.max_blocks = mb; o.check_contract = 0; o.queue_capacity = 0; o.tile_sweeps = tsw; o.halo_sweep_threshold = hth
