@@ -216,6 +216,24 @@ int iwpp_edt_host(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *
                   float *dist, void *workspace, size_t workspace_bytes,
                   int64_t max_rounds, iwpp_stats *stats, void *stream);
 
+/* ---- image I/O on the device (reference: gridwave/imgio.py) ----
+ * The Python readers put the file's raster in pinned host memory, copy it
+ * to the device and decode it there. */
+/* read_pgm (imgio.py:62-110): P5 raster -> samples.  bytes_per_sample 1
+ * (maxval <= 255) or 2 (16-bit big-endian); binary = 1 maps nonzero -> 255
+ * (maxval 1, imgio.py:108-109).  *max_sample_host (if not NULL; syncs) gets
+ * the largest raw sample, for the "sample exceeds maxval" check
+ * (imgio.py:105-106).  dst / raster 16-byte aligned; workspace >= 8 bytes. */
+int iwpp_pgm_decode(void *dst, const void *raster, int64_t n, int bytes_per_sample, int binary,
+                    void *workspace, int64_t *max_sample_host, void *stream);
+/* write_pgm (imgio.py:113-130): samples -> P5 raster (u16 big-endian). */
+int iwpp_pgm_encode(void *raster, const void *src, int64_t n, int bytes_per_sample, void *stream);
+/* gen_marker (imgio.py:216-228): marker = max(mask - h, 0), dtype u8 / u16 /
+ * i32 / f32 (f32: np.maximum semantics, NaN propagates). */
+int iwpp_gen_marker(void *marker, const void *mask, int64_t n, int dtype, double h, void *stream);
+/* the CLI's quantized EDT view (cli.py:98-101): min(rint(dist), 255) as u8 */
+int iwpp_quantize_u8(uint8_t *out, const float *dist, int64_t n, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,7 +35,8 @@ EXPORTS = (
     "iwpp_edt_finalize", "iwpp_edt_host_workspace_bytes", "iwpp_edt_host",
     "iwpp_event_create", "iwpp_event_destroy", "iwpp_event_record", "iwpp_event_elapsed_ms",
     "iwpp_edt_slab_workspace_bytes", "iwpp_edt_slab_init", "iwpp_edt_slab_round",
-    "iwpp_edt_slab_finalize",
+    "iwpp_edt_slab_finalize", "iwpp_pgm_decode", "iwpp_pgm_encode", "iwpp_gen_marker",
+    "iwpp_quantize_u8",
 )
 
 
@@ -103,6 +104,10 @@ def load_library(path: str = LIB_PATH):
             "iwpp_edt_slab_round": ([P, I64, I64, I64, I, I64, P, P, P, P,
                                      ctypes.POINTER(I64), P], I),
             "iwpp_edt_slab_finalize": ([P, I64, I64, I64, I64, P, P, P], I),
+            "iwpp_pgm_decode": ([P, P, I64, I, I, P, ctypes.POINTER(I64), P], I),
+            "iwpp_pgm_encode": ([P, P, I64, I, P], I),
+            "iwpp_gen_marker": ([P, P, I64, I, ctypes.c_double, P], I),
+            "iwpp_quantize_u8": ([P, P, I64, P], I),
         }
         for name, (args, res) in proto.items():
             fn = getattr(L, name)
