@@ -15,7 +15,8 @@ import numpy as np
 from .errors import ContractViolation, EngineError, NoBackgroundError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libiwpp_b200.so")
+# IWPP_B200_LIB: load another build (development: compile-time variants)
+LIB_PATH = os.environ.get("IWPP_B200_LIB") or os.path.join(HERE, "libiwpp_b200.so")
 
 IWPP_OK = 0
 IWPP_E_CONTRACT = -1

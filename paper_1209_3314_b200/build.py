@@ -33,17 +33,22 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile libiwpp_b200.so (or, for development variants, ``out`` with
+    extra ``-D`` ``defines``)."""
+    if out is None and not force and not _stale():
         return LIB
+    target = out or LIB
     cmd = [_nvcc(), "-shared", "-Xcompiler", "-fPIC", "-O3", "-lineinfo", "-std=c++17",
-           *ARCH, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+           *ARCH, *[f"-D{d}" for d in defines], "-o", target + ".tmp",
+           *[os.path.join(CSRC, s) for s in SOURCES]]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=CSRC)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

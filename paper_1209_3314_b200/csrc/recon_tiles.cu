@@ -544,7 +544,7 @@ __device__ void tile_fixpoint(WarpSmem<T> &s, unsigned qlimit, bool full, int sw
   bool rescan = true, pending = false, swept = false, offered = false;
   for (;;) {
     if (rescan) {
-      long long d0 = l0 ? clock64() : 0;
+      long long d0 = pclock(l0);
       unsigned n = 0;
       if (!offered) {  // halo -> border offers, once per activation
         offered = true;
@@ -560,11 +560,11 @@ __device__ void tile_fixpoint(WarpSmem<T> &s, unsigned qlimit, bool full, int sw
         n = 0;
         for (int sp = 1; sp < sweeps; sp++) changed |= sweep_pass<CONN>(s, lane);
         changed |= sweep_detect<CONN>(s, n, qlimit, lane);
-        if (l0) ph[2] += clock64() - d0;
+        if (kPhases && l0) ph[2] += clock64() - d0;
       } else if (full) {
         swept = true;
         n = detect_full<CONN>(s, 0, qlimit, lane);
-        if (l0) ph[3] += clock64() - d0;
+        if (kPhases && l0) ph[3] += clock64() - d0;
       }
       __syncwarp();
       full = true;  // later rescans (overflow recovery) are always full
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
 
   int next_tile = -1;  // a claimed neighbour this warp continues with
   for (;;) {
-    long long c_pop = l0 ? clock64() : 0;
+    long long c_pop = pclock(l0);
     int t = -1;
     unsigned first = 0;
     if (l0) {
@@ -665,8 +665,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
     const int tx = t % a.ntx, ty = t / a.ntx;
     const int x0 = tx * TS, y0 = ty * TS;
     const int limx = min(TS, a.W - x0), limy = min(TS, a.H - y0);
-    long long c_load = l0 ? clock64() : 0;
-    if (l0) ph[0] += c_load - c_pop;
+    long long c_load = pclock(l0);
+    if (kPhases && l0) ph[0] += c_load - c_pop;
 
     load_tile<T>(a, s, x0, y0, lane);
     __syncwarp();
@@ -676,20 +676,20 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
       s.ring0[r] = s.J[sidx(lx, ly)];
     }
     __syncwarp();
-    if (l0) ph[1] += clock64() - c_load;
+    if (kPhases && l0) ph[1] += clock64() - c_load;
     bool rerun = false;
     for (;;) {  // re-run while neighbours request it
       n_tiles += l0;
       n_reruns += l0 && rerun;
-      long long c_fix = l0 ? clock64() : 0;
+      long long c_fix = pclock(l0);
       unsigned long long sd0 = ph[2] + ph[3];
       bool changed = false;
       tile_fixpoint<CONN>(s, a.qlimit, full, a.sweeps, a.halo_thresh, lane, changed, n_push,
                           n_over, n_seeds, ph);
       full = false;
       changed = __any_sync(FULL, changed);
-      long long c_st = l0 ? clock64() : 0;
-      if (l0) ph[4] += (c_st - c_fix) - (ph[2] + ph[3] - sd0);
+      long long c_st = pclock(l0);
+      if (kPhases && l0) ph[4] += (c_st - c_fix) - (ph[2] + ph[3] - sd0);
       if (changed) {
         __syncwarp();
         store_tile<T>(a, s, x0, y0, limx, limy, lane);
@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
         }
       }
       done = __shfl_sync(FULL, done, 0);
-      if (l0) ph[5] += clock64() - c_st;
+      if (kPhases && l0) ph[5] += clock64() - c_st;
       if (done) break;
       __syncwarp();
       load_halo<T>(a, s, x0, y0, lane);  // the interior is ours and current
@@ -786,7 +786,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
     atomicAdd(&counters[CNT_PUSHES], n_push);
     atomicAdd(&counters[CNT_OVERFLOW], n_over);
     atomicAdd(&counters[CNT_SEEDS], n_seeds);
-    for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
+    if (kPhases)
+      for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
   }
 }
 
@@ -1075,7 +1076,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
   unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
   int next_tile = -1;
   for (;;) {
-    long long c_pop = l0 ? clock64() : 0;
+    long long c_pop = pclock(l0);
     int t = -1;
     if (l0) {
       t = next_tile >= 0 ? next_tile : ring_pop(a.q);
@@ -1089,8 +1090,8 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     if (t < 0) break;
     const int tx = t % a.ntx, ty = t / a.ntx;
     const int x0 = tx * TS, y0 = ty * TS;
-    long long c_load = l0 ? clock64() : 0;
-    if (l0) ph[0] += c_load - c_pop;
+    long long c_load = pclock(l0);
+    if (kPhases && l0) ph[0] += c_load - c_pop;
 
     unsigned j[8], m[8];
     RegHalo h;
@@ -1135,18 +1136,18 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     }
     unsigned obl = j[0] & 0xffu, obr = j[7] >> 24;
     __syncwarp();
-    if (l0) ph[1] += clock64() - c_load;
+    if (kPhases && l0) ph[1] += clock64() - c_load;
     bool rerun = false;
     for (;;) {  // re-run while neighbours request it
       n_tiles += l0;
       n_reruns += l0 && rerun;
-      long long c_fix = l0 ? clock64() : 0;
+      long long c_fix = pclock(l0);
       bool changed = false;
       const int steps = reg_fixpoint<CONN>(j, m, h, lane, changed);
       if (l0) n_steps += steps;
       changed = __any_sync(FULL, changed);
-      long long c_st = l0 ? clock64() : 0;
-      if (l0) ph[2] += c_st - c_fix;
+      long long c_st = pclock(l0);
+      if (kPhases && l0) ph[2] += c_st - c_fix;
       if (changed) {
         // store my row
         const int gy = y0 + lane;
@@ -1240,7 +1241,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
         }
       }
       done = __shfl_sync(FULL, done, 0);
-      if (l0) ph[5] += clock64() - c_st;
+      if (kPhases && l0) ph[5] += clock64() - c_st;
       if (done) break;
       if (use_tma) {  // the interior is ours and current: refresh the J halo only
         tma_stage(tmJ, tmI, ts, x0, y0, false, tphase, lane);
@@ -1260,7 +1261,8 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     atomicAdd(&counters[CNT_TILES], n_tiles);
     atomicAdd(&counters[CNT_RERUNS], n_reruns);
     atomicAdd(&counters[CNT_STEPS], n_steps);
-    for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
+    if (kPhases)
+      for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
   }
 }
 
@@ -1404,7 +1406,7 @@ __device__ __forceinline__ int reg32_fixpoint(int *j, const int *m, const Box32S
 }
 
 template <typename T, int CONN>
-__global__ void __launch_bounds__(kCtaThreads, 3)
+__global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
     tile_engine_reg32_kernel(EngineArgs a, unsigned long long *counters, const CUtensorMap *tmaps,
                              int use_tma) {
   constexpr int OFF = R32<T>::OFF, LO = R32<T>::LO;
@@ -1424,7 +1426,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
   unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
   int next_tile = -1;
   for (;;) {
-    long long c_pop = l0 ? clock64() : 0;
+    long long c_pop = pclock(l0);
     int t = -1;
     if (l0) {
       t = next_tile >= 0 ? next_tile : ring_pop(a.q);
@@ -1438,8 +1440,8 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     if (t < 0) break;
     const int tx = t % a.ntx, ty = t / a.ntx;
     const int x0 = tx * TS, y0 = ty * TS;
-    long long c_load = l0 ? clock64() : 0;
-    if (l0) ph[0] += c_load - c_pop;
+    long long c_load = pclock(l0);
+    if (kPhases && l0) ph[0] += c_load - c_pop;
     box32_stage<T>(a, tmaps, use_tma, b, x0, y0, true, phase, lane);
     int j[TS], m[TS];
 #pragma unroll
@@ -1447,18 +1449,18 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
       j[k] = (int)b.J[lane + 1][OFF + k];
       m[k] = (int)b.I[lane + 1][OFF + k];
     }
-    if (l0) ph[1] += clock64() - c_load;
+    if (kPhases && l0) ph[1] += clock64() - c_load;
     bool rerun = false;
     for (;;) {
       n_tiles += l0;
       n_reruns += l0 && rerun;
-      long long c_fix = l0 ? clock64() : 0;
+      long long c_fix = pclock(l0);
       bool changed = false;
       const int steps = reg32_fixpoint<CONN, T>(j, m, b, lane, changed);
       if (l0) n_steps += steps;
       changed = __any_sync(FULL, changed);
-      long long c_st = l0 ? clock64() : 0;
-      if (l0) ph[2] += c_st - c_fix;
+      long long c_st = pclock(l0);
+      if (kPhases && l0) ph[2] += c_st - c_fix;
       if (changed) {
         const int gy = y0 + lane;
         if (gy < a.H) {  // store my row
@@ -1561,7 +1563,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
         }
       }
       done = __shfl_sync(FULL, done, 0);
-      if (l0) ph[5] += clock64() - c_st;
+      if (kPhases && l0) ph[5] += clock64() - c_st;
       if (done) break;
       box32_stage<T>(a, tmaps, use_tma, b, x0, y0, false, phase, lane);  // J halo (+ our rows)
       rerun = true;
@@ -1571,7 +1573,8 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     atomicAdd(&counters[CNT_TILES], n_tiles);
     atomicAdd(&counters[CNT_RERUNS], n_reruns);
     atomicAdd(&counters[CNT_STEPS], n_steps);
-    for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
+    if (kPhases)
+      for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
   }
 }
 
@@ -1705,7 +1708,7 @@ __global__ void __launch_bounds__(kCtaThreads)
   unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
   int next_tile = -1;
   for (;;) {
-    long long c_pop = l0 ? clock64() : 0;
+    long long c_pop = pclock(l0);
     int t = -1;
     if (l0) {
       t = next_tile >= 0 ? next_tile : ring_pop(a.q);
@@ -1719,25 +1722,25 @@ __global__ void __launch_bounds__(kCtaThreads)
     if (t < 0) break;
     const int tx = t % a.ntx, ty = t / a.ntx;
     const int x0 = tx * TSB, y0 = ty * TSB;
-    long long c_load = l0 ? clock64() : 0;
-    if (l0) ph[0] += c_load - c_pop;
+    long long c_load = pclock(l0);
+    if (kPhases && l0) ph[0] += c_load - c_pop;
     unsigned jt[4], mt[4];
     BinHalo h;
     bin_load(a, x0, y0, lane, true, jt, mt, h);
     unsigned a0 = jt[0], a1 = jt[1], b0 = jt[2], b1 = jt[3];
     unsigned oa0 = a0, oa1 = a1, ob0 = b0, ob1 = b1;  // as last published
-    if (l0) ph[1] += clock64() - c_load;
+    if (kPhases && l0) ph[1] += clock64() - c_load;
     bool rerun = false;
     for (;;) {
       n_tiles += l0;
       n_reruns += l0 && rerun;
-      long long c_fix = l0 ? clock64() : 0;
+      long long c_fix = pclock(l0);
       bool changed = false;
       const int steps = bin_fixpoint<CONN>(a0, a1, b0, b1, mt[0], mt[1], mt[2], mt[3], h, lane, changed);
       if (l0) n_steps += steps;
       changed = __any_sync(FULL, changed);
-      long long c_st = l0 ? clock64() : 0;
-      if (l0) ph[2] += c_st - c_fix;
+      long long c_st = pclock(l0);
+      if (kPhases && l0) ph[2] += c_st - c_fix;
       if (changed) {
         uint32_t *Jw = (uint32_t *)a.J;
         const int wx = x0 >> 5, ya = y0 + lane, yb = ya + 32;
@@ -1833,7 +1836,7 @@ __global__ void __launch_bounds__(kCtaThreads)
         }
       }
       done = __shfl_sync(FULL, done, 0);
-      if (l0) ph[5] += clock64() - c_st;
+      if (kPhases && l0) ph[5] += clock64() - c_st;
       if (done) break;
       bin_load(a, x0, y0, lane, false, jt, mt, h);  // the tile is ours: halo only
       rerun = true;
@@ -1843,7 +1846,8 @@ __global__ void __launch_bounds__(kCtaThreads)
     atomicAdd(&counters[CNT_TILES], n_tiles);
     atomicAdd(&counters[CNT_RERUNS], n_reruns);
     atomicAdd(&counters[CNT_STEPS], n_steps);
-    for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
+    if (kPhases)
+      for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
   }
 }
 

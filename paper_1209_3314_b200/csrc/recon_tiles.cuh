@@ -17,7 +17,24 @@ constexpr int BITW = (PNS + 31) / 32;    // in-queue bitmap words
 constexpr int kWarpsPerCta = 4;
 constexpr int kCtaThreads = 32 * kWarpsPerCta;
 constexpr int kCtaMinBlocks = 5;  // resident CTAs per SM (shared memory allows 5 for u8)
-constexpr int kRegCtaMinBlocks = 4;  // register engine: registers are the limit
+#ifndef IWPP_REG_MIN_BLOCKS
+#define IWPP_REG_MIN_BLOCKS 5
+#endif
+#ifndef IWPP_REG32_MIN_BLOCKS
+#define IWPP_REG32_MIN_BLOCKS 4
+#endif
+// register engines: registers are the limit (u8 / binary; 16/32-bit kinds)
+constexpr int kRegCtaMinBlocks = IWPP_REG_MIN_BLOCKS;
+constexpr int kReg32CtaMinBlocks = IWPP_REG32_MIN_BLOCKS;
+
+// Per-phase clock counters (pop / load / sweep / ... ; CNT_PH_*) cost
+// registers in the engines: compiled in only with -DIWPP_PHASES.
+#ifdef IWPP_PHASES
+constexpr bool kPhases = true;
+#else
+constexpr bool kPhases = false;
+#endif
+__device__ __forceinline__ long long pclock(bool l0) { return (kPhases && l0) ? clock64() : 0; }
 static_assert(RQ >= PN && (RQ & (RQ - 1)) == 0, "ring must hold a full rescan");
 static_assert(PNS < 65536, "queue entries are 16-bit");
 
