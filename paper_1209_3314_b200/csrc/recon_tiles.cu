@@ -164,6 +164,25 @@ __device__ __forceinline__ int ring_pop(const TileQueue &q) {
 //   finish   : CAS(R -> 0); failure means Q was set meanwhile -> re-run
 // Returns true when the caller now owns an idle tile's activation (it must
 // either push it or process it itself); pending already counts it.
+// Take a tile (state <- R) with acquire semantics: the borders published
+// before any request this consumes are visible afterwards.  An acquire RMW
+// (ATOM + L1 invalidate) rather than RMW + fence.acq_rel, whose MEMBAR would
+// also wait for this warp's own earlier, unfenced stores.
+#ifndef IWPP_STATE_ACQ
+#define IWPP_STATE_ACQ 1
+#endif
+__device__ __forceinline__ unsigned state_take(unsigned *p) {
+#if IWPP_STATE_ACQ
+  unsigned old;
+  asm volatile("atom.acquire.gpu.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(ST_R) : "memory");
+  return old;
+#else
+  const unsigned old = atomicExch(p, ST_R);
+  fence_acq_rel();
+  return old;
+#endif
+}
+
 __device__ __forceinline__ bool activate_claim(const TileQueue &q, unsigned t) {
   unsigned old = atomicOr(&q.state[t], ST_Q);
   if (old == 0) {
@@ -653,8 +672,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
     if (l0) {
       t = next_tile >= 0 ? next_tile : ring_pop(a.q);
       if (t >= 0) {
-        unsigned old = atomicExch(&a.q.state[t], ST_R);
-        fence_acq_rel();
+        unsigned old = state_take(&a.q.state[t]);
         first = old & ST_V;
       }
     }
@@ -767,8 +785,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
           atomicSub(a.q.pending, 1u);
           done = 1;
         } else {
-          atomicExch(&a.q.state[t], ST_R);  // consume the request (acquire)
-          fence_acq_rel();
+          state_take(&a.q.state[t]);  // consume the request (acquire)
         }
       }
       done = __shfl_sync(FULL, done, 0);
@@ -1081,8 +1098,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     if (l0) {
       t = next_tile >= 0 ? next_tile : ring_pop(a.q);
       if (t >= 0) {
-        atomicExch(&a.q.state[t], ST_R);
-        fence_acq_rel();
+        state_take(&a.q.state[t]);
       }
     }
     t = __shfl_sync(FULL, t, 0);
@@ -1236,8 +1252,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
           atomicSub(a.q.pending, 1u);
           done = 1;
         } else {
-          atomicExch(&a.q.state[t], ST_R);  // consume the request (acquire)
-          fence_acq_rel();
+          state_take(&a.q.state[t]);  // consume the request (acquire)
         }
       }
       done = __shfl_sync(FULL, done, 0);
@@ -1431,8 +1446,7 @@ __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
     if (l0) {
       t = next_tile >= 0 ? next_tile : ring_pop(a.q);
       if (t >= 0) {
-        atomicExch(&a.q.state[t], ST_R);
-        fence_acq_rel();
+        state_take(&a.q.state[t]);
       }
     }
     t = __shfl_sync(FULL, t, 0);
@@ -1558,8 +1572,7 @@ __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
           atomicSub(a.q.pending, 1u);
           done = 1;
         } else {
-          atomicExch(&a.q.state[t], ST_R);  // consume the request (acquire)
-          fence_acq_rel();
+          state_take(&a.q.state[t]);  // consume the request (acquire)
         }
       }
       done = __shfl_sync(FULL, done, 0);
@@ -1713,8 +1726,7 @@ __global__ void __launch_bounds__(kCtaThreads)
     if (l0) {
       t = next_tile >= 0 ? next_tile : ring_pop(a.q);
       if (t >= 0) {
-        atomicExch(&a.q.state[t], ST_R);
-        fence_acq_rel();
+        state_take(&a.q.state[t]);
       }
     }
     t = __shfl_sync(FULL, t, 0);
@@ -1831,8 +1843,7 @@ __global__ void __launch_bounds__(kCtaThreads)
           atomicSub(a.q.pending, 1u);  // (see the register engine: no fence needed)
           done = 1;
         } else {
-          atomicExch(&a.q.state[t], ST_R);  // consume the request (acquire)
-          fence_acq_rel();
+          state_take(&a.q.state[t]);  // consume the request (acquire)
         }
       }
       done = __shfl_sync(FULL, done, 0);
