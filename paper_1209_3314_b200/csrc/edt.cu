@@ -26,6 +26,8 @@
 //    (edt.py:278-280 -- __dsqrt_rn then RN to float), INF count for
 //    NoBackgroundError.
 
+#include <stdio.h>
+#include <stdlib.h>
 #include "edt.cuh"
 
 namespace iwpp {
@@ -138,6 +140,7 @@ __global__ void edt_seed_kernel(const int64_t *__restrict__ seeds, int64_t n_see
 template <int CONN>
 __global__ void __launch_bounds__(kRoundThreads) edt_rounds_kernel(int W, int H, EdtState s,
                                                                    long long max_rounds) {
+  unsigned bar_g = grid_barrier_gen(&s.bar[1]);
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u;
   unsigned long long visits = 0;
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_kernel(int W, int H,
         nxt[pos++] = ((uint32_t)qy << 16) | (uint32_t)qx;
       }
     }
-    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x);
+    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     s.counters[EC_ROUNDS] = (unsigned long long)r;
@@ -332,6 +335,7 @@ enum { QM_BQ = 0, QM_PF = 1, QM_NAIVE = 2 };
 template <int CONN, bool CHECK, int QMODE = QM_BQ>
 __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, int H, EdtState s,
                                                                        long long max_rounds) {
+  unsigned bar_g = grid_barrier_gen(&s.bar[1]);
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u;
   // BQ: the block's next-frontier items, spilled to the global queue (GBQ)
@@ -438,7 +442,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
     if (threadIdx.x == 0 && m) bq_base = atomicAdd(ncnt, m);
     __syncthreads();
     for (unsigned i = threadIdx.x; i < m; i += blockDim.x) nxt[bq_base + i] = bq[i];
-    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x);
+    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     s.counters[EC_ROUNDS] = (unsigned long long)r;
@@ -453,6 +457,8 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
 #define IWPP_RASTER_MIN 262144
 #endif
 constexpr unsigned kRasterMinFrontier = IWPP_RASTER_MIN;
+constexpr int kRtraceRounds = 65536;
+constexpr unsigned kRasterWpt = 4;  // bitmap words per thread per compaction pass
 //
 // The same two-phase rounds as edt_rounds_key_kernel, with no returned
 // atomic on a round's critical path and the frontier in raster order:
@@ -473,6 +479,7 @@ constexpr unsigned kRasterMinFrontier = IWPP_RASTER_MIN;
 template <int CONN, bool CHECK>
 __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W, int H, EdtState s,
                                                                           long long max_rounds) {
+  unsigned bar_g = grid_barrier_gen(&s.bar[1]);
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   __shared__ unsigned wsum[kRoundThreads / 32];
@@ -484,8 +491,8 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
   unsigned long long visits = 0;
   unsigned long long *K = s.keys;
   // this CTA's run of bitmap words (phase 2)
-  const unsigned per = (nwords + gridDim.x - 1) / gridDim.x;
-  const unsigned w_lo = blockIdx.x * per, w_hi = min(nwords, w_lo + per);
+  const unsigned per = ((nwords + gridDim.x - 1) / gridDim.x + kRasterWpt - 1) / kRasterWpt * kRasterWpt;
+  const unsigned w_lo = min(nwords, blockIdx.x * per), w_hi = min(nwords, w_lo + per);
   int r = 0;
   for (;; r++) {
     const unsigned n = ld_acquire(&s.cnt[r % 3]);
@@ -500,6 +507,12 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       s.cnt[(r + 2) % 3] = 0;
       visits += n;
+      if (s.rtrace && r < kRtraceRounds) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        s.rtrace[2 * r] = t;
+        s.rtrace[2 * r + 1] = n;
+      }
     }
     if (n < kRasterMinFrontier) {
       // a small frontier: the queue round (returned atomics, transition-rule
@@ -508,27 +521,29 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
       __syncthreads();
       unsigned *ncnt = &s.cnt[(r + 1) % 3];
       const unsigned stride = gridDim.x * blockDim.x;
+      const unsigned first = blockIdx.x * blockDim.x + threadIdx.x;
+      uint32_t pyx_next = first < n ? __ldcg(cur + first) : 0u;  // one item ahead
       for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
         const unsigned i = base + lane;
         unsigned mask = 0;
-        int px = 0, py = 0;
+        const uint32_t pyx = pyx_next;
+        pyx_next = i + stride < n ? __ldcg(cur + i + stride) : 0u;
+        const int py = (int)(pyx >> 16), px = (int)(pyx & 0xffffu);
         if (i < n) {
-          const uint32_t pyx = __ldcg(cur + i);
-          py = (int)(pyx >> 16);
-          px = (int)(pyx & 0xffffu);
           const size_t p = (size_t)py * W + px;
+          // the cell's key and its neighbours' round-start keys in flight together
           const unsigned long long kp = __ldcg(K + 2 * p + kr);
+          unsigned long long rq[Nbr<CONN>::N], nk[Nbr<CONN>::N];
+#pragma unroll
+          for (int k = 0; k < Nbr<CONN>::N; k++) {
+            const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
+            const bool in = qx >= 0 && qx < W && qy >= 0 && qy < H;
+            rq[k] = in ? __ldcg(K + 2 * ((size_t)qy * W + qx) + kr) : 0ull;
+          }
           atomicMin(K + 2 * p + kw, kp);
           if (kp != KINF) {
             const uint32_t src = (uint32_t)kp;
-            unsigned long long rq[Nbr<CONN>::N], nk[Nbr<CONN>::N];
             unsigned cand = 0;
-#pragma unroll
-            for (int k = 0; k < Nbr<CONN>::N; k++) {
-              const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
-              const bool in = qx >= 0 && qx < W && qy >= 0 && qy < H;
-              rq[k] = in ? __ldcg(K + 2 * ((size_t)qy * W + qx) + kr) : 0ull;
-            }
 #pragma unroll
             for (int k = 0; k < Nbr<CONN>::N; k++) {
               const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
@@ -570,31 +585,31 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
       if (threadIdx.x == 0 && m) blk_base = atomicAdd(ncnt, m);
       __syncthreads();
       for (unsigned i = threadIdx.x; i < m; i += blockDim.x) nxt[blk_base + i] = bq[i];
-      grid_barrier(&s.bar[0], &s.bar[1], gridDim.x);
+      grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
       continue;
     }
     // phase 1: offers
     const unsigned stride = gridDim.x * blockDim.x;
+    const unsigned first = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t pyx_next = first < n ? __ldcg(cur + first) : 0u;  // the item, one step ahead
     for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
       const unsigned i = base + lane;
-      int px = 0, py = 0;
-      unsigned long long kp = KINF;
-      if (i < n) {
-        const uint32_t pyx = __ldcg(cur + i);
-        py = (int)(pyx >> 16);
-        px = (int)(pyx & 0xffffu);
-        const size_t p = (size_t)py * W + px;
-        kp = K[2 * p + kr];
-        atomicMin(K + 2 * p + kw, kp);  // the building key lags on the frontier (RED)
-      }
-      const uint32_t src = (uint32_t)kp;
+      const bool act = i < n;
+      const uint32_t pyx = pyx_next;
+      pyx_next = i + stride < n ? __ldcg(cur + i + stride) : 0u;
+      const int py = (int)(pyx >> 16), px = (int)(pyx & 0xffffu);
+      const size_t p = (size_t)py * W + px;
+      // the cell's key and its neighbours' round-start keys, all in flight at once
+      const unsigned long long kp = act ? K[2 * p + kr] : KINF;
       unsigned long long rq[Nbr<CONN>::N];
 #pragma unroll
       for (int k = 0; k < Nbr<CONN>::N; k++) {
         const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
-        const bool in = kp != KINF && qx >= 0 && qx < W && qy >= 0 && qy < H;
+        const bool in = act && qx >= 0 && qx < W && qy >= 0 && qy < H;
         rq[k] = in ? K[2 * ((size_t)qy * W + qx) + kr] : 0ull;
       }
+      if (act) atomicMin(K + 2 * p + kw, kp);  // the building key lags on the frontier (RED)
+      const uint32_t src = (uint32_t)kp;
 #pragma unroll
       for (int k = 0; k < Nbr<CONN>::N; k++) {
         const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
@@ -606,7 +621,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
         } else {
           nk = make_key(qx, qy, src);
         }
-        const bool push = ok && nk < rq[k];  // rq = 0 off the image / for inactive lanes
+        const bool push = kp != KINF && ok && nk < rq[k];  // rq = 0 off the image / inactive
         if (push) atomicMin(K + 2 * ((size_t)qy * W + qx) + kw, nk);
         const unsigned waddr = push ? (unsigned)qy * (unsigned)WW + ((unsigned)qx >> 5) : 0xffffffffu;
         const unsigned grp = __match_any_sync(FULL, waddr);
@@ -614,14 +629,24 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
         if (push && lane == (unsigned)(__ffs(grp) - 1)) atomicOr(Fb + waddr, orb);
       }
     }
-    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x);
+    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
     // phase 2: compact this CTA's words of the bitmap into the next list,
-    // one 512-word chunk at a time (block prefix sum, one global atomic per
-    // non-empty chunk), clearing them
-    for (unsigned wb = w_lo; wb < w_hi; wb += blockDim.x) {
-      const unsigned wi = wb + threadIdx.x;
-      unsigned w = wi < w_hi ? __ldcg(Fb + wi) : 0u;
-      const unsigned c = __popc(w);
+    // kRasterWpt words per thread per pass (one 16-byte load; one block
+    // prefix sum and one global atomic per pass), clearing them
+    for (unsigned wb = w_lo; wb < w_hi; wb += blockDim.x * kRasterWpt) {
+      const unsigned wi = wb + threadIdx.x * kRasterWpt;
+      unsigned w4[kRasterWpt];
+      const bool full = wi + kRasterWpt <= w_hi;
+      if (full) {
+        const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(Fb + wi));
+        w4[0] = v.x, w4[1] = v.y, w4[2] = v.z, w4[3] = v.w;
+      } else {
+#pragma unroll
+        for (unsigned k = 0; k < kRasterWpt; k++) w4[k] = wi + k < w_hi ? __ldcg(Fb + wi + k) : 0u;
+      }
+      unsigned c = 0;
+#pragma unroll
+      for (unsigned k = 0; k < kRasterWpt; k++) c += __popc(w4[k]);
       unsigned incl = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -641,18 +666,28 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
       }
       __syncthreads();
       unsigned o = blk_base + wsum[warp] + incl - c;
-      if (w) {
-        Fb[wi] = 0u;
-        const unsigned y = wi / (unsigned)WW, x0 = (wi - y * (unsigned)WW) * 32;
-        while (w) {
-          const int bb = __ffs(w) - 1;
-          w &= w - 1;
-          nxt[o++] = (y << 16) | (x0 + bb);
+      if (c) {
+        if (full) {
+          *reinterpret_cast<uint4 *>(Fb + wi) = make_uint4(0u, 0u, 0u, 0u);
+        } else {
+          for (unsigned k = 0; k < kRasterWpt; k++)
+            if (w4[k]) Fb[wi + k] = 0u;
+        }
+#pragma unroll
+        for (unsigned k = 0; k < kRasterWpt; k++) {
+          unsigned w = w4[k];
+          if (!w) continue;
+          const unsigned y = (wi + k) / (unsigned)WW, x0 = (wi + k - y * (unsigned)WW) * 32;
+          while (w) {
+            const int bb = __ffs(w) - 1;
+            w &= w - 1;
+            nxt[o++] = (y << 16) | (x0 + bb);
+          }
         }
       }
       __syncthreads();
     }
-    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x);
+    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     s.counters[EC_ROUNDS] = (unsigned long long)r;
@@ -742,6 +777,7 @@ static EdtState carve_any(Carver &c, int64_t W, int64_t H, bool cas) {
   s.rflag = c.take<unsigned>(nreg);
   for (int i = 0; i < 3; i++) s.alist[i] = c.take<unsigned>(nreg);
   s.diag = c.take<unsigned long long>(16);
+  s.rtrace = nullptr;
   return s;
 }
 
@@ -836,7 +872,24 @@ int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_round
     int w = W, h = H;
     EdtState ss = s;
     void *args[] = {&w, &h, &ss, &max_rounds};
+    static unsigned long long *rtrace = nullptr;  // diagnostics: IWPP_EDT_RTRACE=1
+    const char *tr = getenv("IWPP_EDT_RTRACE");
+    if (tr && tr[0] == '1') {
+      if (!rtrace) IWPP_CUDA_TRY(cudaMalloc(&rtrace, 2 * sizeof(unsigned long long) * kRtraceRounds));
+      IWPP_CUDA_TRY(cudaMemsetAsync(rtrace, 0, 2 * sizeof(unsigned long long) * kRtraceRounds, st));
+      ss.rtrace = rtrace;
+    }
     IWPP_CUDA_TRY(cudaLaunchCooperativeKernel(rk, dim3(rb), dim3(kRoundThreads), args, 0, st));
+    if (ss.rtrace) {
+      static unsigned long long h[2 * kRtraceRounds];
+      IWPP_CUDA_TRY(cudaMemcpyAsync(h, rtrace, sizeof h, cudaMemcpyDeviceToHost, st));
+      IWPP_CUDA_TRY(cudaStreamSynchronize(st));
+      int nr = 0;
+      while (nr + 1 < kRtraceRounds && h[2 * (nr + 1)]) nr++;
+      for (int i = 0; i < nr; i++)
+        fprintf(stderr, "[edt rtrace] round %d n %llu dt_us %.2f\n", i, h[2 * i + 1],
+                (h[2 * i + 2] - h[2 * i]) * 1e-3);
+    }
     return IWPP_OK;
   }
   void *kern = s.keymode

@@ -36,6 +36,7 @@ struct EdtState {
   unsigned *alist[3];        // active region lists (triple-buffered)
   unsigned *acnt, *wc;       // [3] list sizes, [3] work counters
   unsigned long long *diag;  // [16] block-engine diagnostics (IWPP_TRACE)
+  unsigned long long *rtrace;  // per-round (globaltimer, frontier) pairs or null (IWPP_EDT_RTRACE)
 };
 
 // Images the 32-bit (y,x) source code can address.
@@ -82,14 +83,21 @@ __device__ __forceinline__ unsigned long long make_key_checked(int qx, int qy, u
 }
 
 // Software grid barrier for the persistent cooperative kernels.
-__device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen, unsigned nblocks) {
+// Thread 0's view of the barrier generation, read once at kernel start
+// (every block reads it before its first arrival, so no block can have
+// advanced it yet) and then tracked locally: one round trip less per barrier.
+__device__ __forceinline__ unsigned grid_barrier_gen(const unsigned *gen) {
+  return threadIdx.x == 0 ? ld_acquire(gen) : 0u;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen, unsigned nblocks,
+                                             unsigned &g) {
   // Arrival is an acq_rel RMW (publishes this block's writes, and the last
   // arriver acquires everyone's); the release is a release add on the
   // generation, which the waiters acquire.  No sequentially consistent
   // fences (MEMBAR.SC) on the round's critical path.
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g = ld_acquire(gen);
     unsigned arrived;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(count) : "memory");
     if (arrived == nblocks - 1) {
@@ -98,6 +106,7 @@ __device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen, uns
     } else {
       while (ld_acquire(gen) == g) __nanosleep(16);
     }
+    g++;
   }
   __syncthreads();
 }
