@@ -457,8 +457,15 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
 #define IWPP_RASTER_MIN 262144
 #endif
 constexpr unsigned kRasterMinFrontier = IWPP_RASTER_MIN;
-constexpr int kRtraceRounds = 65536;
-constexpr unsigned kRasterWpt = 4;  // bitmap words per thread per compaction pass
+constexpr int kRtraceRounds = 32768;
+__device__ __forceinline__ void rtrace_stamp(const EdtState &s, int r, int slot) {
+  if (s.rtrace && blockIdx.x == 0 && threadIdx.x == 0 && r < kRtraceRounds) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    s.rtrace[4 * r + slot] = t;
+  }
+}
+constexpr unsigned kRasterWpt = 4;  // bitmap words per thread per compaction pass (one uint4)
 //
 // The same two-phase rounds as edt_rounds_key_kernel, with no returned
 // atomic on a round's critical path and the frontier in raster order:
@@ -510,8 +517,8 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
       if (s.rtrace && r < kRtraceRounds) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        s.rtrace[2 * r] = t;
-        s.rtrace[2 * r + 1] = n;
+        s.rtrace[4 * r] = t;
+        s.rtrace[4 * r + 1] = n;
       }
     }
     if (n < kRasterMinFrontier) {
@@ -629,7 +636,10 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
         if (push && lane == (unsigned)(__ffs(grp) - 1)) atomicOr(Fb + waddr, orb);
       }
     }
+    __syncthreads();
+    rtrace_stamp(s, r, 3);
     grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
+    rtrace_stamp(s, r, 2);
     // phase 2: compact this CTA's words of the bitmap into the next list,
     // kRasterWpt words per thread per pass (one 16-byte load; one block
     // prefix sum and one global atomic per pass), clearing them
@@ -875,20 +885,24 @@ int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_round
     static unsigned long long *rtrace = nullptr;  // diagnostics: IWPP_EDT_RTRACE=1
     const char *tr = getenv("IWPP_EDT_RTRACE");
     if (tr && tr[0] == '1') {
-      if (!rtrace) IWPP_CUDA_TRY(cudaMalloc(&rtrace, 2 * sizeof(unsigned long long) * kRtraceRounds));
-      IWPP_CUDA_TRY(cudaMemsetAsync(rtrace, 0, 2 * sizeof(unsigned long long) * kRtraceRounds, st));
+      if (!rtrace) IWPP_CUDA_TRY(cudaMalloc(&rtrace, 4 * sizeof(unsigned long long) * kRtraceRounds));
+      IWPP_CUDA_TRY(cudaMemsetAsync(rtrace, 0, 4 * sizeof(unsigned long long) * kRtraceRounds, st));
       ss.rtrace = rtrace;
     }
     IWPP_CUDA_TRY(cudaLaunchCooperativeKernel(rk, dim3(rb), dim3(kRoundThreads), args, 0, st));
     if (ss.rtrace) {
-      static unsigned long long h[2 * kRtraceRounds];
+      static unsigned long long h[4 * kRtraceRounds];
       IWPP_CUDA_TRY(cudaMemcpyAsync(h, rtrace, sizeof h, cudaMemcpyDeviceToHost, st));
       IWPP_CUDA_TRY(cudaStreamSynchronize(st));
       int nr = 0;
-      while (nr + 1 < kRtraceRounds && h[2 * (nr + 1)]) nr++;
-      for (int i = 0; i < nr; i++)
-        fprintf(stderr, "[edt rtrace] round %d n %llu dt_us %.2f\n", i, h[2 * i + 1],
-                (h[2 * i + 2] - h[2 * i]) * 1e-3);
+      while (nr + 1 < kRtraceRounds && h[4 * (nr + 1)]) nr++;
+      for (int i = 0; i < nr; i++) {
+        const unsigned long long t0 = h[4 * i], t1 = h[4 * i + 4];
+        const bool rs = h[4 * i + 2] != 0;  // a raster round: work / barrier / compaction
+        fprintf(stderr, "[edt rtrace] round %d n %llu dt_us %.2f work_us %.2f bar_us %.2f comp_us %.2f\n",
+                i, h[4 * i + 1], (t1 - t0) * 1e-3, rs ? (h[4 * i + 3] - t0) * 1e-3 : 0.0,
+                rs ? (h[4 * i + 2] - h[4 * i + 3]) * 1e-3 : 0.0, rs ? (t1 - h[4 * i + 2]) * 1e-3 : 0.0);
+      }
     }
     return IWPP_OK;
   }
