@@ -9,3 +9,4 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:edt_
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:edt_rounds_raster -s 2 -c 1 -o gpurun_out/prof_edt_blob python scripts/prof_edt.py blob 4096 8 1 > /dev/null 2>&1; echo "ncu edt blob rc=$?"
 EDT_ENGINE=4 timeout 600 ncu --set full --import-source on --clock-control none -k regex:edt_block_kernel -s 2 -c 1 -o gpurun_out/prof_edtblock_nuclei python scripts/prof_edt.py nuclei 4096 8 1 > /dev/null 2>&1; echo "ncu edt block nuclei rc=$?"
 timeout 300 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"; tail -c 1500 gpurun_out/bench_ref.json
+DTYPE=2 ENGINE=0 timeout 600 ncu --set full --import-source on --clock-control none -k regex:tile_engine_reg32 -s 2 -c 1 -o gpurun_out/prof_reg32_i32 python scripts/prof_recon.py 4096 8 -1 0 rand 1 > /dev/null 2>&1; echo "ncu reg32 rc=$?"
