@@ -2126,6 +2126,37 @@ int tile_side(int dtype, const EngineOpts &o) {
   return use_bin_engine(dtype == IWPP_BIN, o) ? TSB : TS;
 }
 
+
+// the 16 / 32-bit register engine (no u8 instantiation)
+template <typename T, int CONN>
+static int launch_reg32(const EngineArgs &a, unsigned long long *counters, const TileQueue &q,
+                        const void *J, const void *I, int W, int H, const EngineOpts &o,
+                        unsigned max_b, cudaStream_t st) {
+  if constexpr (sizeof(T) == 1) {
+    return set_error(IWPP_E_CONTRACT, "no 8-bit register32 engine");
+  } else {
+    static int r32_blocks = 0;
+    if (r32_blocks == 0) {
+      int per_sm = 0;
+      IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, tile_engine_reg32_kernel<T, CONN>, kCtaThreads, 0));
+      r32_blocks = device_sm_count() * (per_sm < 1 ? 1 : per_sm);
+    }
+    int rb = r32_blocks;
+    if (o.max_blocks > 0 && rb > o.max_blocks) rb = o.max_blocks;
+    if ((unsigned)rb > max_b) rb = (int)max_b;
+    alignas(128) static thread_local CUtensorMap maps32[2];
+    const int use_tma = q.tmaps && make_box_map(&maps32[0], J, W, H, sizeof(T), R32<T>::BW) &&
+                        make_box_map(&maps32[1], I, W, H, sizeof(T), R32<T>::BW);
+    if (use_tma)
+      IWPP_CUDA_TRY(cudaMemcpyAsync(q.tmaps, maps32, sizeof maps32, cudaMemcpyHostToDevice, st));
+    tile_engine_reg32_kernel<T, CONN><<<rb, kCtaThreads, 0, st>>>(a, counters,
+                                                                  (const CUtensorMap *)q.tmaps, use_tma);
+    IWPP_CUDA_TRY(cudaGetLastError());
+    return IWPP_OK;
+  }
+}
+
 template <typename T, int CONN>
 static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
                          unsigned long long *counters, const EngineOpts &o, cudaStream_t st,
@@ -2183,23 +2214,8 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
     if ((unsigned)bb > max_b) bb = (int)max_b;
     tile_engine_bin_kernel<CONN><<<bb, kCtaThreads, 0, st>>>(a, counters);
   } else if (sizeof(T) > 1 && use_reg_engine<T>(o)) {  // 16 / 32-bit register engine
-    static int r32_blocks = 0;
-    if (r32_blocks == 0) {
-      int per_sm = 0;
-      IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, tile_engine_reg32_kernel<T, CONN>, kCtaThreads, 0));
-      r32_blocks = device_sm_count() * (per_sm < 1 ? 1 : per_sm);
-    }
-    int rb = r32_blocks;
-    if (o.max_blocks > 0 && rb > o.max_blocks) rb = o.max_blocks;
-    if ((unsigned)rb > max_b) rb = (int)max_b;
-    alignas(128) static thread_local CUtensorMap maps32[2];
-    const int use_tma = q.tmaps && make_box_map(&maps32[0], J, W, H, sizeof(T), R32<T>::BW) &&
-                        make_box_map(&maps32[1], I, W, H, sizeof(T), R32<T>::BW);
-    if (use_tma)
-      IWPP_CUDA_TRY(cudaMemcpyAsync(q.tmaps, maps32, sizeof maps32, cudaMemcpyHostToDevice, st));
-    tile_engine_reg32_kernel<T, CONN><<<rb, kCtaThreads, 0, st>>>(a, counters,
-                                                                  (const CUtensorMap *)q.tmaps, use_tma);
+    const int rc = launch_reg32<T, CONN>(a, counters, q, J, I, W, H, o, max_b, st);
+    if (rc) return rc;
   } else if (use_reg_engine<T>(o)) {
     static int reg_blocks = 0;
     if (reg_blocks == 0) {
