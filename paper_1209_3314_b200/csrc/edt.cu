@@ -140,7 +140,7 @@ __global__ void edt_seed_kernel(const int64_t *__restrict__ seeds, int64_t n_see
 template <int CONN>
 __global__ void __launch_bounds__(kRoundThreads) edt_rounds_kernel(int W, int H, EdtState s,
                                                                    long long max_rounds) {
-  unsigned bar_g = grid_barrier_gen(&s.bar[1]);
+  unsigned bar_g = grid_barrier_gen(&s.bar[kBarGen]);
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u;
   unsigned long long visits = 0;
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_kernel(int W, int H,
         nxt[pos++] = ((uint32_t)qy << 16) | (uint32_t)qx;
       }
     }
-    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
+    grid_barrier(&s.bar[0], &s.bar[kBarGen], gridDim.x, bar_g);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     s.counters[EC_ROUNDS] = (unsigned long long)r;
@@ -335,7 +335,7 @@ enum { QM_BQ = 0, QM_PF = 1, QM_NAIVE = 2 };
 template <int CONN, bool CHECK, int QMODE = QM_BQ>
 __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, int H, EdtState s,
                                                                        long long max_rounds) {
-  unsigned bar_g = grid_barrier_gen(&s.bar[1]);
+  unsigned bar_g = grid_barrier_gen(&s.bar[kBarGen]);
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u;
   // BQ: the block's next-frontier items, spilled to the global queue (GBQ)
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
     if (threadIdx.x == 0 && m) bq_base = atomicAdd(ncnt, m);
     __syncthreads();
     for (unsigned i = threadIdx.x; i < m; i += blockDim.x) nxt[bq_base + i] = bq[i];
-    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
+    grid_barrier(&s.bar[0], &s.bar[kBarGen], gridDim.x, bar_g);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     s.counters[EC_ROUNDS] = (unsigned long long)r;
@@ -486,7 +486,7 @@ constexpr unsigned kRasterWpt = 4;  // bitmap words per thread per compaction pa
 template <int CONN, bool CHECK>
 __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W, int H, EdtState s,
                                                                           long long max_rounds) {
-  unsigned bar_g = grid_barrier_gen(&s.bar[1]);
+  unsigned bar_g = grid_barrier_gen(&s.bar[kBarGen]);
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   __shared__ unsigned wsum[kRoundThreads / 32];
@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
       if (threadIdx.x == 0 && m) blk_base = atomicAdd(ncnt, m);
       __syncthreads();
       for (unsigned i = threadIdx.x; i < m; i += blockDim.x) nxt[blk_base + i] = bq[i];
-      grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
+      grid_barrier(&s.bar[0], &s.bar[kBarGen], gridDim.x, bar_g);
       continue;
     }
     // phase 1: offers
@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
     }
     __syncthreads();
     rtrace_stamp(s, r, 3);
-    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
+    grid_barrier(&s.bar[0], &s.bar[kBarGen], gridDim.x, bar_g);
     rtrace_stamp(s, r, 2);
     // phase 2: compact this CTA's words of the bitmap into the next list,
     // kRasterWpt words per thread per pass (one 16-byte load; one block
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
       }
       __syncthreads();
     }
-    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
+    grid_barrier(&s.bar[0], &s.bar[kBarGen], gridDim.x, bar_g);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     s.counters[EC_ROUNDS] = (unsigned long long)r;
@@ -756,11 +756,13 @@ static EdtState carve_any(Carver &c, int64_t W, int64_t H, bool cas) {
   }
   s.F[0] = c.take<uint32_t>(n);
   s.F[1] = c.take<uint32_t>(n);
-  unsigned *ctl = c.take<unsigned>(16);
-  s.cnt = ctl;      // [0..2]
-  s.bar = ctl + 4;  // [4..5]
-  s.acnt = ctl + 8;  // [8..10]
-  s.wc = ctl + 12;   // [12..14]
+  // the frontier counters, the barrier's arrival count and its generation
+  // (polled by every CTA) each get their own 256-byte line
+  unsigned *ctl = c.take<unsigned>(256);
+  s.cnt = ctl;        // [0..2]
+  s.bar = ctl + 64;   // bar[0] = arrivals, bar[kBarGen] = generation
+  s.acnt = ctl + 192;  // [192..194]
+  s.wc = ctl + 200;    // [200..202]
   s.counters = c.take<unsigned long long>(EC_N);
   // block engine: two planes over the same 2n keys, frontier bitmaps, regions
   const bool force_queue = g_engine_override == ENGINE_QUEUE ||
@@ -815,7 +817,7 @@ static int grid_for(size_t n, int threads) {
 }
 
 int reset_control(const EdtState &s, cudaStream_t st) {
-  IWPP_CUDA_TRY(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * 8, st));
+  IWPP_CUDA_TRY(cudaMemsetAsync(s.cnt, 0, sizeof(unsigned) * (64 + kBarGen + 1), st));
   IWPP_CUDA_TRY(cudaMemsetAsync(s.counters, 0, sizeof(unsigned long long) * EC_N, st));
   return IWPP_OK;
 }

@@ -22,7 +22,7 @@ struct EdtState {
   uint32_t *stamp;           // !keymode: round stamp per cell (frontier dedupe)
   uint32_t *F[2];            // frontier queues (yx codes)
   unsigned *cnt;             // [3] frontier sizes (triple-buffered)
-  unsigned *bar;             // [2] grid barrier count / generation
+  unsigned *bar;             // grid barrier: [0] arrivals, [kBarGen] generation
   unsigned long long *counters;
   // block engine (edt_block.cu)
   int block;                 // keymode runs on the temporally blocked engine
@@ -86,6 +86,8 @@ __device__ __forceinline__ unsigned long long make_key_checked(int qx, int qy, u
 // Thread 0's view of the barrier generation, read once at kernel start
 // (every block reads it before its first arrival, so no block can have
 // advanced it yet) and then tracked locally: one round trip less per barrier.
+constexpr int kBarGen = 64;  // generation word offset (its own 256-byte line)
+
 __device__ __forceinline__ unsigned grid_barrier_gen(const unsigned *gen) {
   return threadIdx.x == 0 ? ld_acquire(gen) : 0u;
 }

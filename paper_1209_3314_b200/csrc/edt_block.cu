@@ -349,7 +349,7 @@ __device__ void process_region(BlockSmem &S, const EdtState &s, int W, int H, un
 template <int CONN, bool CHECK>
 __global__ void __launch_bounds__(BT, kBlockMinCtas)
     edt_block_kernel(int W, int H, EdtState s, long long max_rounds) {
-  unsigned bar_g = grid_barrier_gen(&s.bar[1]);
+  unsigned bar_g = grid_barrier_gen(&s.bar[kBarGen]);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BlockSmem &S = *reinterpret_cast<BlockSmem *>(smem_raw);
   const int tid = threadIdx.x;
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(BT, kBlockMinCtas)
                                   lastchg);
       __syncthreads();
     }
-    grid_barrier(&s.bar[0], &s.bar[1], gridDim.x, bar_g);
+    grid_barrier(&s.bar[0], &s.bar[kBarGen], gridDim.x, bar_g);
     r0 += kp;
   }
   if (tid == 0 && visits) atomicAdd(&s.counters[EC_VISITS], visits);
