@@ -54,6 +54,8 @@
 #include <cstring>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+#include <type_traits>
 #include <cuda.h>  // CUtensorMap (the encoder is fetched from the driver at run time)
 
 #include "iwpp_common.cuh"
@@ -177,6 +179,11 @@ __device__ __forceinline__ int ring_pop(const TileQueue &q) {
 #ifndef IWPP_CTR_SPREAD
 #define IWPP_CTR_SPREAD 1
 #endif
+#ifndef IWPP_FUSED_INIT
+#define IWPP_FUSED_INIT 1
+#endif
+// below this many tiles a cooperative launch costs more than the init kernel
+constexpr unsigned kFusedInitMinTiles = 128;
 __device__ __forceinline__ unsigned state_take(unsigned *p) {
 #if IWPP_STATE_ACQ
   unsigned old;
@@ -1073,10 +1080,26 @@ __device__ __forceinline__ void tma_row(const uint8_t *box, int r, unsigned *w) 
   w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
 }
 
+// the two box descriptors travel as a __grid_constant__ kernel parameter
+// (no upload, no tensormap proxy fence)
+struct alignas(64) BoxMaps {
+  CUtensorMap m[2];
+};
+
+__device__ __forceinline__ void tile_queue_init(const TileQueue &q, int ntx, int nty,
+                                                unsigned long long *counters, int keep);
+
+// fused_init: the launch is cooperative and the kernel builds the initial
+// queue itself (all tiles, INIT_FULL) before one grid-wide sync, instead of
+// a separate init kernel
 template <int CONN>
 __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
-    tile_engine_reg_kernel(EngineArgs a, unsigned long long *counters, const CUtensorMap *tmaps,
-                           int use_tma) {
+    tile_engine_reg_kernel(EngineArgs a, unsigned long long *counters,
+                           const __grid_constant__ BoxMaps maps, int use_tma, int fused_init) {
+  if (fused_init) {
+    tile_queue_init(a.q, a.ntx, a.nty, counters, 0);
+    cooperative_groups::this_grid().sync();
+  }
   __shared__ RegWarpSmem wsm[kWarpsPerCta];
   // two staging buffers per warp with prefetch: the continuation tile's boxes
   // load while the current tile publishes and finishes
@@ -1084,16 +1107,13 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
   __shared__ TmaWarpSmem tsm[kWarpsPerCta][NB];
   int cur = 0;
   TmaWarpSmem *tsp = &tsm[threadIdx.x >> 5][0];
-  const CUtensorMap *tmJ = tmaps, *tmI = tmaps + 1;  // in global memory (workspace)
+  const CUtensorMap *tmJ = &maps.m[0], *tmI = &maps.m[1];
   unsigned tph[NB];
   for (int b = 0; b < NB; b++) tph[b] = 0;
   bool pf = false;  // the continuation's boxes are in flight in the other buffer
   if (use_tma && (threadIdx.x & 31) == 0) {
     for (int b = 0; b < NB; b++) mbar_init(&tsm[threadIdx.x >> 5][b].bar);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // the descriptors were written by a copy before this launch
-    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmJ) : "memory");
-    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmI) : "memory");
   }
   __syncwarp();
   const int lane = threadIdx.x & 31;
@@ -1456,9 +1476,14 @@ __device__ __forceinline__ int reg32_fixpoint(int *j, const int *m, const Box32S
 
 template <typename T, int CONN>
 __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
-    tile_engine_reg32_kernel(EngineArgs a, unsigned long long *counters, const CUtensorMap *tmaps,
-                             int use_tma) {
+    tile_engine_reg32_kernel(EngineArgs a, unsigned long long *counters,
+                             const __grid_constant__ BoxMaps maps, int use_tma, int fused_init) {
   constexpr int OFF = R32<T>::OFF, LO = R32<T>::LO;
+  if (fused_init) {  // cooperative launch: build the initial queue here
+    tile_queue_init(a.q, a.ntx, a.nty, counters, 0);
+    cooperative_groups::this_grid().sync();
+  }
+  const CUtensorMap *tmaps = &maps.m[0];
   __shared__ Box32Smem<T> bsm[kWarpsPerCta];
   Box32Smem<T> &b = bsm[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1467,8 +1492,6 @@ __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
   if (use_tma && l0) {
     mbar_init(&b.bar);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmaps) : "memory");
-    asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tmaps + 1) : "memory");
   }
   __syncwarp();
   unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0;
@@ -1976,8 +1999,8 @@ int bin_unpack(const uint32_t *bits, int W, int H, void *dst, cudaStream_t st) {
 
 // Initial GBQ: every tile, ordered by 2x2 colour class (then raster) so the
 // first wave of concurrently running tiles are never neighbours.
-__global__ void tile_queue_init_kernel(TileQueue q, int ntx, int nty, unsigned long long *counters,
-                                       int keep) {
+__device__ __forceinline__ void tile_queue_init(const TileQueue &q, int ntx, int nty,
+                                                unsigned long long *counters, int keep) {
   unsigned ntiles = (unsigned)ntx * nty;
   unsigned stride = gridDim.x * blockDim.x;
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2001,6 +2024,11 @@ __global__ void tile_queue_init_kernel(TileQueue q, int ntx, int nty, unsigned l
     *q.pending = ntiles;
   }
   if (!keep && i < CNT_N) counters[i] = 0;
+}
+
+__global__ void tile_queue_init_kernel(TileQueue q, int ntx, int nty, unsigned long long *counters,
+                                       int keep) {
+  tile_queue_init(q, ntx, nty, counters, keep);
 }
 
 // Re-activation fill for slab runs (multi-GPU waves): only the tile rows
@@ -2168,7 +2196,7 @@ int tile_side(int dtype, const EngineOpts &o) {
 template <typename T, int CONN>
 static int launch_reg32(const EngineArgs &a, unsigned long long *counters, const TileQueue &q,
                         const void *J, const void *I, int W, int H, const EngineOpts &o,
-                        unsigned max_b, cudaStream_t st) {
+                        unsigned max_b, int fused_init, cudaStream_t st) {
   if constexpr (sizeof(T) == 1) {
     return set_error(IWPP_E_CONTRACT, "no 8-bit register32 engine");
   } else {
@@ -2182,13 +2210,18 @@ static int launch_reg32(const EngineArgs &a, unsigned long long *counters, const
     int rb = r32_blocks;
     if (o.max_blocks > 0 && rb > o.max_blocks) rb = o.max_blocks;
     if ((unsigned)rb > max_b) rb = (int)max_b;
-    alignas(128) static thread_local CUtensorMap maps32[2];
-    const int use_tma = q.tmaps && make_box_map(&maps32[0], J, W, H, sizeof(T), R32<T>::BW) &&
-                        make_box_map(&maps32[1], I, W, H, sizeof(T), R32<T>::BW);
-    if (use_tma)
-      IWPP_CUDA_TRY(cudaMemcpyAsync(q.tmaps, maps32, sizeof maps32, cudaMemcpyHostToDevice, st));
-    tile_engine_reg32_kernel<T, CONN><<<rb, kCtaThreads, 0, st>>>(a, counters,
-                                                                  (const CUtensorMap *)q.tmaps, use_tma);
+    BoxMaps maps;
+    memset(&maps, 0, sizeof maps);
+    int use_tma = q.tmaps && make_box_map(&maps.m[0], J, W, H, sizeof(T), R32<T>::BW) &&
+                  make_box_map(&maps.m[1], I, W, H, sizeof(T), R32<T>::BW);
+    if (fused_init) {
+      int fi = 1;
+      void *args[] = {const_cast<EngineArgs *>(&a), &counters, &maps, &use_tma, &fi};
+      IWPP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)tile_engine_reg32_kernel<T, CONN>,
+                                                dim3(rb), dim3(kCtaThreads), args, 0, st));
+    } else {
+      tile_engine_reg32_kernel<T, CONN><<<rb, kCtaThreads, 0, st>>>(a, counters, maps, use_tma, 0);
+    }
     IWPP_CUDA_TRY(cudaGetLastError());
     return IWPP_OK;
   }
@@ -2216,7 +2249,14 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   if ((unsigned)blocks > max_b) blocks = (int)max_b;
   unsigned ib = (q.mask + 1 + 255) / 256;
   if (ib > 1024) ib = 1024;
-  if (o.init_mode == INIT_CONTINUE) {
+  // the u8 register engine builds a full initial queue itself (cooperative
+  // launch): one launch less per call
+  const int fused_init = IWPP_FUSED_INIT && !use_bin_engine(binary, o) &&
+                         use_reg_engine<T>(o) && o.init_mode != INIT_CONTINUE && !o.rows_mode &&
+                         !o.keep_counters && ntiles >= kFusedInitMinTiles;
+  if (fused_init) {
+    // (the engine kernel initialises the queue)
+  } else if (o.init_mode == INIT_CONTINUE) {
     int lo = o.sel_lo < 0 ? 0 : o.sel_lo;
     int hi = (o.sel_hi < 0 || o.sel_hi >= nty) ? nty - 1 : o.sel_hi;
     if (lo > hi) return IWPP_OK;  // nothing to queue
@@ -2251,7 +2291,7 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
     if ((unsigned)bb > max_b) bb = (int)max_b;
     tile_engine_bin_kernel<CONN><<<bb, kCtaThreads, 0, st>>>(a, counters);
   } else if (sizeof(T) > 1 && use_reg_engine<T>(o)) {  // 16 / 32-bit register engine
-    const int rc = launch_reg32<T, CONN>(a, counters, q, J, I, W, H, o, max_b, st);
+    const int rc = launch_reg32<T, CONN>(a, counters, q, J, I, W, H, o, max_b, fused_init, st);
     if (rc) return rc;
   } else if (use_reg_engine<T>(o)) {
     static int reg_blocks = 0;
@@ -2264,14 +2304,19 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
     int rb = reg_blocks;
     if (o.max_blocks > 0 && rb > o.max_blocks) rb = o.max_blocks;
     if ((unsigned)rb > max_b) rb = (int)max_b;
-    // the two box descriptors go to the workspace (global memory)
-    alignas(128) static thread_local CUtensorMap maps[2];
-    const int use_tma = vec && q.tmaps && make_box_map(&maps[0], J, W, H, 1, kBoxW) &&
-                        make_box_map(&maps[1], I, W, H, 1, kBoxW);
-    if (use_tma) IWPP_CUDA_TRY(cudaMemcpyAsync(q.tmaps, maps, sizeof maps, cudaMemcpyHostToDevice, st));
-    if (getenv("IWPP_TRACE")) fprintf(stderr, "[iwpp] reg engine %dx%d use_tma=%d vec=%d\n", W, H, use_tma, (int)vec);
-    tile_engine_reg_kernel<CONN><<<rb, kCtaThreads, 0, st>>>(a, counters, (const CUtensorMap *)q.tmaps,
-                                                            use_tma);
+    BoxMaps maps;
+    memset(&maps, 0, sizeof maps);
+    int use_tma = vec && q.tmaps && make_box_map(&maps.m[0], J, W, H, 1, kBoxW) &&
+                  make_box_map(&maps.m[1], I, W, H, 1, kBoxW);
+    if (getenv("IWPP_TRACE")) fprintf(stderr, "[iwpp] reg engine %dx%d use_tma=%d vec=%d fused=%d\n", W, H, use_tma, (int)vec, fused_init);
+    if (fused_init) {
+      int fi = fused_init;
+      void *args[] = {&a, &counters, &maps, &use_tma, &fi};
+      IWPP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)tile_engine_reg_kernel<CONN>, dim3(rb),
+                                                dim3(kCtaThreads), args, 0, st));
+    } else {
+      tile_engine_reg_kernel<CONN><<<rb, kCtaThreads, 0, st>>>(a, counters, maps, use_tma, 0);
+    }
   } else {
     kern<<<blocks, kCtaThreads, smem, st>>>(a, counters);
   }
