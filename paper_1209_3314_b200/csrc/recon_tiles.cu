@@ -173,9 +173,6 @@ __device__ __forceinline__ int ring_pop(const TileQueue &q) {
 #ifndef IWPP_STATE_ACQ
 #define IWPP_STATE_ACQ 1
 #endif
-#ifndef IWPP_REG_PREFETCH
-#define IWPP_REG_PREFETCH 0
-#endif
 #ifndef IWPP_CTR_SPREAD
 #define IWPP_CTR_SPREAD 1
 #endif
@@ -1101,18 +1098,12 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     cooperative_groups::this_grid().sync();
   }
   __shared__ RegWarpSmem wsm[kWarpsPerCta];
-  // two staging buffers per warp with prefetch: the continuation tile's boxes
-  // load while the current tile publishes and finishes
-  constexpr int NB = IWPP_REG_PREFETCH ? 2 : 1;
-  __shared__ TmaWarpSmem tsm[kWarpsPerCta][NB];
-  int cur = 0;
-  TmaWarpSmem *tsp = &tsm[threadIdx.x >> 5][0];
+  __shared__ TmaWarpSmem tsm[kWarpsPerCta];
+  TmaWarpSmem &ts = tsm[threadIdx.x >> 5];
   const CUtensorMap *tmJ = &maps.m[0], *tmI = &maps.m[1];
-  unsigned tph[NB];
-  for (int b = 0; b < NB; b++) tph[b] = 0;
-  bool pf = false;  // the continuation's boxes are in flight in the other buffer
+  unsigned tphase = 0;
   if (use_tma && (threadIdx.x & 31) == 0) {
-    for (int b = 0; b < NB; b++) mbar_init(&tsm[threadIdx.x >> 5][b].bar);
+    mbar_init(&ts.bar);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
@@ -1129,7 +1120,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     int t = -1;
     if (l0) {
       t = next_tile >= 0 ? next_tile : ring_pop(a.q);
-      if (t >= 0 && !pf) state_take(&a.q.state[t]);  // (a prefetched tile was taken already)
+      if (t >= 0) state_take(&a.q.state[t]);
     }
     t = __shfl_sync(FULL, t, 0);
     next_tile = -1;
@@ -1142,16 +1133,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     unsigned j[8], m[8];
     RegHalo h;
     if (use_tma) {
-      if (IWPP_REG_PREFETCH && pf) {
-        cur ^= 1;
-        tsp = &tsm[threadIdx.x >> 5][cur];
-        mbar_wait(&tsp->bar, tph[cur]);
-        tph[cur] ^= 1u;
-        pf = false;
-      } else {
-        tma_stage(tmJ, tmI, *tsp, x0, y0, true, tph[cur], lane);
-      }
-      TmaWarpSmem &ts = *tsp;
+      tma_stage(tmJ, tmI, ts, x0, y0, true, tphase, lane);
       const int hr = lane == 0 ? 0 : TS + 1;  // halo row (lanes 0 / 31)
       tma_row(ts.J, lane + 1, j);
       tma_row(ts.I, lane + 1, m);
@@ -1281,20 +1263,6 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
         int keep = (ownmask && next_tile < 0) ? __ffs(ownmask) - 1 : -1;
         if (own && lane != keep) ring_push(a.q, ntile);
         if (keep >= 0) next_tile = __shfl_sync(FULL, (int)ntile, keep);
-        if (IWPP_REG_PREFETCH && use_tma && keep >= 0) {
-          // the continuation is ours (we won its claim): take it and start
-          // its boxes now, behind this tile's finish
-          if (l0) {
-            state_take(&a.q.state[next_tile]);
-            TmaWarpSmem &nb = tsm[threadIdx.x >> 5][cur ^ 1];
-            const int nx0 = (next_tile % a.ntx) * TS, ny0 = (next_tile / a.ntx) * TS;
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            mbar_expect_tx(&nb.bar, 2u * kBoxBytes);
-            tma_load_box(tmJ, nb.J, &nb.bar, nx0 - kBoxX, ny0 - 1);
-            tma_load_box(tmI, nb.I, &nb.bar, nx0 - kBoxX, ny0 - 1);
-          }
-          pf = true;
-        }
       }
       int done = 0;
       if (l0) {
@@ -1312,8 +1280,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
       if (kPhases && l0) ph[5] += clock64() - c_st;
       if (done) break;
       if (use_tma) {  // the interior is ours and current: refresh the J halo only
-        TmaWarpSmem &ts = *tsp;
-        tma_stage(tmJ, tmI, ts, x0, y0, false, tph[cur], lane);
+        tma_stage(tmJ, tmI, ts, x0, y0, false, tphase, lane);
         const int hr = lane == 0 ? 0 : TS + 1;
         tma_row(ts.J, hr, h.row);
         h.l = ts.J[(lane + 1) * kBoxW + kBoxX - 1];
