@@ -146,6 +146,10 @@ constexpr int kBinCtasPerSm = 4;
 #define IWPP_POP_MAX_SLEEP_NS 2048
 #endif
 constexpr unsigned kPopMaxSleepNs = IWPP_POP_MAX_SLEEP_NS;
+#ifndef IWPP_PENDING_POLL_NS
+#define IWPP_PENDING_POLL_NS 1024
+#endif
+constexpr unsigned kPendingPollNs = IWPP_PENDING_POLL_NS;
 
 __device__ __forceinline__ int ring_pop(const TileQueue &q) {
   unsigned ticket = atomicAdd(q.head, 1u);
@@ -153,7 +157,9 @@ __device__ __forceinline__ int ring_pop(const TileQueue &q) {
   for (unsigned ns = 32;; ns = ns < kPopMaxSleepNs ? ns * 2 : kPopMaxSleepNs) {
     unsigned long long v = ld_acquire64(slot);
     if ((unsigned)(v >> 32) == ticket) return (int)(v & 0xffffffffu);
-    if (ld_acquire(q.pending) == 0) return -1;
+    // the termination test reads the hot pending line: only once the
+    // slot has stayed empty for a few polls
+    if (ns >= kPendingPollNs && ld_acquire(q.pending) == 0) return -1;
     __nanosleep(ns);
   }
 }
