@@ -151,6 +151,7 @@ constexpr unsigned kPopMaxSleepNs = IWPP_POP_MAX_SLEEP_NS;
 #endif
 constexpr unsigned kPendingPollNs = IWPP_PENDING_POLL_NS;
 
+template <unsigned PollNs = kPendingPollNs>
 __device__ __forceinline__ int ring_pop(const TileQueue &q) {
   unsigned ticket = atomicAdd(q.head, 1u);
   unsigned long long *slot = &q.ring[ticket & q.mask];
@@ -158,8 +159,13 @@ __device__ __forceinline__ int ring_pop(const TileQueue &q) {
     unsigned long long v = ld_acquire64(slot);
     if ((unsigned)(v >> 32) == ticket) return (int)(v & 0xffffffffu);
     // the termination test reads the hot pending line: only once the
-    // slot has stayed empty for a few polls
-    if (ns >= kPendingPollNs && ld_acquire(q.pending) == 0) return -1;
+    // slot has stayed empty for a few polls (PollNs; the binary engine's
+    // narrow fronts keep most warps idle and measured best polling at once)
+    if constexpr (PollNs <= 32) {
+      if (ld_acquire(q.pending) == 0) return -1;
+    } else {
+      if (ns >= PollNs && ld_acquire(q.pending) == 0) return -1;
+    }
     __nanosleep(ns);
   }
 }
@@ -1754,7 +1760,7 @@ __global__ void __launch_bounds__(kCtaThreads)
     long long c_pop = pclock(l0);
     int t = -1;
     if (l0) {
-      t = next_tile >= 0 ? next_tile : ring_pop(a.q);
+      t = next_tile >= 0 ? next_tile : ring_pop<32>(a.q);
       if (t >= 0) {
         state_take(&a.q.state[t]);
       }
