@@ -2,6 +2,7 @@
 set -e; python paper_1209_3314_b200/build.py >/dev/null; python -c "import oracle; oracle.build()"; set +e
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -c 3000 gpurun_out/bench.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-extras --no-cpu > /dev/null 2>&1; echo "launches rc=$?"
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:tile_engine -s 3 -c 1 -o gpurun_out/prof_tile python bench.py --steps 1 --warmup 3 --no-extras --no-cpu > /dev/null 2>&1; echo "ncu tile rc=$?"
