@@ -205,6 +205,11 @@ __device__ __forceinline__ unsigned state_take(unsigned *p) {
 #endif
 }
 
+// the claim alone: the caller accounts for pending itself
+__device__ __forceinline__ bool activate_claim_nopend(const TileQueue &q, unsigned t) {
+  return atomicOr(&q.state[t], ST_Q) == 0;
+}
+
 __device__ __forceinline__ bool activate_claim(const TileQueue &q, unsigned t) {
   unsigned old = atomicOr(&q.state[t], ST_Q);
   if (old == 0) {
@@ -784,12 +789,17 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
           int ntxi = tx + (lane % 3) - 1, ntyi = ty + (lane / 3) - 1;
           if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty) {
             ntile = (unsigned)(ntyi * a.ntx + ntxi);
-            own = activate_claim(a.q, ntile);
+            own = activate_claim_nopend(a.q, ntile);
           }
         }
         unsigned ownmask = __ballot_sync(FULL, own);
         int keep = (ownmask && next_tile < 0) ? __ffs(ownmask) - 1 : -1;
-        if (own && lane != keep) ring_push(a.q, ntile);
+        // the kept continuation inherits this tile's pending count (no +1 here,
+        // no -1 at this tile's finish); a pushed tile counts before its push
+        if (own && lane != keep) {
+          atomicAdd(a.q.pending, 1u);
+          ring_push(a.q, ntile);
+        }
         if (keep >= 0) next_tile = __shfl_sync(FULL, (int)ntile, keep);
         for (int r = lane; r < 4 * TS; r += 32) {
           int lx, ly;
@@ -804,7 +814,7 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
         if (old == ST_R) {
           // no fence: pending is only ever changed by RMWs, whose per-location
           // order already puts our activations' increments before this
-          atomicSub(a.q.pending, 1u);
+          if (next_tile < 0) atomicSub(a.q.pending, 1u);  // (else passed on, above)
           done = 1;
         } else {
           state_take(&a.q.state[t]);  // consume the request (acquire)
@@ -1268,12 +1278,17 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
           int ntxi = tx + (lane % 3) - 1, ntyi = ty + (lane / 3) - 1;
           if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty) {
             ntile = (unsigned)(ntyi * a.ntx + ntxi);
-            own = activate_claim(a.q, ntile);
+            own = activate_claim_nopend(a.q, ntile);
           }
         }
         unsigned ownmask = __ballot_sync(FULL, own);
         int keep = (ownmask && next_tile < 0) ? __ffs(ownmask) - 1 : -1;
-        if (own && lane != keep) ring_push(a.q, ntile);
+        // the kept continuation inherits this tile's pending count (no +1 here,
+        // no -1 at this tile's finish); a pushed tile counts before its push
+        if (own && lane != keep) {
+          atomicAdd(a.q.pending, 1u);
+          ring_push(a.q, ntile);
+        }
         if (keep >= 0) next_tile = __shfl_sync(FULL, (int)ntile, keep);
       }
       int done = 0;
@@ -1282,7 +1297,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
         if (old == ST_R) {
           // no fence: pending is only ever changed by RMWs, whose per-location
           // order already puts our activations' increments before this
-          atomicSub(a.q.pending, 1u);
+          if (next_tile < 0) atomicSub(a.q.pending, 1u);  // (else passed on, above)
           done = 1;
         } else {
           state_take(&a.q.state[t]);  // consume the request (acquire)
@@ -1593,19 +1608,24 @@ __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
           int ntxi = tx + (lane % 3) - 1, ntyi = ty + (lane / 3) - 1;
           if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty) {
             ntile = (unsigned)(ntyi * a.ntx + ntxi);
-            own = activate_claim(a.q, ntile);
+            own = activate_claim_nopend(a.q, ntile);
           }
         }
         unsigned ownmask = __ballot_sync(FULL, own);
         int keep = (ownmask && next_tile < 0) ? __ffs(ownmask) - 1 : -1;
-        if (own && lane != keep) ring_push(a.q, ntile);
+        // the kept continuation inherits this tile's pending count (no +1 here,
+        // no -1 at this tile's finish); a pushed tile counts before its push
+        if (own && lane != keep) {
+          atomicAdd(a.q.pending, 1u);
+          ring_push(a.q, ntile);
+        }
         if (keep >= 0) next_tile = __shfl_sync(FULL, (int)ntile, keep);
       }
       int done = 0;
       if (l0) {
         unsigned old = atomicCAS(&a.q.state[t], ST_R, 0u);
         if (old == ST_R) {
-          atomicSub(a.q.pending, 1u);
+          if (next_tile < 0) atomicSub(a.q.pending, 1u);  // (else passed on, above)
           done = 1;
         } else {
           state_take(&a.q.state[t]);  // consume the request (acquire)
@@ -1864,19 +1884,24 @@ __global__ void __launch_bounds__(kCtaThreads)
           int ntxi = tx + (lane % 3) - 1, ntyi = ty + (lane / 3) - 1;
           if (ntxi >= 0 && ntxi < a.ntx && ntyi >= 0 && ntyi < a.nty) {
             ntile = (unsigned)(ntyi * a.ntx + ntxi);
-            own = activate_claim(a.q, ntile);
+            own = activate_claim_nopend(a.q, ntile);
           }
         }
         unsigned ownmask = __ballot_sync(FULL, own);
         int keep = (ownmask && next_tile < 0) ? __ffs(ownmask) - 1 : -1;
-        if (own && lane != keep) ring_push(a.q, ntile);
+        // the kept continuation inherits this tile's pending count (no +1 here,
+        // no -1 at this tile's finish); a pushed tile counts before its push
+        if (own && lane != keep) {
+          atomicAdd(a.q.pending, 1u);
+          ring_push(a.q, ntile);
+        }
         if (keep >= 0) next_tile = __shfl_sync(FULL, (int)ntile, keep);
       }
       int done = 0;
       if (l0) {
         unsigned old = atomicCAS(&a.q.state[t], ST_R, 0u);
         if (old == ST_R) {
-          atomicSub(a.q.pending, 1u);  // (see the register engine: no fence needed)
+          if (next_tile < 0) atomicSub(a.q.pending, 1u);  // (else passed on, above)  // (see the register engine: no fence needed)
           done = 1;
         } else {
           state_take(&a.q.state[t]);  // consume the request (acquire)
