@@ -140,7 +140,20 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
   cudaStream_t st = (cudaStream_t)stream;
   Carver c(workspace);
   ReconWs w = carve_recon(c, W, H);
-  if (dtype == IWPP_F32) {  // int32 engine on order-preserving ints, then back
+  // f32: the 32-bit register engine orders the float bits as it stages its
+  // boxes (no conversion passes); other engine choices run the int32 engine
+  // on converted copies
+  bool f32_fused = false;
+  if (dtype == IWPP_F32) {
+    recon::EngineOpts probe;
+    if (opts) {
+      probe.qcap = opts->queue_capacity;
+      probe.sweeps_set = opts->tile_sweeps >= 0;
+      probe.engine = opts->engine;
+    }
+    f32_fused = (!opts || (opts->sweeps <= 0 && !opts->slab_rows)) && recon::f32_in_engine(probe);
+  }
+  if (dtype == IWPP_F32 && !f32_fused) {  // int32 engine on order-preserving ints, then back
     const size_t n = (size_t)W * H;
     void *Io = c.take<int32_t>(n);
     if ((rc = recon::f32_to_ord(J, J, n, st))) return rc;

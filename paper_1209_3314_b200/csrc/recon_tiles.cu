@@ -147,7 +147,7 @@ constexpr int kBinCtasPerSm = 4;
 #endif
 constexpr unsigned kPopMaxSleepNs = IWPP_POP_MAX_SLEEP_NS;
 #ifndef IWPP_PENDING_POLL_NS
-#define IWPP_PENDING_POLL_NS 1024
+#define IWPP_PENDING_POLL_NS 32
 #endif
 constexpr unsigned kPendingPollNs = IWPP_PENDING_POLL_NS;
 
@@ -197,6 +197,11 @@ __device__ __forceinline__ unsigned state_take(unsigned *p) {
 #if IWPP_STATE_ACQ
   unsigned old;
   asm volatile("atom.acquire.gpu.exch.b32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(ST_R) : "memory");
+  // Consume the returned value here: with the result unused, ptxas emits the
+  // exchange with no destination and nothing waits for it, so a TMA box load
+  // (async proxy) issued next could read a border published before the
+  // request this exchange consumes from before it became visible.
+  if (old > (ST_Q | ST_R | ST_V)) __trap();
   return old;
 #else
   const unsigned old = atomicExch(p, ST_R);
@@ -1267,10 +1272,11 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
           for (int k = 0; k < 8; k++) ws.ob[sel][k] = j[k];
         obl = jl;
         obr = jr;
-        // publish the tile before any neighbour is (re)queued.  With no
-        // neighbour to activate no fence is needed: a neighbour that this
-        // border cannot raise never needs to see it (need_h was false)
-        if (dirs) fence_acq_rel();
+        // publish the tile before any neighbour is (re)queued, and before
+        // this tile's finish: the finish CAS is what lets a later activation
+        // pop the tile again, and its next owner must load these values (a
+        // stale interior could be recomputed lower and overwrite them)
+        fence_acq_rel();
         __syncwarp();
         bool own = false;
         unsigned ntile = 0;
@@ -1357,7 +1363,15 @@ struct alignas(128) Box32Smem {
 };
 
 // stage the J (and I) box of tile (x0, y0); cells outside the image hold LO
-template <typename T>
+// f32 as order-preserving int32 (the same map as recon_sweeps.cu's
+// f32_to_ord: -0.0 -> +0.0, negative floats flip their magnitude bits)
+__device__ __forceinline__ int f32_ord(int b) {
+  if (b == INT_MIN) b = 0;
+  return b >= 0 ? b : (b ^ 0x7fffffff);
+}
+__device__ __forceinline__ int f32_unord(int v) { return v >= 0 ? v : (v ^ 0x7fffffff); }
+
+template <typename T, bool ORD = false>
 __device__ __forceinline__ void box32_stage(const EngineArgs &a, const CUtensorMap *maps, int use_tma,
                                             Box32Smem<T> &b, int x0, int y0, bool withI,
                                             unsigned &phase, int lane) {
@@ -1374,6 +1388,14 @@ __device__ __forceinline__ void box32_stage(const EngineArgs &a, const CUtensorM
     }
     mbar_wait(&b.bar, phase);
     phase ^= 1u;
+    if (ORD) {  // f32 bit patterns -> ordered ints, in place
+      int *bj = reinterpret_cast<int *>(&b.J[0][0]), *bi = reinterpret_cast<int *>(&b.I[0][0]);
+      for (int i = lane; i < (TS + 2) * BW; i += 32) {
+        bj[i] = f32_ord(bj[i]);
+        if (withI) bi[i] = f32_ord(bi[i]);
+      }
+      __syncwarp();
+    }
     if (edge && Elem<T>::lo != 0) {  // TMA fills with 0: patch the sentinel in
       for (int i = lane; i < (TS + 2) * BW; i += 32) {
         const int r = i / BW, c = i - r * BW, gx = x0 - OFF + c, gy = y0 - 1 + r;
@@ -1389,8 +1411,13 @@ __device__ __forceinline__ void box32_stage(const EngineArgs &a, const CUtensorM
       const int r = i / BW, c = i - r * BW, gx = x0 - OFF + c, gy = y0 - 1 + r;
       const bool in = gx >= 0 && gx < a.W && gy >= 0 && gy < a.H;
       const size_t g = (size_t)gy * a.W + gx;
-      b.J[r][c] = in ? ld_cg(J + g) : Elem<T>::lo;
-      if (withI) b.I[r][c] = in ? __ldg(I + g) : Elem<T>::lo;
+      if (ORD) {
+        b.J[r][c] = in ? (T)f32_ord((int)ld_cg(J + g)) : Elem<T>::lo;
+        if (withI) b.I[r][c] = in ? (T)f32_ord((int)__ldg(I + g)) : Elem<T>::lo;
+      } else {
+        b.J[r][c] = in ? ld_cg(J + g) : Elem<T>::lo;
+        if (withI) b.I[r][c] = in ? __ldg(I + g) : Elem<T>::lo;
+      }
     }
   }
   __syncwarp();
@@ -1468,7 +1495,7 @@ __device__ __forceinline__ int reg32_fixpoint(int *j, const int *m, const Box32S
   return steps;
 }
 
-template <typename T, int CONN>
+template <typename T, int CONN, bool ORD = false>
 __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
     tile_engine_reg32_kernel(EngineArgs a, unsigned long long *counters,
                              const __grid_constant__ BoxMaps maps, int use_tma, int fused_init) {
@@ -1507,7 +1534,7 @@ __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
     const int x0 = tx * TS, y0 = ty * TS;
     long long c_load = pclock(l0);
     if (kPhases && l0) ph[0] += c_load - c_pop;
-    box32_stage<T>(a, tmaps, use_tma, b, x0, y0, true, phase, lane);
+    box32_stage<T, ORD>(a, tmaps, use_tma, b, x0, y0, true, phase, lane);
     int j[TS], m[TS];
 #pragma unroll
     for (int k = 0; k < TS; k++) {
@@ -1537,13 +1564,13 @@ __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
               uint4 w;
               T *e = reinterpret_cast<T *>(&w);
 #pragma unroll
-              for (int q = 0; q < E; q++) e[q] = (T)j[v * E + q];
+              for (int q = 0; q < E; q++) e[q] = (T)(ORD ? f32_unord(j[v * E + q]) : j[v * E + q]);
               reinterpret_cast<uint4 *>(p)[v] = w;
             }
           } else {
 #pragma unroll
             for (int k = 0; k < TS; k++)
-              if (x0 + k < a.W) p[k] = (T)j[k];
+              if (x0 + k < a.W) p[k] = (T)(ORD ? f32_unord(j[k]) : j[k]);
           }
         }
         if (a.dirty && l0) a.dirty[ty] = 1;
@@ -1600,7 +1627,7 @@ __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
         if (l0 || l31)
 #pragma unroll
           for (int k = 0; k < TS; k++) b.J[ob_row][OFF + k] = (T)j[k];
-        if (dirs) fence_acq_rel();  // publish before any neighbour is (re)queued
+        fence_acq_rel();  // publish before any neighbour is (re)queued and before the finish
         __syncwarp();
         bool own = false;
         unsigned ntile = 0;
@@ -1634,7 +1661,7 @@ __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
       done = __shfl_sync(FULL, done, 0);
       if (kPhases && l0) ph[5] += clock64() - c_st;
       if (done) break;
-      box32_stage<T>(a, tmaps, use_tma, b, x0, y0, false, phase, lane);  // J halo (+ our rows)
+      box32_stage<T, ORD>(a, tmaps, use_tma, b, x0, y0, false, phase, lane);  // J halo (+ our rows)
       rerun = true;
     }
   }
@@ -1873,10 +1900,11 @@ __global__ void __launch_bounds__(kCtaThreads)
         oa1 = a1;
         ob0 = b0;
         ob1 = b1;
-        // publish the tile before any neighbour is (re)queued.  With no
-        // neighbour to activate no fence is needed: a neighbour that this
-        // border cannot raise never needs to see it (need_h was false)
-        if (dirs) fence_acq_rel();
+        // publish the tile before any neighbour is (re)queued, and before
+        // this tile's finish: the finish CAS is what lets a later activation
+        // pop the tile again, and its next owner must load these values (a
+        // stale interior could be recomputed lower and overwrite them)
+        fence_acq_rel();
         __syncwarp();
         bool own = false;
         unsigned ntile = 0;
@@ -2191,16 +2219,33 @@ static bool use_bin_engine(bool binary, const EngineOpts &o) {
          o.sweeps_set == 0;
 }
 
+bool f32_in_engine(const EngineOpts &o) { return use_reg_engine<int32_t>(o); }
+
 int tile_side(int dtype, const EngineOpts &o) {
   return use_bin_engine(dtype == IWPP_BIN, o) ? TSB : TS;
 }
 
 
 // the 16 / 32-bit register engine (no u8 instantiation)
+template <typename T, int CONN, bool ORD>
+static int launch_reg32_kernel(const EngineArgs &a, unsigned long long *counters, const TileQueue &q,
+                               const void *J, const void *I, int W, int H, const EngineOpts &o,
+                               unsigned max_b, int fused_init, cudaStream_t st);
+
 template <typename T, int CONN>
 static int launch_reg32(const EngineArgs &a, unsigned long long *counters, const TileQueue &q,
                         const void *J, const void *I, int W, int H, const EngineOpts &o,
-                        unsigned max_b, int fused_init, cudaStream_t st) {
+                        unsigned max_b, int fused_init, cudaStream_t st, bool ord = false) {
+  if constexpr (std::is_same<T, int32_t>::value) {
+    if (ord) return launch_reg32_kernel<T, CONN, true>(a, counters, q, J, I, W, H, o, max_b, fused_init, st);
+  }
+  return launch_reg32_kernel<T, CONN, false>(a, counters, q, J, I, W, H, o, max_b, fused_init, st);
+}
+
+template <typename T, int CONN, bool ORD>
+static int launch_reg32_kernel(const EngineArgs &a, unsigned long long *counters, const TileQueue &q,
+                               const void *J, const void *I, int W, int H, const EngineOpts &o,
+                               unsigned max_b, int fused_init, cudaStream_t st) {
   if constexpr (sizeof(T) == 1) {
     return set_error(IWPP_E_CONTRACT, "no 8-bit register32 engine");
   } else {
@@ -2208,7 +2253,7 @@ static int launch_reg32(const EngineArgs &a, unsigned long long *counters, const
     if (r32_blocks == 0) {
       int per_sm = 0;
       IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, tile_engine_reg32_kernel<T, CONN>, kCtaThreads, 0));
+          &per_sm, tile_engine_reg32_kernel<T, CONN, ORD>, kCtaThreads, 0));
       r32_blocks = device_sm_count() * (per_sm < 1 ? 1 : per_sm);
     }
     int rb = r32_blocks;
@@ -2221,10 +2266,10 @@ static int launch_reg32(const EngineArgs &a, unsigned long long *counters, const
     if (fused_init) {
       int fi = 1;
       void *args[] = {const_cast<EngineArgs *>(&a), &counters, &maps, &use_tma, &fi};
-      IWPP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)tile_engine_reg32_kernel<T, CONN>,
+      IWPP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)tile_engine_reg32_kernel<T, CONN, ORD>,
                                                 dim3(rb), dim3(kCtaThreads), args, 0, st));
     } else {
-      tile_engine_reg32_kernel<T, CONN><<<rb, kCtaThreads, 0, st>>>(a, counters, maps, use_tma, 0);
+      tile_engine_reg32_kernel<T, CONN, ORD><<<rb, kCtaThreads, 0, st>>>(a, counters, maps, use_tma, 0);
     }
     IWPP_CUDA_TRY(cudaGetLastError());
     return IWPP_OK;
@@ -2234,7 +2279,7 @@ static int launch_reg32(const EngineArgs &a, unsigned long long *counters, const
 template <typename T, int CONN>
 static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
                          unsigned long long *counters, const EngineOpts &o, cudaStream_t st,
-                         bool binary = false) {
+                         bool binary = false, bool f32 = false) {
   const int ts = use_bin_engine(binary, o) ? TSB : TS;
   int ntx = (W + ts - 1) / ts, nty = (H + ts - 1) / ts;
   unsigned ntiles = (unsigned)ntx * nty;
@@ -2295,7 +2340,7 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
     if ((unsigned)bb > max_b) bb = (int)max_b;
     tile_engine_bin_kernel<CONN><<<bb, kCtaThreads, 0, st>>>(a, counters);
   } else if (sizeof(T) > 1 && use_reg_engine<T>(o)) {  // 16 / 32-bit register engine
-    const int rc = launch_reg32<T, CONN>(a, counters, q, J, I, W, H, o, max_b, fused_init, st);
+    const int rc = launch_reg32<T, CONN>(a, counters, q, J, I, W, H, o, max_b, fused_init, st, f32);
     if (rc) return rc;
   } else if (use_reg_engine<T>(o)) {
     static int reg_blocks = 0;
@@ -2344,6 +2389,10 @@ int run_tile_engine(void *J, const void *I, int W, int H, int dtype, int conn, T
       DISPATCH(uint16_t);
     case IWPP_I32:
       DISPATCH(int32_t);
+    case IWPP_F32:  // f32 bit patterns, ordered inside the 32-bit register engine
+      if (!f32_in_engine(o)) break;
+      return conn == 8 ? launch_engine<int32_t, 8>(J, I, W, H, q, counters, o, st, false, true)
+                       : launch_engine<int32_t, 4>(J, I, W, H, q, counters, o, st, false, true);
   }
 #undef DISPATCH
   return set_error(IWPP_E_CONTRACT, "unsupported dtype %d", dtype);

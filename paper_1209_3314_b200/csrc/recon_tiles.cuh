@@ -83,6 +83,9 @@ enum { INIT_FULL = 0, INIT_CONTINUE = 1 };
 
 size_t tile_queue_bytes(unsigned ntiles);
 TileQueue carve_tile_queue(Carver &c, unsigned ntiles);
+// f32 images can run on their float bits directly (the register engine
+// orders them as it stages its boxes) under these options
+bool f32_in_engine(const EngineOpts &o);
 int run_tile_engine(void *J, const void *I, int W, int H, int dtype, int conn, TileQueue q,
                     unsigned long long *counters, const EngineOpts &o, cudaStream_t st);
 // side of the square tiles the engine run_tile_engine picks for (dtype, o)
