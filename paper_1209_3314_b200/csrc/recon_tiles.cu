@@ -147,7 +147,7 @@ constexpr int kBinCtasPerSm = 4;
 #endif
 constexpr unsigned kPopMaxSleepNs = IWPP_POP_MAX_SLEEP_NS;
 #ifndef IWPP_PENDING_POLL_NS
-#define IWPP_PENDING_POLL_NS 32
+#define IWPP_PENDING_POLL_NS 1024
 #endif
 constexpr unsigned kPendingPollNs = IWPP_PENDING_POLL_NS;
 

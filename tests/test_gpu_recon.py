@@ -278,6 +278,31 @@ def test_host_pipeline_4k_auto(gw):
     assert np.array_equal(gw.reconstruct(J, I, 8), want)
 
 
+@pytest.mark.parametrize("conn", [8, 4])
+def test_host_pipeline_repeated_runs_agree(gw, conn):
+    """Race guard: the pipelined host path runs the engine once per slab
+    over growing heights, with tiles re-popped across runs; 24 calls on
+    the same input must all give the oracle's image (a lost update between
+    a tile's finish and its next owner showed up here as 1-3 wrong pixels
+    in ~15% of calls before it was fixed)."""
+    J, I = oracle.gray_pair(4096, 0, h=40)
+    want = oracle.recon_fh(J, I, conn)
+    bad = sum(not np.array_equal(gw.reconstruct(J, I, conn), want) for _ in range(24))
+    assert bad == 0
+
+
+@pytest.mark.parametrize("kind", ["i32", "u16"])
+def test_device_repeated_runs_agree_wide(gw, kind):
+    """The same guard for the 32-bit register engine (device-resident)."""
+    import torch
+    dt = np.int32 if kind == "i32" else np.uint16
+    J, I = oracle.gray_pair(2048, 5, h=(1 << 27) if kind == "i32" else 5000, dtype=dt)
+    want = oracle.recon_fh(J, I, 8)
+    dJ, dI = torch.from_numpy(J).cuda(), torch.from_numpy(I).cuda()
+    bad = sum(not np.array_equal(gw.reconstruct(dJ, dI, 8).cpu().numpy(), want) for _ in range(16))
+    assert bad == 0
+
+
 def test_host_pipeline_contract_in_late_slab(gw):
     J, I = oracle.gray_pair((600, 128), 4, h=40)
     J[590, 100] = 255
