@@ -173,15 +173,16 @@ __device__ __forceinline__ int ring_pop(const TileQueue &q) {
 // Tile state bits: Q = queued, or re-run requested while running; R =
 // running; V = never processed (set only by the initial fill).
 //   activate : old = atomicOr(Q); old == 0 (idle) -> we own the push
-//   pop      : old = atomicExch(R) + fence (acquire: sees every border write
+//   pop      : old = acquire exchange to R (sees every border write
 //              made before a request that found Q already set)
-//   finish   : CAS(R -> 0); failure means Q was set meanwhile -> re-run
+//   finish   : CAS(R -> 0), after a changed tile fenced its stores (the
+//              next owner loads them); failure means Q was set meanwhile -> re-run
 // Returns true when the caller now owns an idle tile's activation (it must
 // either push it or process it itself); pending already counts it.
 // Take a tile (state <- R) with acquire semantics: the borders published
 // before any request this consumes are visible afterwards.  An acquire RMW
-// (ATOM + L1 invalidate) rather than RMW + fence.acq_rel, whose MEMBAR would
-// also wait for this warp's own earlier, unfenced stores.
+// (ATOM + L1 invalidate) rather than RMW + fence.acq_rel.  (A changed tile
+// fences its own stores before its finish, so nothing unfenced is pending.)
 #ifndef IWPP_STATE_ACQ
 #define IWPP_STATE_ACQ 1
 #endif
@@ -1929,7 +1930,7 @@ __global__ void __launch_bounds__(kCtaThreads)
       if (l0) {
         unsigned old = atomicCAS(&a.q.state[t], ST_R, 0u);
         if (old == ST_R) {
-          if (next_tile < 0) atomicSub(a.q.pending, 1u);  // (else passed on, above)  // (see the register engine: no fence needed)
+          if (next_tile < 0) atomicSub(a.q.pending, 1u);  // (else passed on, above)
           done = 1;
         } else {
           state_take(&a.q.state[t]);  // consume the request (acquire)
