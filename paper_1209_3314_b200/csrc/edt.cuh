@@ -7,8 +7,14 @@ namespace edt {
 
 constexpr uint32_t INF32 = 0xFFFFFFFFu;
 constexpr uint32_t SEED_STAMP = 0xFFFFFFFEu;
-constexpr int kRoundThreads = 512;
-constexpr int kRoundBlocksPerSm = 2;
+#ifndef IWPP_EDT_ROUND_THREADS
+#define IWPP_EDT_ROUND_THREADS 256
+#endif
+#ifndef IWPP_EDT_ROUND_BLOCKS
+#define IWPP_EDT_ROUND_BLOCKS 4
+#endif
+constexpr int kRoundThreads = IWPP_EDT_ROUND_THREADS;
+constexpr int kRoundBlocksPerSm = IWPP_EDT_ROUND_BLOCKS;
 constexpr int kEdtBq = 6144;  // per-block next-frontier buffer (shared memory, 24 KB)
 
 enum { EC_ROUNDS = 0, EC_VISITS, EC_NINF, EC_LIMIT, EC_FINAL, EC_BAD, EC_RANGE, EC_LASTCHG, EC_N = 8 };
