@@ -206,6 +206,8 @@ def _read_pgm_device(path: str, device) -> Image2D:
     dev = torch.device(device)
     if dev.type != "cuda":
         raise ContractViolation(f"device reads need a CUDA device, got {device!r}")
+    if not os.path.exists(path):  # a missing file is a contract error, device or not
+        raise FileNotFoundError(path)
     L = _lib.lib()
     pinned = _pinned_file(path)
     hb = pinned.numpy()
