@@ -175,7 +175,7 @@ int iwpp_edt_propagate(int64_t *vr, int64_t W, int64_t H, int conn,
                        const int64_t *seeds, int64_t n_seeds, void *workspace,
                        size_t workspace_bytes, int64_t max_rounds,
                        iwpp_stats *stats, void *stream);
-/* Engine selection for tests/diagnostics (process-wide, not thread-safe):
+/* Engine selection for tests/diagnostics (per host thread):
  * 0 = auto (64-bit keys on the raster-frontier engine; range-checked with a
  * CAS re-run when W, H exceed the 32-bit d^2 range), 1 = force the 32-bit-source CAS
  * engine, 2 = force range-checked keys, 3 = force the per-round
@@ -188,6 +188,23 @@ int iwpp_edt_set_engine(int mode);
  * Returns IWPP_E_NO_BACKGROUND if any vr == -1.  d2 may be NULL. */
 int iwpp_edt_finalize(const int64_t *vr, int64_t W, int64_t H, float *dist,
                       int64_t *d2, void *workspace, void *stream);
+/* init_packed / edt_init (edt.py:187-202; K.edt_assign K.339-347,
+ * K.edt_contour_seeds K.350-373): vr (device int64 (H,W), may be NULL) =
+ * own packed index on background, -1 on foreground; seeds (device int64,
+ * capacity W*H, may be NULL) = background cells with an in-bounds foreground
+ * neighbour, in raster order; *n_seeds_host (may be NULL; syncs) = count. */
+size_t iwpp_edt_init_workspace_bytes(int64_t W, int64_t H);
+int iwpp_edt_init(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *vr, int64_t *seeds,
+                  int64_t *n_seeds_host, void *workspace, size_t workspace_bytes, void *stream);
+/* edt_exact_bruteforce (edt.py:313-323, oracles.bruteforce_sqdist
+ * oracles.py:57-73): exact squared distance to the nearest background cell
+ * (separable exact transform, integer arithmetic: the brute-force minimum).
+ * d2 (device int64, may be NULL: then the workspace holds it), dist (device
+ * f32 = f32(sqrt(f64(d2))), may be NULL).  IWPP_E_NO_BACKGROUND if the mask
+ * has no background (syncs). */
+size_t iwpp_edt_exact_workspace_bytes(int64_t W, int64_t H);
+int iwpp_edt_exact(const uint8_t *mask, int64_t W, int64_t H, int64_t *d2, float *dist,
+                   void *workspace, size_t workspace_bytes, void *stream);
 /* ---- EDT on one horizontal slab of a multi-GPU run ----
  * The rank owns rows [y0, y0+h) of an H-row image.  The synchronous rule
  * needs one exchange per round (tiles.py:10-15, edt_bp_sweep K.493-522):

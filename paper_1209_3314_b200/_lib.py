@@ -37,7 +37,8 @@ EXPORTS = (
     "iwpp_event_create", "iwpp_event_destroy", "iwpp_event_record", "iwpp_event_elapsed_ms",
     "iwpp_edt_slab_workspace_bytes", "iwpp_edt_slab_init", "iwpp_edt_slab_round",
     "iwpp_edt_slab_finalize", "iwpp_pgm_decode", "iwpp_pgm_encode", "iwpp_gen_marker",
-    "iwpp_quantize_u8",
+    "iwpp_quantize_u8", "iwpp_edt_init_workspace_bytes", "iwpp_edt_init",
+    "iwpp_edt_exact_workspace_bytes", "iwpp_edt_exact",
 )
 
 
@@ -109,6 +110,10 @@ def load_library(path: str = LIB_PATH):
             "iwpp_pgm_encode": ([P, P, I64, I, P], I),
             "iwpp_gen_marker": ([P, P, I64, I, ctypes.c_double, P], I),
             "iwpp_quantize_u8": ([P, P, I64, P], I),
+            "iwpp_edt_init_workspace_bytes": ([I64, I64], SZ),
+            "iwpp_edt_init": ([P, I64, I64, I, P, P, ctypes.POINTER(I64), P, SZ, P], I),
+            "iwpp_edt_exact_workspace_bytes": ([I64, I64], SZ),
+            "iwpp_edt_exact": ([P, I64, I64, P, P, P, SZ, P], I),
         }
         for name, (args, res) in proto.items():
             fn = getattr(L, name)
@@ -146,21 +151,27 @@ def check(rc: int, what: str = ""):
     raise RuntimeError(f"iwpp error {rc}: {msg}")
 
 
-# -- workspace cache (one growable device buffer per device) ---------------
+# -- workspace cache: one growable device buffer per (device, stream) ------
 _ws = {}
+_ws_lock = threading.Lock()
 
 
 def workspace(nbytes: int):
-    """A device byte buffer of at least nbytes on the current device.  The
-    buffer is reused by later calls on the same stream order; callers that
-    run concurrently on several streams must pass their own."""
+    """A device byte buffer of at least nbytes on the current device, private
+    to torch's current stream there.  Calls on one stream are ordered, so they
+    share it safely; calls on different streams (e.g. from several host
+    threads, SURVEY 8(b) "Threading") get different buffers.  A buffer that
+    is replaced by a larger one is released to torch's caching allocator,
+    which reuses it only in that stream's order."""
     torch = _torch()
     dev = torch.cuda.current_device()
-    buf = _ws.get(dev)
-    if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=f"cuda:{dev}")
-        _ws[dev] = buf
-    return buf
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    with _ws_lock:
+        buf = _ws.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=f"cuda:{dev}")
+            _ws[key] = buf
+        return buf
 
 
 def stream_ptr():
@@ -197,3 +208,22 @@ def ptr(a):
     if isinstance(a, np.ndarray):
         return ctypes.c_void_p(a.ctypes.data)
     return ctypes.c_void_p(a.data_ptr())
+
+
+def device_of(*arrays):
+    """``with device_of(t, ...)``: run the call on the device of the CUDA
+    tensors among ``arrays`` (all must share it), so kernels launch on the
+    device that owns the pointers and pick that device's workspace and
+    current stream.  Host arrays impose nothing; with no tensor at all the
+    current device is used."""
+    import contextlib
+    torch = _torch()
+    devs = {a.device for a in arrays if isinstance(a, torch.Tensor)}
+    if len(devs) > 1:
+        raise ContractViolation(f"arrays live on different devices: {sorted(map(str, devs))}")
+    if not devs:
+        return contextlib.nullcontext()
+    (d,) = devs
+    if d.type != "cuda":
+        raise ContractViolation(f"tensor on {d}; the B200 engines need CUDA tensors or numpy arrays")
+    return torch.cuda.device(d)

@@ -213,7 +213,9 @@ size_t iwpp_recon_host_workspace_bytes(int64_t W, int64_t H, int dtype, int conn
   size_t nty = (size_t)((H + recon::TS - 1) / recon::TS);
   // the device call runs on the copies (f32 is converted in place first)
   const size_t inner = iwpp_recon_workspace_bytes(W, H, dtype == IWPP_F32 ? IWPP_I32 : dtype, conn);
-  return 2 * img + align_up(nty, 256) + inner + 512;
+  // + one violation counter of its own (the engine resets its counter block
+  // at every pipelined run, so check_le must not count into CNT_VIOL there)
+  return 2 * img + align_up(nty, 256) + 256 + inner + 512;
 }
 
 }  // extern "C"
@@ -350,7 +352,7 @@ struct Trace {
 // compute, so the call costs ~ max(H2D, D2H) + one slab's compute.
 static int recon_host_pipelined(char *out, const char *marker, const char *mask, int64_t W,
                                 int64_t H, int dtype, int conn, const std::vector<int64_t> &bnd, char *dJ,
-                                char *dI, uint8_t *dirty, char *rest,
+                                char *dI, uint8_t *dirty, unsigned long long *vctr, char *rest,
                                 const iwpp_recon_opts *opts, iwpp_stats *stats,
                                 cudaStream_t st) {
   HostPipe *hp;
@@ -388,7 +390,7 @@ static int recon_host_pipelined(char *out, const char *marker, const char *mask,
     IWPP_CUDA_TRY(cudaEventRecord(hp->in[k], hp->h2d));
     tr.mark(hp->h2d, "h2d done", k);
   }
-  IWPP_CUDA_TRY(cudaMemsetAsync(&w.counters[recon::CNT_VIOL], 0, sizeof(unsigned long long), st));
+  IWPP_CUDA_TRY(cudaMemsetAsync(vctr, 0, sizeof(unsigned long long), st));
   IWPP_CUDA_TRY(cudaMemsetAsync(dirty, 0, (size_t)nty, st));
   auto copy_back = [&](int64_t r0, int64_t r1) -> int {  // rows [r0, r1) -> host (d2h)
     size_t off = (size_t)r0 * row_bytes;
@@ -401,8 +403,7 @@ static int recon_host_pipelined(char *out, const char *marker, const char *mask,
     size_t off = (size_t)y0 * row_bytes;
     IWPP_CUDA_TRY(cudaStreamWaitEvent(st, hp->in[k], 0));
     tr.mark(st, "compute begin", k);
-    if ((rc = recon::check_le(dJ + off, dI + off, (size_t)(y1 - y0) * W, dtype,
-                              &w.counters[recon::CNT_VIOL], st)))
+    if ((rc = recon::check_le(dJ + off, dI + off, (size_t)(y1 - y0) * W, dtype, vctr, st)))
       return rc;
     // Rows [0, y1): the slab's tiles (first visits) plus the tile row above
     // the cut at y0 (re-visited with the slab's rows as its halo); a raise
@@ -431,8 +432,7 @@ static int recon_host_pipelined(char *out, const char *marker, const char *mask,
   std::vector<uint8_t> flags((size_t)nty);
   unsigned long long viol = 0;
   IWPP_CUDA_TRY(cudaMemcpyAsync(flags.data(), dirty, (size_t)nty, cudaMemcpyDeviceToHost, st));
-  IWPP_CUDA_TRY(cudaMemcpyAsync(&viol, &w.counters[recon::CNT_VIOL], sizeof viol,
-                                cudaMemcpyDeviceToHost, st));
+  IWPP_CUDA_TRY(cudaMemcpyAsync(&viol, vctr, sizeof viol, cudaMemcpyDeviceToHost, st));
   IWPP_CUDA_TRY(cudaStreamSynchronize(st));
   tr.mark(st, "flags read", 0);
   for (int64_t t = 0; t < nty;) {
@@ -473,6 +473,7 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   char *dJ = c.take<char>(nb);
   char *dI = c.take<char>(nb);
   uint8_t *dirty = c.take<uint8_t>((size_t)((H + recon::TS - 1) / recon::TS));
+  unsigned long long *vctr = c.take<unsigned long long>(1);
   char *rest = c.base + align_up(c.off, 256);
   size_t rest_bytes = workspace_bytes - align_up(c.off, 256);
   std::vector<int64_t> bnd;
@@ -482,7 +483,7 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
       host_slabs(W, H, es, opts ? opts->pipeline_rows : 0, bnd);
   if (pipelined)
     return recon_host_pipelined((char *)out, (const char *)marker, (const char *)mask, W, H, dtype,
-                                conn, bnd, dJ, dI, dirty, rest, opts, stats, st);
+                                conn, bnd, dJ, dI, dirty, vctr, rest, opts, stats, st);
   IWPP_CUDA_TRY(cudaMemcpyAsync(dJ, marker, nb, cudaMemcpyHostToDevice, st));
   IWPP_CUDA_TRY(cudaMemcpyAsync(dI, mask, nb, cudaMemcpyHostToDevice, st));
   // contract check (recon.py:60) fused into the same stream

@@ -733,7 +733,7 @@ __global__ void edt_finalize_key_kernel(EdtState s, int W, int H, int64_t *vr, f
 
 // ---- host side -------------------------------------------------------------
 
-int g_engine_override = ENGINE_AUTO;
+thread_local int g_engine_override = ENGINE_AUTO;  // per host thread: diagnostics only
 
 // One layout for both engines: the key engine's 16 B/px key array doubles
 // as the CAS engine's two source buffers + stamps (12 B/px), so a key run

@@ -62,7 +62,7 @@ enum {
   ENGINE_RASTER = 7       // raster-frontier engine (bitmap + compaction, no returned atomics)
 };
 
-extern int g_engine_override;
+extern thread_local int g_engine_override;
 // The key engine needs every squared distance to fit 32 bits.
 inline bool key_mode_ok(int64_t W, int64_t H) {
   return (uint64_t)(W - 1) * (W - 1) + (uint64_t)(H - 1) * (H - 1) < (1ull << 32);

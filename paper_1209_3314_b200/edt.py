@@ -60,11 +60,12 @@ class VoronoiMap:
         L = _lib.lib()
         torch = _lib._torch()
         host = not self.on_device
-        vr = torch.from_numpy(np.ascontiguousarray(self.vr)).cuda() if host else self.vr.contiguous()
-        d2 = torch.empty_like(vr)
-        ws = _lib.workspace(256)
-        rc = L.iwpp_edt_finalize(_lib.ptr(vr), self.width, self.height, None, _lib.ptr(d2),
-                                 _lib.ptr(ws), _lib.stream_ptr())
+        with _lib.device_of(self.vr):
+            vr = torch.from_numpy(np.ascontiguousarray(self.vr)).cuda() if host else self.vr.contiguous()
+            d2 = torch.empty_like(vr)
+            ws = _lib.workspace(256)
+            rc = L.iwpp_edt_finalize(_lib.ptr(vr), self.width, self.height, None, _lib.ptr(d2),
+                                     _lib.ptr(ws), _lib.stream_ptr())
         if rc not in (_lib.IWPP_OK, _lib.IWPP_E_NO_BACKGROUND):
             _lib.check(rc, "squared_distances")
         return d2.cpu().numpy() if host else d2
@@ -98,6 +99,14 @@ def _edt_arrays(mask, conn: int, max_rounds: int = -1, stats: dict | None = None
     L = _lib.lib()
     H, W = mask.shape
     st = _lib.Stats()
+    with _lib.device_of(mask):
+        vr, dist, rc = _edt_arrays_on(L, mask, W, H, conn, max_rounds, st, want_dist)
+    if stats is not None:
+        stats.update(st.as_dict())
+    return vr, dist, rc
+
+
+def _edt_arrays_on(L, mask, W, H, conn, max_rounds, st, want_dist):
     if is_device_array(mask):
         torch = _lib._torch()
         m = mask.contiguous()
@@ -115,8 +124,6 @@ def _edt_arrays(mask, conn: int, max_rounds: int = -1, stats: dict | None = None
         rc = L.iwpp_edt_host(_lib.ptr(m), W, H, conn, _lib.ptr(vr),
                              _lib.ptr(dist) if dist is not None else None, _lib.ptr(ws),
                              ws.numel(), max_rounds, _lib.ctypes.byref(st), _lib.stream_ptr())
-    if stats is not None:
-        stats.update(st.as_dict())
     return vr, dist, rc
 
 
@@ -138,23 +145,25 @@ def edt(mask: Image2D, se: StructuringElement = SE8, mode: str = "sequential",
 
 
 def init_packed(mask: Image2D, se: StructuringElement = SE8):
-    """edt.py:187-196: (VoronoiMap, packed contour seeds in raster order)."""
+    """edt.py:187-196: (VoronoiMap, packed contour seeds in raster order).
+    Device kernels (``iwpp_edt_init``): K.edt_assign + K.edt_contour_seeds."""
     _require_binary(mask)
+    L = _lib.lib()
     torch = _lib._torch()
     host = not mask.on_device
-    m = torch.from_numpy(np.ascontiguousarray(mask.data)).cuda() if host else mask.data
-    bg = m == 0
-    H, W = m.shape
-    idx = torch.arange(H * W, device=m.device, dtype=torch.int64).view(H, W)
-    vr = torch.where(bg, idx, torch.full_like(idx, INF))
-    # contour seeds: background cells with a foreground neighbour in bounds
-    fg = torch.nn.functional.pad((~bg).to(torch.uint8), (1, 1, 1, 1))
-    near = torch.zeros_like(bg)
-    for dx, dy in se.offsets:
-        near |= fg[1 + dy:1 + dy + H, 1 + dx:1 + dx + W].bool()
-    seeds = idx[bg & near]  # row-major nonzero order == raster order
-    if host:
-        return VoronoiMap(W, H, vr.cpu().numpy()), seeds.cpu().numpy()
+    H, W = mask.height, mask.width
+    with _lib.device_of(mask.data):
+        m = torch.from_numpy(np.ascontiguousarray(mask.data)).cuda() if host else mask.data.contiguous()
+        vr = torch.empty((H, W), dtype=torch.int64, device=m.device)
+        seeds = torch.empty(H * W, dtype=torch.int64, device=m.device)
+        n = _lib.ctypes.c_int64(0)
+        ws = _lib.workspace(L.iwpp_edt_init_workspace_bytes(W, H))
+        _lib.check(L.iwpp_edt_init(_lib.ptr(m), W, H, se.connectivity, _lib.ptr(vr), _lib.ptr(seeds),
+                                   _lib.ctypes.byref(n), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
+                   "edt_init")
+        seeds = seeds[:n.value]
+        if host:
+            return VoronoiMap(W, H, vr.cpu().numpy()), seeds.cpu().numpy()
     return VoronoiMap(W, H, vr), seeds
 
 
@@ -187,24 +196,24 @@ def edt_propagate(vmap: VoronoiMap, seeds, se: StructuringElement = SE8,
     W, H = vmap.width, vmap.height
     packed = _norm_seeds(seeds, W)
     host = not vmap.on_device
-    vr = torch.from_numpy(np.ascontiguousarray(vmap.vr)).cuda() if host else vmap.vr
-    dev = vr.device
-    sd = torch.as_tensor(packed, dtype=torch.int64).to(dev) if not is_device_array(packed) else packed
-    if sd.numel() == 0:
-        sd = torch.zeros(1, dtype=torch.int64, device=dev)
-        n = 0
-    else:
+    with _lib.device_of(vmap.vr, packed):
+        vr = torch.from_numpy(np.ascontiguousarray(vmap.vr)).cuda() if host else vmap.vr
+        dev = vr.device
+        sd = torch.as_tensor(packed, dtype=torch.int64).to(dev) if not is_device_array(packed) \
+            else packed.to(torch.int64).contiguous()
         n = sd.numel()
-    st = _lib.Stats()
-    ws = _lib.workspace(L.iwpp_edt_workspace_bytes(W, H, se.connectivity))
-    rc = L.iwpp_edt_propagate(_lib.ptr(vr), W, H, se.connectivity, _lib.ptr(sd), n,
-                              _lib.ptr(ws), ws.numel(), _max_rounds(cfg, mode),
-                              _lib.ctypes.byref(st), _lib.stream_ptr())
-    if cfg is not None and mode == "parallel":
-        cfg.stats.add(st.as_dict())
-    _lib.check(rc, "edt_propagate")
-    if host:
-        vmap.vr[...] = vr.cpu().numpy()
+        if n == 0:
+            sd = torch.zeros(1, dtype=torch.int64, device=dev)
+        st = _lib.Stats()
+        ws = _lib.workspace(L.iwpp_edt_workspace_bytes(W, H, se.connectivity))
+        rc = L.iwpp_edt_propagate(_lib.ptr(vr), W, H, se.connectivity, _lib.ptr(sd), n,
+                                  _lib.ptr(ws), ws.numel(), _max_rounds(cfg, mode),
+                                  _lib.ctypes.byref(st), _lib.stream_ptr())
+        if cfg is not None and mode == "parallel":
+            cfg.stats.add(st.as_dict())
+        _lib.check(rc, "edt_propagate")
+        if host:
+            vmap.vr[...] = vr.cpu().numpy()
     return vmap
 
 
@@ -214,11 +223,12 @@ def finalize_distance_map(vmap: VoronoiMap) -> Image2D:
     L = _lib.lib()
     torch = _lib._torch()
     host = not vmap.on_device
-    vr = torch.from_numpy(np.ascontiguousarray(vmap.vr)).cuda() if host else vmap.vr.contiguous()
-    dist = torch.empty(vr.shape, dtype=torch.float32, device=vr.device)
-    ws = _lib.workspace(256)
-    rc = L.iwpp_edt_finalize(_lib.ptr(vr), vmap.width, vmap.height, _lib.ptr(dist), None,
-                             _lib.ptr(ws), _lib.stream_ptr())
+    with _lib.device_of(vmap.vr):
+        vr = torch.from_numpy(np.ascontiguousarray(vmap.vr)).cuda() if host else vmap.vr.contiguous()
+        dist = torch.empty(vr.shape, dtype=torch.float32, device=vr.device)
+        ws = _lib.workspace(256)
+        rc = L.iwpp_edt_finalize(_lib.ptr(vr), vmap.width, vmap.height, _lib.ptr(dist), None,
+                                 _lib.ptr(ws), _lib.stream_ptr())
     if rc == _lib.IWPP_E_NO_BACKGROUND:
         raise NoBackgroundError("no background reachable: distance map undefined")
     _lib.check(rc, "finalize_distance_map")
@@ -238,22 +248,31 @@ def edt_tiled(mask: Image2D, se: StructuringElement = SE8,
 
 
 def edt_exact_bruteforce(mask: Image2D) -> Image2D:
-    """edt.py:313-323 / oracles.py:57-73: exact distances by direct
-    minimisation over all background cells (quadratic; torch on device)."""
+    """edt.py:313-323 / oracles.py:57-73: exact distances, the minimum over
+    every background cell.  The device computes that same integer minimum by
+    the separable exact transform (``iwpp_edt_exact``: column distances, then
+    the lower envelope of parabolas per row), linear instead of quadratic."""
     _require_binary(mask)
+    d2, dist = exact_sqdist(mask.data, want_dist=True)
+    return Image2D(mask.width, mask.height, "f32", dist)
+
+
+def exact_sqdist(mask, want_dist: bool = False):
+    """(d2 int64, dist f32 or None) of the exact EDT of a raw 0/nonzero mask
+    (numpy -> numpy, tensor -> tensor).  NoBackgroundError without background."""
+    L = _lib.lib()
     torch = _lib._torch()
-    host = not mask.on_device
-    m = torch.from_numpy(np.ascontiguousarray(mask.data)).cuda() if host else mask.data
-    if not bool((m == 0).any()):
-        raise NoBackgroundError("no background reachable: distance map undefined")
-    H, W = m.shape
-    by, bx = torch.nonzero(m == 0, as_tuple=True)
-    ys = torch.arange(H, device=m.device, dtype=torch.int64)[:, None]
-    xs = torch.arange(W, device=m.device, dtype=torch.int64)[None, :]
-    best = torch.full((H, W), FAR, dtype=torch.int64, device=m.device)
-    for i in range(0, by.numel(), 256):
-        cy = by[i:i + 256].to(torch.int64)[:, None, None]
-        cx = bx[i:i + 256].to(torch.int64)[:, None, None]
-        best = torch.minimum(best, ((ys[None] - cy) ** 2 + (xs[None] - cx) ** 2).amin(0))
-    dist = torch.sqrt(best.to(torch.float64)).to(torch.float32)
-    return Image2D(W, H, "f32", dist.cpu().numpy() if host else dist)
+    host = not is_device_array(mask)
+    H, W = mask.shape
+    with _lib.device_of(mask):
+        m = torch.from_numpy(np.ascontiguousarray(mask, dtype=np.uint8)).cuda() if host \
+            else mask.contiguous()
+        d2 = torch.empty((H, W), dtype=torch.int64, device=m.device)
+        dist = torch.empty((H, W), dtype=torch.float32, device=m.device) if want_dist else None
+        ws = _lib.workspace(L.iwpp_edt_exact_workspace_bytes(W, H))
+        _lib.check(L.iwpp_edt_exact(_lib.ptr(m), W, H, _lib.ptr(d2),
+                                    _lib.ptr(dist) if dist is not None else None, _lib.ptr(ws),
+                                    ws.numel(), _lib.stream_ptr()), "edt_exact")
+        if host:
+            return d2.cpu().numpy(), dist.cpu().numpy() if dist is not None else None
+    return d2, dist

@@ -63,11 +63,12 @@ def _count_violations(m: Image2D, i: Image2D) -> int:
     if m.elem_kind not in DEVICE_KINDS:
         return int((m.data > i.data).sum())
     L = _lib.lib()
-    ws = _lib.workspace(256)
     n = _lib.ctypes.c_int64(0)
-    _lib.check(L.iwpp_check_le(_lib.ptr(m.data), _lib.ptr(i.data), m.width * m.height,
-                               DEVICE_KINDS[m.elem_kind], _lib.ptr(ws), _lib.ctypes.byref(n),
-                               _lib.stream_ptr()), "check_le")
+    with _lib.device_of(m.data, i.data):
+        ws = _lib.workspace(256)
+        _lib.check(L.iwpp_check_le(_lib.ptr(m.data), _lib.ptr(i.data), m.width * m.height,
+                                   DEVICE_KINDS[m.elem_kind], _lib.ptr(ws), _lib.ctypes.byref(n),
+                                   _lib.stream_ptr()), "check_le")
     return int(n.value)
 
 
@@ -112,36 +113,44 @@ def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
     L = _lib.lib()
     from .grid import np_dtype_of, is_device_array
     dt = np_dtype_of(marker)
+    if is_device_array(marker) != is_device_array(mask):
+        raise ContractViolation("marker and mask must both be host or both be device arrays")
+    if len(marker.shape) != 2 or tuple(marker.shape) != tuple(mask.shape):
+        raise ContractViolation(f"marker shape {tuple(marker.shape)} != mask shape "
+                                f"{tuple(mask.shape)} (both must be 2-D)")
+    if np_dtype_of(mask) != dt:
+        raise ContractViolation(f"marker dtype {dt} != mask dtype {np_dtype_of(mask)}")
     code = {np.dtype(np.uint8): 0, np.dtype(np.uint16): 1, np.dtype(np.int32): 2,
             np.dtype(np.float32): 3}.get(dt)
     if kind == "binary" and code == 0:
         code = 4
     if code is None:
         raise ContractViolation(f"no device engine for dtype {dt}")
+    if conn not in (4, 8):
+        raise ContractViolation(f"connectivity must be 4 or 8, got {conn}")
     H, W = marker.shape
     st = _lib.Stats()
     sp = _lib.ctypes.byref(st) if stats is not None else None
     opts = _opts(cfg, sweeps, tile_sweeps, halo_sweep_threshold, max_blocks, pipeline_rows,
                  engine)
-    if is_device_array(marker):
-        torch = _lib._torch()
-        J = marker.clone()
-        I = mask.contiguous()
-        nbytes = L.iwpp_recon_workspace_bytes(W, H, code, conn)
-        ws = _lib.workspace(nbytes)
-        _lib.check(L.iwpp_recon(_lib.ptr(J), _lib.ptr(I), W, H, code, conn, _lib.ptr(ws),
-                                ws.numel(), _lib.ctypes.byref(opts), sp, _lib.stream_ptr()),
-                   "recon")
-        del torch
-    else:
-        m = np.ascontiguousarray(marker)
-        i = np.ascontiguousarray(mask, dtype=m.dtype)
-        J = np.empty_like(m)
-        nbytes = L.iwpp_recon_host_workspace_bytes(W, H, code, conn)
-        ws = _lib.workspace(nbytes)
-        _lib.check(L.iwpp_recon_host(_lib.ptr(J), _lib.ptr(m), _lib.ptr(i), W, H, code, conn,
-                                     _lib.ptr(ws), ws.numel(), _lib.ctypes.byref(opts), sp,
-                                     _lib.stream_ptr()), "recon")
+    with _lib.device_of(marker, mask):
+        if is_device_array(marker):
+            J = marker.clone()
+            I = mask.contiguous()
+            nbytes = L.iwpp_recon_workspace_bytes(W, H, code, conn)
+            ws = _lib.workspace(nbytes)
+            _lib.check(L.iwpp_recon(_lib.ptr(J), _lib.ptr(I), W, H, code, conn, _lib.ptr(ws),
+                                    ws.numel(), _lib.ctypes.byref(opts), sp, _lib.stream_ptr()),
+                       "recon")
+        else:
+            m = np.ascontiguousarray(marker)
+            i = np.ascontiguousarray(mask)
+            J = np.empty_like(m)
+            nbytes = L.iwpp_recon_host_workspace_bytes(W, H, code, conn)
+            ws = _lib.workspace(nbytes)
+            _lib.check(L.iwpp_recon_host(_lib.ptr(J), _lib.ptr(m), _lib.ptr(i), W, H, code, conn,
+                                         _lib.ptr(ws), ws.numel(), _lib.ctypes.byref(opts), sp,
+                                         _lib.stream_ptr()), "recon")
     if stats is not None:
         stats.update(st.as_dict())
     return J

@@ -87,7 +87,8 @@ def test_4k_u8_vs_oracle(gw, conn):
 
 
 @pytest.mark.parametrize("conn", [4, 8])
-def test_4k_int32_vs_oracle(gw, conn):
+def test_2k_int32_seed3_vs_oracle(gw, conn):
+    # 4096^2 int32 (configs[1]'s int32 variant) is in test_gpu_config_parity.py
     J, I = oracle.gray_pair(2048, 3, h=1 << 28, dtype=np.int32)
     want = oracle.recon_fh(J, I, conn)
     got = gw.reconstruct(_torch().from_numpy(J).cuda(), _torch().from_numpy(I).cuda(), conn)
@@ -303,13 +304,21 @@ def test_device_repeated_runs_agree_wide(gw, kind):
     assert bad == 0
 
 
-def test_host_pipeline_contract_in_late_slab(gw):
+@pytest.mark.parametrize("row", [0, 63, 64, 300, 590])
+def test_host_pipeline_contract_in_any_slab(gw, row):
+    # the violation counter must survive every later engine run (the first
+    # slab's count used to be wiped by the next run's counter reset)
     J, I = oracle.gray_pair((600, 128), 4, h=40)
-    J[590, 100] = 255
-    I[590, 100] = 3
-    from paper_1209_3314_b200 import _lib
+    J[row, 100] = 255
+    I[row, 100] = 3
     with pytest.raises(gw.ContractViolation):
         gw.reconstruct(J, I, 8, pipeline_rows=64)
+    # default slab heights (~4 MB per slab): violation in the first slab
+    J, I = oracle.gray_pair((4096, 2048), 5, h=40)
+    J[0, 7] = 9
+    I[0, 7] = 8
+    with pytest.raises(gw.ContractViolation):
+        gw.reconstruct(J, I, 8)
 
 
 # ---------------------------------------------------------------------------
@@ -394,3 +403,25 @@ def test_binary_engine_vs_oracle(gw, conn):
         assert np.array_equal(got, want), (marker.shape, "host")
         out = gw.recon_fh(_pair(gw, marker, mask, conn, "binary", True))
         assert np.array_equal(_np(out.data), want)
+
+
+def test_reconstruct_validates_raw_inputs(gw):
+    """reconstruct() on raw arrays checks shape, dtype and residency before
+    any kernel reads the buffers (an int32 marker with a u8 mask, or a
+    smaller mask, would otherwise be read out of bounds)."""
+    t = _torch()
+    J, I = oracle.gray_pair(64, 2, h=40)
+    dJ, dI = t.from_numpy(J).cuda(), t.from_numpy(I).cuda()
+    with pytest.raises(gw.ContractViolation):
+        gw.reconstruct(dJ.int(), dI, 8)
+    with pytest.raises(gw.ContractViolation):
+        gw.reconstruct(dJ, dI[:32], 8)
+    with pytest.raises(gw.ContractViolation):
+        gw.reconstruct(dJ, I, 8)  # device marker, host mask
+    with pytest.raises(gw.ContractViolation):
+        gw.reconstruct(t.from_numpy(J), t.from_numpy(I), 8)  # CPU tensors
+    with pytest.raises(gw.ContractViolation):
+        gw.reconstruct(J, I.astype(np.uint16), 8)
+    with pytest.raises(gw.ContractViolation):
+        gw.reconstruct(dJ, dI, 6)
+    assert np.array_equal(gw.reconstruct(dJ, dI, 8).cpu().numpy(), oracle.recon_fh(J, I, 8))
