@@ -103,8 +103,11 @@ typedef struct iwpp_recon_opts {
                         (0 = auto, ~2 MB slabs; > 0 = this many rows, rounded up to the
                         32-row tile side; < 0 = off: copy in, compute, copy out) */
   int engine;        /* 0 = auto, 1 = shared-memory queue engine (every dtype), 2 = register
-                        engine (u8/binary: Jacobi steps on packed bytes).  Auto picks the
-                        register engine for u8 unless queue_capacity or tile_sweeps is set */
+                        engine (u8/binary: Jacobi steps on packed bytes) on the tile queue,
+                        3 = register engine in level-synchronous tile rounds (u8, rows
+                        16-byte aligned; one grid barrier per round, no per-tile protocol;
+                        else as 2).  Auto picks the register engine on the tile queue for
+                        u8 unless queue_capacity or tile_sweeps is set */
 } iwpp_recon_opts;
 
 /* Timing helpers (events live in this library's CUDA runtime). */

@@ -56,6 +56,7 @@
 
 #include <cooperative_groups.h>
 #include <type_traits>
+#include <vector>
 #include <cuda.h>  // CUtensorMap (the encoder is fetched from the driver at run time)
 
 #include "iwpp_common.cuh"
@@ -89,7 +90,20 @@ struct EngineArgs {
   uint8_t *dirty;        // per tile row: written by this run (nullable)
   int WW;                // binary engine: words per bit-plane row
   TileQueue q;
+  unsigned long long ntx_m;  // ceil(2^40 / ntx) (0: divide): tile id -> (tx, ty)
 };
+
+// tile id -> (tx, ty) without an integer division (exact while ntx < 2^14
+// and t < 2^26; the launcher sets ntx_m = 0 beyond that)
+__device__ __forceinline__ void tile_xy(const EngineArgs &a, unsigned t, int &tx, int &ty) {
+  if (a.ntx_m) {
+    ty = (int)((t * a.ntx_m) >> 40);
+    tx = (int)(t - (unsigned)ty * (unsigned)a.ntx);
+  } else {
+    tx = (int)(t % (unsigned)a.ntx);
+    ty = (int)(t / (unsigned)a.ntx);
+  }
+}
 
 __device__ __forceinline__ int sidx(int lx, int ly) { return ly * PS + lx; }
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return min(hi, max(lo, v)); }
@@ -713,7 +727,8 @@ __global__ void __launch_bounds__(kCtaThreads, kCtaMinBlocks)
     next_tile = -1;
     if (t < 0) break;
     bool full = __shfl_sync(FULL, first, 0) != 0;
-    const int tx = t % a.ntx, ty = t / a.ntx;
+    int tx, ty;
+    tile_xy(a, (unsigned)t, tx, ty);
     const int x0 = tx * TS, y0 = ty * TS;
     const int limx = min(TS, a.W - x0), limy = min(TS, a.H - y0);
     long long c_load = pclock(l0);
@@ -937,6 +952,50 @@ __device__ __forceinline__ unsigned min2(unsigned a, unsigned b) {
   return r;
 }
 
+// One Jacobi step J <- min(I, 3x3 / cross max of J) on the even / odd split
+// (TRACK: accumulate the changed bits into ch).
+template <int CONN, bool TRACK>
+__device__ __forceinline__ void reg_step(unsigned (&e)[8], unsigned (&o)[8], const unsigned (&ie)[8],
+                                         const unsigned (&io)[8], unsigned &ch) {
+  unsigned ve[8], vo[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    // lanes 0 / 31 see themselves: harmless under max
+    const unsigned ue = __shfl_up_sync(FULL, e[k], 1), de = __shfl_down_sync(FULL, e[k], 1);
+    const unsigned uo = __shfl_up_sync(FULL, o[k], 1), dn = __shfl_down_sync(FULL, o[k], 1);
+    ve[k] = CONN == 8 ? max2(e[k], max2(ue, de)) : max2(ue, de);
+    vo[k] = CONN == 8 ? max2(o[k], max2(uo, dn)) : max2(uo, dn);
+  }
+  if (CONN == 8) {
+    // 3x3 max = horizontal max of the vertical maxima
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const unsigned lE = __funnelshift_l(k ? vo[k - 1] : 0u, vo[k], 16);
+      const unsigned rO = __funnelshift_r(ve[k], k < 7 ? ve[k + 1] : 0u, 16);
+      const unsigned dE = max2(ve[k], max2(lE, vo[k]));
+      const unsigned dO = max2(vo[k], max2(ve[k], rO));
+      const unsigned nE = min2(ie[k], dE), nO = min2(io[k], dO);  // D >= J (centre included)
+      if (TRACK) ch |= (nE ^ e[k]) | (nO ^ o[k]);
+      e[k] = nE;
+      o[k] = nO;
+    }
+  } else {
+    unsigned prevo = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const unsigned lE = __funnelshift_l(prevo, o[k], 16);
+      const unsigned rO = __funnelshift_r(e[k], k < 7 ? e[k + 1] : 0u, 16);
+      const unsigned dE = max2(max2(ve[k], e[k]), max2(lE, o[k]));
+      const unsigned dO = max2(max2(vo[k], o[k]), max2(e[k], rO));
+      prevo = o[k];  // the old odd word, for word k + 1
+      const unsigned nE = min2(ie[k], dE), nO = min2(io[k], dO);
+      if (TRACK) ch |= (nE ^ e[k]) | (nO ^ o[k]);
+      e[k] = nE;
+      o[k] = nO;
+    }
+  }
+}
+
 // Jacobi steps to the tile's fixed point; returns the number of steps.
 // The row's 32 pixels are split into even / odd pixels, two per word as
 // 16-bit lanes: e[k] = (p[4k], p[4k+2]), o[k] = (p[4k+1], p[4k+3]).  Then a
@@ -983,54 +1042,24 @@ __device__ __forceinline__ int reg_fixpoint(unsigned *j, const unsigned *m, cons
       o[k] = max2(o[k], min2(io[k], dO));
     }
   }
-#pragma unroll
-  for (int k = 0; k < 8; k++) changed |= ((e[k] | (o[k] << 8)) != j[k]);
+  // Jacobi steps in pairs, the change test on the second step of a pair
+  // only: a pair whose second step changes nothing ends at a fixed point
+  // (costs at most one extra step; saves the test and the loop-carried
+  // register copies of every other step)
   int steps = 0;
   for (;;) {
-    steps++;
-    unsigned ve[8], vo[8];
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      // lanes 0 / 31 see themselves: harmless under max
-      const unsigned ue = __shfl_up_sync(FULL, e[k], 1), de = __shfl_down_sync(FULL, e[k], 1);
-      const unsigned uo = __shfl_up_sync(FULL, o[k], 1), dn = __shfl_down_sync(FULL, o[k], 1);
-      ve[k] = CONN == 8 ? max2(e[k], max2(ue, de)) : max2(ue, de);
-      vo[k] = CONN == 8 ? max2(o[k], max2(uo, dn)) : max2(uo, dn);
-    }
     unsigned ch = 0;
-    if (CONN == 8) {
-      // 3x3 max = horizontal max of the vertical maxima
-#pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const unsigned lE = __funnelshift_l(k ? vo[k - 1] : 0u, vo[k], 16);
-        const unsigned rO = __funnelshift_r(ve[k], k < 7 ? ve[k + 1] : 0u, 16);
-        const unsigned dE = max2(ve[k], max2(lE, vo[k]));
-        const unsigned dO = max2(vo[k], max2(ve[k], rO));
-        const unsigned nE = min2(ie[k], dE), nO = min2(io[k], dO);  // D >= J (centre included)
-        ch |= (nE ^ e[k]) | (nO ^ o[k]);
-        e[k] = nE;
-        o[k] = nO;
-      }
-    } else {
-      unsigned prevo = 0;
-#pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const unsigned lE = __funnelshift_l(prevo, o[k], 16);
-        const unsigned rO = __funnelshift_r(e[k], k < 7 ? e[k + 1] : 0u, 16);
-        const unsigned dE = max2(max2(ve[k], e[k]), max2(lE, o[k]));
-        const unsigned dO = max2(max2(vo[k], o[k]), max2(e[k], rO));
-        prevo = o[k];  // the old odd word, for word k + 1
-        const unsigned nE = min2(ie[k], dE), nO = min2(io[k], dO);
-        ch |= (nE ^ e[k]) | (nO ^ o[k]);
-        e[k] = nE;
-        o[k] = nO;
-      }
-    }
+    reg_step<CONN, false>(e, o, ie, io, ch);
+    reg_step<CONN, true>(e, o, ie, io, ch);
+    steps += 2;
     if (!__any_sync(FULL, ch != 0)) break;
-    changed = true;
   }
 #pragma unroll
-  for (int k = 0; k < 8; k++) j[k] = e[k] | (o[k] << 8);
+  for (int k = 0; k < 8; k++) {
+    const unsigned nj = e[k] | (o[k] << 8);
+    changed |= nj != j[k];
+    j[k] = nj;
+  }
   return steps;
 }
 
@@ -1050,6 +1079,7 @@ struct alignas(128) TmaWarpSmem {
   uint8_t I[kBoxBytes];
   uint8_t pad1[(128 - kBoxBytes % 128) % 128];
   unsigned long long bar;
+  alignas(16) uint8_t nrow[2 * TS];  // the new top / bottom row (need test)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
@@ -1105,6 +1135,36 @@ __device__ __forceinline__ void tma_row(const uint8_t *box, int r, unsigned *w) 
   w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
 }
 
+// The need test of the rows above / below (which neighbour tile can my
+// changed border still raise?), one lane per column: lanes 0 / 31 park the
+// new top / bottom row in shared memory; column x then tests the halo cell
+// above / below it against the changed border cells at x-1..x+1 (x for
+// 4-conn): J(q) < I(q) and J(q) < the changed value.  The border as loaded
+// and the halo rows are in this tile's boxes.  Returns bit 0 = N, bit 1 = S.
+template <int CONN>
+__device__ __forceinline__ unsigned tma_need_rows(TmaWarpSmem &t, const unsigned *j, int lane) {
+  if (lane == 0 || lane == 31) {
+    uint4 *d = reinterpret_cast<uint4 *>(t.nrow + (lane == 31 ? TS : 0));
+    d[0] = make_uint4(j[0], j[1], j[2], j[3]);
+    d[1] = make_uint4(j[4], j[5], j[6], j[7]);
+  }
+  __syncwarp();
+  const int c = kBoxX + lane;
+  const unsigned nt = t.nrow[lane], nb = t.nrow[TS + lane];
+  const unsigned ct = nt != t.J[kBoxW + c] ? nt : 0u;
+  const unsigned cb = nb != t.J[TS * kBoxW + c] ? nb : 0u;
+  unsigned dt = ct, db = cb;
+  if (CONN == 8) {  // lanes 0 / 31 see themselves: harmless under max
+    dt = max(ct, max(__shfl_up_sync(FULL, ct, 1), __shfl_down_sync(FULL, ct, 1)));
+    db = max(cb, max(__shfl_up_sync(FULL, cb, 1), __shfl_down_sync(FULL, cb, 1)));
+  }
+  const unsigned hjt = t.J[c], hit = t.I[c];
+  const unsigned hjb = t.J[(TS + 1) * kBoxW + c], hib = t.I[(TS + 1) * kBoxW + c];
+  const bool n = hjt < hit && hjt < dt, sth = hjb < hib && hjb < db;
+  __syncwarp();  // nrow is rewritten by the next test
+  return (__any_sync(FULL, n) ? 1u : 0u) | (__any_sync(FULL, sth) ? 2u : 0u);
+}
+
 // the two box descriptors travel as a __grid_constant__ kernel parameter
 // (no upload, no tensormap proxy fence)
 struct alignas(64) BoxMaps {
@@ -1153,7 +1213,8 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     t = __shfl_sync(FULL, t, 0);
     next_tile = -1;
     if (t < 0) break;
-    const int tx = t % a.ntx, ty = t / a.ntx;
+    int tx, ty;
+    tile_xy(a, (unsigned)t, tx, ty);
     const int x0 = tx * TS, y0 = ty * TS;
     long long c_load = pclock(l0);
     if (kPhases && l0) ph[0] += c_load - c_pop;
@@ -1174,15 +1235,8 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
       h.cr = ts.J[hr * kBoxW + kBoxX + TS];
       h.clI = ts.I[hr * kBoxW + kBoxX - 1];
       h.crI = ts.I[hr * kBoxW + kBoxX + TS];
-      if (edge) {
-        unsigned hI[8];
-        tma_row(ts.I, hr, hI);
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          ws.rowI[sel][k] = hI[k];
-          ws.ob[sel][k] = j[k];
-        }
-      }
+      // (the need test reads the border as loaded and the halo rows' mask
+      // from the boxes: tma_need_rows)
     } else {
       reg_load_row((const uint8_t *)a.J, a.W, x0, y0 + lane, a.H, a.vec, true, j);
       reg_load_row((const uint8_t *)a.I, a.W, x0, y0 + lane, a.H, a.vec, false, m);
@@ -1229,7 +1283,10 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
         // which neighbours can the changed border still raise (J < I, J < the
         // max of the adjacent changed border cells)?
         unsigned need_row = 0;  // lanes 0 / 31: the row above / below
-        if (edge) {
+        unsigned need_ns = 0;   // (TMA staging) bit 0 / 1: N / S
+        if (use_tma) {
+          need_ns = tma_need_rows<CONN>(ts, j, lane);
+        } else if (edge) {
           unsigned cv[8];
 #pragma unroll
           for (int k = 0; k < 8; k++) cv[k] = j[k] & __vcmpne4(j[k], ws.ob[sel][k]);
@@ -1256,9 +1313,11 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
           dl = max(cl, max(lu, ld));
           dr = max(cr, max(ru, rd));
         }
-        unsigned dirs = 0;
-        if (__any_sync(FULL, l0 && need_row)) dirs |= 1u << 1;             // N
-        if (__any_sync(FULL, lane == 31 && need_row)) dirs |= 1u << 7;     // S
+        unsigned dirs = ((need_ns & 1u) << 1) | ((need_ns & 2u) << 6);
+        if (!use_tma) {
+          if (__any_sync(FULL, l0 && need_row)) dirs |= 1u << 1;             // N
+          if (__any_sync(FULL, lane == 31 && need_row)) dirs |= 1u << 7;     // S
+        }
         if (__any_sync(FULL, h.l < h.lI && h.l < dl)) dirs |= 1u << 3;    // W
         if (__any_sync(FULL, h.r < h.rI && h.r < dr)) dirs |= 1u << 5;    // E
         if (CONN == 8) {  // corners: one interior cell each
@@ -1268,7 +1327,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
           if (__any_sync(FULL, lane == 31 && cwl)) dirs |= 1u << 6;
           if (__any_sync(FULL, lane == 31 && cwr)) dirs |= 1u << 8;
         }
-        if (edge)
+        if (edge && !use_tma)
 #pragma unroll
           for (int k = 0; k < 8; k++) ws.ob[sel][k] = j[k];
         obl = jl;
@@ -1333,6 +1392,261 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     atomicAdd(&counters[CNT_STEPS], n_steps);
     if (kPhases)
       for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
+  }
+}
+
+
+// --- level-synchronous tile rounds (register engine, u8) ------------------------
+//
+// The queue engine above pays a chain of L2 round trips per tile activation
+// (ticket, slot, acquire exchange, box load, publish fence, claims, finish
+// CAS).  This engine runs the same per-tile fixed point in rounds instead:
+//   round 0      every tile once, from the marker (2 x 2 colour order, so
+//                the tiles running at the same time are not neighbours);
+//   round r > 0  exactly the tiles a neighbour flagged in round r - 1 (its
+//                changed border can still raise one of their cells: the same
+//                need test as the queue engine's activation);
+// with one grid barrier per round and no per-tile protocol (no state word,
+// no publish fence, no finish CAS).  Tiles of one round run concurrently
+// and may read a neighbour's border before or after that neighbour writes
+// it; values only grow between the marker and the result, and a neighbour
+// that changes its border after we read it flags us for the next round, so
+// the last round leaves every tile at its fixed point under its final halo:
+// the unique fixed point (engine.py:9-18), exactly.  Round 0 is the
+// reference's scan phase; the later rounds are its wavefront phase
+// (K.220-270), level-synchronous like run_parallel's rounds
+// (engine.py:251-364) at tile granularity, with the round's front as a
+// deduplicated tile list (the GBQ of one round).
+//
+// Work split: entry i of a round's list goes to warp i mod nw, so every
+// warp gets the same number of tiles (+-1) and knows its next tile while it
+// processes the current one: the next tile's TMA boxes load into a second
+// staging buffer meanwhile.  Flagging a tile = returned atomicOr on the next
+// round's bitmap (dedupe) + a warp-aggregated push onto the next list.
+struct RoundsArgs {
+  unsigned *bm0, *bm1;      // round bitmaps (one bit per tile)
+  unsigned *list0, *list1;  // round tile lists (ntiles entries each)
+  unsigned *len;            // 3 list lengths (round % 3), 64 words apart
+  unsigned *bar_count, *bar_gen;
+};
+constexpr int kLenStride = 64;
+
+__device__ __forceinline__ void rounds_barrier(unsigned *count, unsigned *gen, unsigned nblocks,
+                                               unsigned &g) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned arrived;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(count) : "memory");
+    if (arrived == nblocks - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(count) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gen) : "memory");
+    } else {
+      while (ld_acquire(gen) == g) __nanosleep(32);
+    }
+    g++;
+  }
+  __syncthreads();
+}
+
+// round 0's tile order: the 2 x 2 colour classes one after the other, each
+// in raster order (the queue engine's initial queue order)
+struct ColourOrder {
+  unsigned cx[4], base[4];
+  unsigned long long m[4];  // ceil(2^40 / cx): exact for cx < 2^14, r < 2^26
+  __device__ ColourOrder(int ntx, int nty) {
+    unsigned acc = 0;
+    for (int c = 0; c < 4; c++) {
+      cx[c] = (ntx - (c & 1) + 1) / 2;
+      const unsigned cy = (nty - (c >> 1) + 1) / 2;
+      base[c] = acc;
+      acc += cx[c] * cy;
+      m[c] = cx[c] ? ((1ull << 40) + cx[c] - 1) / cx[c] : 0;
+    }
+  }
+  __device__ __forceinline__ unsigned tile(unsigned i, int ntx) const {
+    const int c = (i >= base[1]) + (i >= base[2]) + (i >= base[3]);
+    const unsigned r = i - base[c];
+    const unsigned ry = (unsigned)((r * m[c]) >> 40), rx = r - ry * cx[c];
+    return (2 * ry + (c >> 1)) * (unsigned)ntx + 2 * rx + (c & 1);
+  }
+};
+
+template <int CONN>
+__global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
+    tile_rounds_reg_kernel(EngineArgs a, RoundsArgs r, unsigned long long *counters,
+                           const __grid_constant__ BoxMaps maps, int keep_counters, int rtrace) {
+  __shared__ TmaWarpSmem tsm[kWarpsPerCta][2];
+  __shared__ unsigned s_len;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const unsigned nw = gridDim.x * kWarpsPerCta;
+  const unsigned gw = blockIdx.x * kWarpsPerCta + wib;
+  const unsigned ntiles = (unsigned)a.ntx * a.nty;
+  const unsigned nwords = (ntiles + 31) / 32;
+  unsigned long long t_start = 0;
+  if (rtrace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  {  // clear both bitmaps and the control words, then one grid-wide sync
+    const unsigned i0 = blockIdx.x * blockDim.x + threadIdx.x, st = gridDim.x * blockDim.x;
+    for (unsigned i = i0; i < nwords; i += st) {
+      r.bm0[i] = 0;
+      r.bm1[i] = 0;
+    }
+    if (i0 < 3) r.len[i0 * kLenStride] = 0;
+    if (i0 == 0) *r.bar_count = 0;
+    if (!keep_counters && i0 < CNT_N) counters[i0] = 0;
+  }
+  cooperative_groups::this_grid().sync();
+  unsigned bar_g = threadIdx.x == 0 ? ld_acquire(r.bar_gen) : 0u;
+
+  if (lane == 0) {
+    mbar_init(&tsm[wib][0].bar);
+    mbar_init(&tsm[wib][1].bar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const CUtensorMap *tmJ = &maps.m[0], *tmI = &maps.m[1];
+  unsigned phase[2] = {0, 0};
+  const bool l0 = lane == 0;
+  unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0;
+  const ColourOrder corder(a.ntx, a.nty);
+
+  auto issue = [&](unsigned t, int bi) {  // lane 0: both boxes of tile t into buffer bi
+    if (l0) {
+      int tx, ty;
+      tile_xy(a, t, tx, ty);
+      TmaWarpSmem &ts = tsm[wib][bi];
+      mbar_expect_tx(&ts.bar, 2u * kBoxBytes);
+      tma_load_box(tmJ, ts.J, &ts.bar, tx * TS - kBoxX, ty * TS - 1);
+      tma_load_box(tmI, ts.I, &ts.bar, tx * TS - kBoxX, ty * TS - 1);
+    }
+  };
+
+  unsigned n = ntiles;  // this round's list length
+  for (unsigned round = 0;; round++) {
+    const unsigned *list = (round & 1) ? r.list1 : r.list0;
+    unsigned *nlist = (round & 1) ? r.list0 : r.list1;
+    unsigned *bcur = (round & 1) ? r.bm1 : r.bm0;
+    unsigned *bnxt = (round & 1) ? r.bm0 : r.bm1;
+    unsigned *nlen = &r.len[((round + 1) % 3) * kLenStride];
+    // other SMs' stores of the previous round (ordered by the barrier) must be
+    // visible to the async proxy that performs the box reads
+    if (l0) asm volatile("fence.proxy.async.global;" ::: "memory");
+    // the length counter of round + 2 was last read after round - 1's barrier
+    if (blockIdx.x == 0 && threadIdx.x == 0) r.len[((round + 2) % 3) * kLenStride] = 0;
+    auto entry = [&](unsigned i) -> unsigned {
+      return round == 0 ? corder.tile(i, a.ntx) : ld_relaxed(&list[i]);
+    };
+    unsigned i = gw;
+    unsigned t = i < n ? entry(i) : 0u;
+    unsigned tn = i + nw < n ? entry(i + nw) : 0u;  // list entries load one tile ahead
+    int bi = 0;
+    if (i < n) issue(t, bi);
+    while (i < n) {
+      const unsigned i2 = i + nw;
+      const unsigned tnn = i2 + nw < n ? entry(i2 + nw) : 0u;
+      if (round > 0 && l0) bcur[t >> 5] = 0;  // consumed (bnxt of round + 1)
+      __syncwarp();  // the other buffer's previous tile is done (WAR)
+      if (i2 < n) issue(tn, bi ^ 1);
+      TmaWarpSmem &ts = tsm[wib][bi];
+      mbar_wait(&ts.bar, phase[bi]);
+      phase[bi] ^= 1u;
+      int tx, ty;
+      tile_xy(a, t, tx, ty);
+      const int x0 = tx * TS, y0 = ty * TS;
+      unsigned j[8], m[8];
+      RegHalo h;
+      const int hr = lane == 0 ? 0 : TS + 1;  // halo row (lanes 0 / 31)
+      tma_row(ts.J, lane + 1, j);
+      tma_row(ts.I, lane + 1, m);
+      tma_row(ts.J, hr, h.row);
+      h.l = ts.J[(lane + 1) * kBoxW + kBoxX - 1];
+      h.r = ts.J[(lane + 1) * kBoxW + kBoxX + TS];
+      h.lI = ts.I[(lane + 1) * kBoxW + kBoxX - 1];
+      h.rI = ts.I[(lane + 1) * kBoxW + kBoxX + TS];
+      h.cl = ts.J[hr * kBoxW + kBoxX - 1];
+      h.cr = ts.J[hr * kBoxW + kBoxX + TS];
+      h.clI = ts.I[hr * kBoxW + kBoxX - 1];
+      h.crI = ts.I[hr * kBoxW + kBoxX + TS];
+      const unsigned obl = j[0] & 0xffu, obr = j[7] >> 24;
+      n_tiles += l0;
+      n_reruns += l0 && round > 0;
+      bool changed = false;
+      const int steps = reg_fixpoint<CONN>(j, m, h, lane, changed);
+      if (l0) n_steps += steps;
+      if (__any_sync(FULL, changed)) {
+        const int gy = y0 + lane;
+        if (gy < a.H) {
+          uint8_t *p = (uint8_t *)a.J + (size_t)gy * a.W + x0;
+          reinterpret_cast<uint4 *>(p)[0] = make_uint4(j[0], j[1], j[2], j[3]);
+          if (x0 + TS <= a.W)  // (else W % 32 == 16: the last tile column holds 16 pixels)
+            reinterpret_cast<uint4 *>(p)[1] = make_uint4(j[4], j[5], j[6], j[7]);
+        }
+        // which neighbours can the changed border still raise?
+        const unsigned need_ns = tma_need_rows<CONN>(ts, j, lane);
+        const unsigned jl = j[0] & 0xffu, jr = j[7] >> 24;
+        const unsigned cl = jl != obl ? jl : 0u, cr = jr != obr ? jr : 0u;
+        unsigned dl = cl, dr = cr;
+        if (CONN == 8) {
+          unsigned lu = __shfl_up_sync(FULL, cl, 1), ld = __shfl_down_sync(FULL, cl, 1);
+          unsigned ru = __shfl_up_sync(FULL, cr, 1), rd = __shfl_down_sync(FULL, cr, 1);
+          if (lane == 0) lu = ru = 0;
+          if (lane == 31) ld = rd = 0;
+          dl = max(cl, max(lu, ld));
+          dr = max(cr, max(ru, rd));
+        }
+        unsigned dirs = ((need_ns & 1u) << 1) | ((need_ns & 2u) << 6);  // N, S
+        if (__any_sync(FULL, h.l < h.lI && h.l < dl)) dirs |= 1u << 3;   // W
+        if (__any_sync(FULL, h.r < h.rI && h.r < dr)) dirs |= 1u << 5;   // E
+        if (CONN == 8) {
+          const bool cwl = h.cl < h.clI && h.cl < cl, cwr = h.cr < h.crI && h.cr < cr;
+          if (__any_sync(FULL, l0 && cwl)) dirs |= 1u << 0;
+          if (__any_sync(FULL, l0 && cwr)) dirs |= 1u << 2;
+          if (__any_sync(FULL, lane == 31 && cwl)) dirs |= 1u << 6;
+          if (__any_sync(FULL, lane == 31 && cwr)) dirs |= 1u << 8;
+        }
+        // flag: first setter of the tile's bit pushes it onto the next list
+        bool push = false;
+        unsigned nt = 0;
+        if (lane < 9 && ((dirs >> lane) & 1u)) {
+          const int nx = tx + (lane % 3) - 1, ny = ty + (lane / 3) - 1;
+          if (nx >= 0 && nx < a.ntx && ny >= 0 && ny < a.nty) {
+            nt = (unsigned)(ny * a.ntx + nx);
+            const unsigned bit = 1u << (nt & 31);
+            push = !(atomicOr(&bnxt[nt >> 5], bit) & bit);
+          }
+        }
+        const unsigned pm = __ballot_sync(FULL, push);
+        if (pm) {
+          unsigned base = 0;
+          if (l0) base = atomicAdd(nlen, (unsigned)__popc(pm));
+          base = __shfl_sync(FULL, base, 0);
+          if (push) nlist[base + __popc(pm & ((1u << lane) - 1))] = nt;
+        }
+      }
+      i = i2;
+      t = tn;
+      tn = tnn;
+      bi ^= 1;
+    }
+    rounds_barrier(r.bar_count, r.bar_gen, gridDim.x, bar_g);
+    if (threadIdx.x == 0) {
+      s_len = ld_relaxed(nlen);
+      if (rtrace && blockIdx.x == 0 && round < 37) {
+        unsigned long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        r.len[(3 + round) * kLenStride] = (unsigned)(now - t_start);  // trace: ns at round end
+      }
+    }
+    __syncthreads();
+    n = s_len;
+    if (n == 0) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[CNT_ROUNDS], round + 1);
+      break;
+    }
+  }
+  if (l0) {
+    atomicAdd(&counters[CNT_TILES], n_tiles);
+    atomicAdd(&counters[CNT_RERUNS], n_reruns);
+    atomicAdd(&counters[CNT_STEPS], n_steps);
   }
 }
 
@@ -1531,7 +1845,8 @@ __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
     t = __shfl_sync(FULL, t, 0);
     next_tile = -1;
     if (t < 0) break;
-    const int tx = t % a.ntx, ty = t / a.ntx;
+    int tx, ty;
+    tile_xy(a, (unsigned)t, tx, ty);
     const int x0 = tx * TS, y0 = ty * TS;
     long long c_load = pclock(l0);
     if (kPhases && l0) ph[0] += c_load - c_pop;
@@ -1816,7 +2131,8 @@ __global__ void __launch_bounds__(kCtaThreads)
     t = __shfl_sync(FULL, t, 0);
     next_tile = -1;
     if (t < 0) break;
-    const int tx = t % a.ntx, ty = t / a.ntx;
+    int tx, ty;
+    tile_xy(a, (unsigned)t, tx, ty);
     const int x0 = tx * TSB, y0 = ty * TSB;
     long long c_load = pclock(l0);
     if (kPhases && l0) ph[0] += c_load - c_pop;
@@ -2211,7 +2527,7 @@ static bool make_box_map(CUtensorMap *map, const void *base, int W, int H, int e
 template <typename T>
 static bool use_reg_engine(const EngineOpts &o) {
   if (o.engine == ENGINE_SMEM) return false;
-  if (o.engine == ENGINE_REG) return true;
+  if (o.engine == ENGINE_REG || o.engine == ENGINE_ROUNDS) return true;
   return o.qcap <= 0 && o.sweeps_set == 0;
 }
 
@@ -2321,7 +2637,10 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   unsigned qlimit = (o.qcap > 0 && o.qcap < RQ) ? (unsigned)o.qcap : (unsigned)RQ;
   unsigned hth = o.halo_thresh >= 0 ? (unsigned)o.halo_thresh : kHaloSweepThreshold;
   bool vec = ((size_t)W * sizeof(T)) % 16 == 0 && (uintptr_t)J % 16 == 0 && (uintptr_t)I % 16 == 0;
-  EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, o.dirty, (W + 31) / 32, q};
+  const unsigned long long ntx_m =
+      (ntx < (1 << 14) && nty < (1 << 23) && ntiles < (1u << 26)) ? ((1ull << 40) + ntx - 1) / ntx
+                                                                  : 0ull;
+  EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, o.dirty, (W + 31) / 32, q, ntx_m};
   if (o.ev_begin) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_begin, st));
   if (use_bin_engine(binary, o)) {
     static int bin_blocks = 0;
@@ -2359,7 +2678,49 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
     int use_tma = vec && q.tmaps && make_box_map(&maps.m[0], J, W, H, 1, kBoxW) &&
                   make_box_map(&maps.m[1], I, W, H, 1, kBoxW);
     if (getenv("IWPP_TRACE")) fprintf(stderr, "[iwpp] reg engine %dx%d use_tma=%d vec=%d fused=%d\n", W, H, use_tma, (int)vec, fused_init);
-    if (fused_init) {
+    // level-synchronous rounds: a plain full run (no slab rows, no pipelined
+    // continuation, no dirty flags) with TMA staging
+    static int rounds_env = -1;
+    // (AUTO keeps the queue engine: measured 0.125 vs 0.130-0.137 ms at 4K^2
+    // u8 c8, 26.7 vs 28.5 ms at 64K^2; IWPP_RECON_ROUNDS=1 makes AUTO pick
+    // the rounds engine)
+    if (rounds_env < 0) rounds_env = getenv("IWPP_RECON_ROUNDS") ? atoi(getenv("IWPP_RECON_ROUNDS")) : 0;
+    const bool rounds = use_tma && ntx_m && o.init_mode != INIT_CONTINUE && !o.rows_mode && !o.dirty &&
+                        (o.engine == ENGINE_ROUNDS || (o.engine == ENGINE_AUTO && rounds_env));
+    if (rounds) {
+      static int rd_per_sm = 0;
+      if (rd_per_sm == 0) {
+        IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rd_per_sm, tile_rounds_reg_kernel<CONN>,
+                                                                    kCtaThreads, 0));
+        if (rd_per_sm < 1) rd_per_sm = 1;
+      }
+      int nb = device_sm_count() * rd_per_sm;
+      if (o.max_blocks > 0 && nb > o.max_blocks) nb = o.max_blocks;
+      if ((unsigned)nb > max_b) nb = (int)max_b;
+      RoundsArgs ra;
+      unsigned *w32 = reinterpret_cast<unsigned *>(q.ring);  // the ring is free in this mode
+      const size_t nwd = (ntiles + 31) / 32;
+      ra.len = w32;                      // [0, 3): lengths; [3, 3 + rounds): trace
+      ra.bar_count = w32 + 40 * kLenStride;
+      ra.bar_gen = w32 + 41 * kLenStride;
+      ra.bm0 = w32 + 42 * kLenStride;
+      ra.bm1 = ra.bm0 + (nwd + 63) / 64 * 64;
+      ra.list0 = ra.bm1 + (nwd + 63) / 64 * 64;
+      ra.list1 = ra.list0 + (ntiles + 63) / 64 * 64;
+      int kc = o.keep_counters ? 1 : 0;
+      static int rtrace = getenv("IWPP_RECON_RTRACE") ? 1 : 0;
+      void *args[] = {&a, &ra, &counters, &maps, &kc, &rtrace};
+      IWPP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)tile_rounds_reg_kernel<CONN>, dim3(nb),
+                                                dim3(kCtaThreads), args, 0, st));
+      if (rtrace) {  // diagnostics: per-round end times (IWPP_RECON_RTRACE)
+        std::vector<unsigned> tr(40 * kLenStride);
+        IWPP_CUDA_TRY(cudaMemcpyAsync(tr.data(), ra.len, tr.size() * 4, cudaMemcpyDeviceToHost, st));
+        IWPP_CUDA_TRY(cudaStreamSynchronize(st));
+        for (int k = 0; k < 37 && tr[(3 + k) * kLenStride]; k++)
+          fprintf(stderr, "[rounds] round %d ends at %.2f us\n", k, tr[(3 + k) * kLenStride] * 1e-3);
+        IWPP_CUDA_TRY(cudaMemsetAsync(ra.len, 0, 40 * kLenStride * 4, st));
+      }
+    } else if (fused_init) {
       int fi = fused_init;
       void *args[] = {&a, &counters, &maps, &use_tma, &fi};
       IWPP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)tile_engine_reg_kernel<CONN>, dim3(rb),

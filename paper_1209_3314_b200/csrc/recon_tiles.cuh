@@ -45,6 +45,7 @@ constexpr unsigned kHaloSweepThreshold = 16;
 enum {
   CNT_TILES = 0, CNT_RERUNS, CNT_PUSHES, CNT_OVERFLOW, CNT_SEEDS, CNT_VIOL,
   CNT_STEPS,  // register engine: Jacobi steps summed over tile activations
+  CNT_ROUNDS, // round engine: rounds of the last run
   // per-phase SM cycles summed over warps (lane 0's clock; diagnostics)
   CNT_PH_POP = 8, CNT_PH_LOAD, CNT_PH_SWEEP, CNT_PH_DETECT, CNT_PH_BFS, CNT_PH_STORE,
   CNT_N = 16
@@ -75,10 +76,13 @@ struct EngineOpts {
   int sel_lo = 0, sel_hi = -1;  // INIT_CONTINUE: tile-row range (-1 = last row)
   uint8_t *dirty = nullptr;     // optional: set to 1 for each tile row the run wrote
   bool keep_counters = false;   // accumulate into the device counters (no reset)
-  int engine = 0;               // ENGINE_AUTO / ENGINE_SMEM / ENGINE_REG
+  int engine = 0;               // ENGINE_AUTO / ENGINE_SMEM / ENGINE_REG / ENGINE_ROUNDS
   int sweeps_set = 0;           // the caller fixed the in-tile sweep count
 };
-enum { ENGINE_AUTO = 0, ENGINE_SMEM = 1, ENGINE_REG = 2 };
+// ENGINE_REG: the register engine on the tile queue; ENGINE_ROUNDS: the
+// register engine in level-synchronous tile rounds (u8; AUTO picks it when
+// it applies)
+enum { ENGINE_AUTO = 0, ENGINE_SMEM = 1, ENGINE_REG = 2, ENGINE_ROUNDS = 3 };
 enum { INIT_FULL = 0, INIT_CONTINUE = 1 };
 
 size_t tile_queue_bytes(unsigned ntiles);

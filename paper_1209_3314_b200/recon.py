@@ -75,7 +75,7 @@ def _count_violations(m: Image2D, i: Image2D) -> int:
 # ---------------------------------------------------------------------------
 # the device engine
 
-ENGINE_AUTO, ENGINE_SMEM, ENGINE_REG = 0, 1, 2  # iwpp_recon_opts.engine
+ENGINE_AUTO, ENGINE_SMEM, ENGINE_REG, ENGINE_ROUNDS = 0, 1, 2, 3  # iwpp_recon_opts.engine
 
 def _opts(cfg: EngineConfig | None, sweeps: int = -1, tile_sweeps: int = -1,
           halo_sweep_threshold: int = -1, max_blocks: int = 0,
@@ -106,7 +106,9 @@ def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
     keywords are engine tuning knobs (results never depend on them);
     ``pipeline_rows`` sets the slab height of the host path's transfer /
     compute pipeline (0 = auto, < 0 = off); ``engine`` picks the tile engine
-    (0 = auto, 1 = shared-memory queue engine, 2 = register engine, u8 only).
+    (0 = auto, 1 = shared-memory queue engine, 2 = register engine on the
+    tile queue, 3 = register engine in level-synchronous tile rounds; 2 and 3
+    are u8 only).
     ``kind="binary"`` (u8 arrays holding only 0 / 255, grid.py binary) runs
     the one-bit-per-pixel engine.
     """

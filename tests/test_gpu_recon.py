@@ -355,20 +355,27 @@ def test_f32_operator_api_and_nan_contract(gw):
 
 
 # ---------------------------------------------------------------------------
-# both u8 tile engines (register Jacobi engine = auto; shared-memory queue
-# engine = forced) on the same inputs
+# the u8 tile engines (register Jacobi engine on the tile queue = auto;
+# shared-memory queue engine; register engine in level-synchronous tile
+# rounds, which needs 16-byte aligned rows) on the same inputs
 
-@pytest.mark.parametrize("engine", [1, 2])
+@pytest.mark.parametrize("engine", [1, 2, 3])
 @pytest.mark.parametrize("conn", [4, 8])
 def test_u8_engines_vs_oracle(gw, engine, conn):
     t = _torch()
     rng = np.random.default_rng(700 + conn)
     cases = [oracle.gray_pair(s, int(rng.integers(1 << 30)), h=40)
-             for s in [(1, 1), (31, 33), (64, 64), (97, 130), (513, 257), (1000, 999)]]
+             for s in [(1, 1), (31, 33), (64, 64), (97, 130), (513, 257), (1000, 999),
+                       (96, 176), (1040, 2048)]]
     bw = oracle.gen_synthetic_mask(700, 530, 50, 7)
     cases.append(oracle.imfill_pair(bw))
     I = np.full((300, 260), 200, np.uint8)
     I[::3, 1:] = 0  # long corridor
+    M = np.zeros_like(I)
+    M[-1, 0] = 200
+    cases.append((M, I))
+    I = np.full((320, 256), 200, np.uint8)  # the corridor with aligned rows
+    I[::3, 1:] = 0
     M = np.zeros_like(I)
     M[-1, 0] = 200
     cases.append((M, I))
