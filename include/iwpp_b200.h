@@ -59,7 +59,8 @@ enum iwpp_status {
 /* Counters mirrored from RunStats (engine.py:46-59) plus device-engine
  * counters.  Filled only when a non-NULL pointer is passed (forces a sync). */
 typedef struct iwpp_stats {
-  int64_t rounds;          /* EDT: two-phase rounds; recon: 0 (asynchronous engine) */
+  int64_t rounds;          /* EDT: two-phase rounds; recon: tile rounds of the round engine
+                              (engine 3), 0 for the asynchronous tile-queue engines */
   int64_t executions;      /* engine executions (overflow re-runs included) */
   int64_t overflow_count;  /* block-queue overflows resolved by an in-tile rescan */
   int64_t queued_total;    /* queue insertions (pixels) */
@@ -108,6 +109,10 @@ typedef struct iwpp_recon_opts {
                         16-byte aligned; one grid barrier per round, no per-tile protocol;
                         else as 2).  Auto picks the register engine on the tile queue for
                         u8 unless queue_capacity or tile_sweeps is set */
+  int max_rounds;    /* EngineConfig.max_rounds (engine.py:311-317): > 0 caps the rounds
+                        of the tile-rounds engine (engine 3; auto picks it when set):
+                        IWPP_E_ENGINE_LIMIT if the fixed point needs more.  0 / -1: no cap.
+                        Other engines have no rounds and ignore it */
 } iwpp_recon_opts;
 
 /* Timing helpers (events live in this library's CUDA runtime). */
@@ -153,6 +158,22 @@ int iwpp_recon_sweep_rows(void *J, const void *I, int64_t W, int64_t H, int dtyp
  * composites + carry scan + apply).  workspace: iwpp_recon_workspace_bytes. */
 int iwpp_recon_sweep_cols(void *J, const void *I, int64_t W, int64_t H, int dtype,
                           void *workspace, void *stream);
+/* The reference's individual sequential passes, cell for cell (their
+ * intermediate states are schedule-specific): recon.raster_pass
+ * (recon.py:134-139 -> K.38-74), recon.antiraster_pass / _antiraster_packed
+ * (recon.py:142-161 -> K.77-112; seeds = packed y*W+x in the order the
+ * sweep met them, written to `seeds` (W*H capacity) when non-null) and the
+ * four phases of recon.parallel_sweeps (recon.py:275-305 -> K.115-190,
+ * single band).  In place on J; *changed_host = any cell changed.  Syncs.
+ * workspace: iwpp_recon_pass_workspace_bytes. */
+enum {
+  IWPP_PASS_RASTER = 0, IWPP_PASS_ANTIRASTER = 1, IWPP_PASS_ROWS_FWD = 2, IWPP_PASS_COLS_FWD = 3,
+  IWPP_PASS_ROWS_BWD = 4, IWPP_PASS_COLS_BWD = 5
+};
+size_t iwpp_recon_pass_workspace_bytes(int64_t W, int64_t H, int dtype);
+int iwpp_recon_pass(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn, int pass,
+                    int64_t *seeds, int64_t *n_seeds_host, int *changed_host, void *workspace,
+                    void *stream);
 /* Full-neighbourhood seed scan (K.193-217): writes active pixels (packed
  * y*W+x, int64, raster order NOT guaranteed) to out; *n_host = count. */
 int iwpp_recon_seed_scan(const void *J, const void *I, int64_t W, int64_t H,

@@ -237,6 +237,29 @@ DEFINE_RECON(uint16_t, u16)
 DEFINE_RECON(int32_t, i32)
 DEFINE_RECON(float, f32)
 
+/* The single passes of recon.py:134-161 and parallel_sweeps
+ * (recon.py:275-305, one band): K.38-112 via the statics above, and the
+ * axis sweeps K.115-190 restated here.  pass: 0 raster, 1 anti-raster (+
+ * seeds), 2 rows forward, 3 columns forward, 4 rows backward, 5 columns
+ * backward.  Returns the seed count (pass 1) and sets *changed. */
+#define DEFINE_PASSES(T, SUF)                                                    /* K.115-126 recon_rows_forward */                                             static int rows_fwd_##SUF(T *J, const T *I, long W, long H) {                    int ch = 0;                                                                    for (long y = 0; y < H; y++)                                                     for (long x = 1; x < W; x++) {                                                   T v = J[y * W + x - 1];                                                        if (v > J[y * W + x]) {                                                          if (v > I[y * W + x]) v = I[y * W + x];                                        if (v > J[y * W + x]) { J[y * W + x] = v; ch = 1; }                          }                                                                            }                                                                            return ch;                                                                   }                                                                              /* K.129-139 recon_rows_backward */                                            static int rows_bwd_##SUF(T *J, const T *I, long W, long H) {                    int ch = 0;                                                                    for (long y = 0; y < H; y++)                                                     for (long x = W - 2; x >= 0; x--) {                                              T v = J[y * W + x + 1];                                                        if (v > J[y * W + x]) {                                                          if (v > I[y * W + x]) v = I[y * W + x];                                        if (v > J[y * W + x]) { J[y * W + x] = v; ch = 1; }                          }                                                                            }                                                                            return ch;                                                                   }                                                                              /* K.142-167 recon_cols_forward / K.170-190 recon_cols_backward (dir)     */   static int cols_##SUF(T *J, const T *I, long W, long H, int conn8, int dir) {    int ch = 0;                                                                    for (long x = 0; x < W; x++)                                                     for (long k = 1; k < H; k++) {                                                   long y = dir > 0 ? k : H - 1 - k, py = y - dir;                                T v = J[py * W + x];                                                           if (conn8) {                                                                     if (x - 1 >= 0 && J[py * W + x - 1] > v) v = J[py * W + x - 1];                if (x + 1 < W && J[py * W + x + 1] > v) v = J[py * W + x + 1];               }                                                                              if (v > J[y * W + x]) {                                                          if (v > I[y * W + x]) v = I[y * W + x];                                        if (v > J[y * W + x]) { J[y * W + x] = v; ch = 1; }                          }                                                                            }                                                                            return ch;                                                                   }                                                                              static long pass_##SUF(T *J, const T *I, long W, long H, int conn8,                                   int pass, int64_t *seeds, int *changed) {                 long n = 0;                                                                    switch (pass) {                                                                  case 0: *changed = raster_pass_##SUF(J, I, W, conn8, 0, 0, W, H); break;       case 1:                                                                          n = antiraster_pass_##SUF(J, I, W, conn8, 0, 0, W, H, seeds,                                             seeds != 0, changed);                                break;                                                                       case 2: *changed = rows_fwd_##SUF(J, I, W, H); break;                          case 3: *changed = cols_##SUF(J, I, W, H, conn8, 1); break;                    case 4: *changed = rows_bwd_##SUF(J, I, W, H); break;                          case 5: *changed = cols_##SUF(J, I, W, H, conn8, -1); break;                   default: return -2;                                                          }                                                                              return n;                                                                    }
+
+DEFINE_PASSES(uint8_t, u8)
+DEFINE_PASSES(uint16_t, u16)
+DEFINE_PASSES(int32_t, i32)
+DEFINE_PASSES(float, f32)
+
+long iwpo_recon_pass(void *J, const void *I, int dtype, long W, long H, int conn8, int pass,
+                     int64_t *seeds, int *changed) {
+  switch (dtype) {
+    case 0: return pass_u8((uint8_t *)J, (const uint8_t *)I, W, H, conn8, pass, seeds, changed);
+    case 1: return pass_u16((uint16_t *)J, (const uint16_t *)I, W, H, conn8, pass, seeds, changed);
+    case 2: return pass_i32((int32_t *)J, (const int32_t *)I, W, H, conn8, pass, seeds, changed);
+    case 3: return pass_f32((float *)J, (const float *)I, W, H, conn8, pass, seeds, changed);
+  }
+  return -2;
+}
+
 /* dtype-dispatching front ends used by the Python wrapper */
 long iwpo_recon_fh(void *J, const void *I, int dtype, long W, long H, int conn8,
                    int64_t *stats) {

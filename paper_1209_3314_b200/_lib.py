@@ -32,7 +32,8 @@ EXPORTS = (
     "iwpp_recon_workspace_bytes", "iwpp_recon", "iwpp_recon_host_workspace_bytes",
     "iwpp_recon_host", "iwpp_recon_engine_counters", "iwpp_check_le", "iwpp_edt_set_engine",
     "iwpp_recon_sweep_rows", "iwpp_recon_sweep_cols",
-    "iwpp_recon_seed_scan", "iwpp_edt_workspace_bytes", "iwpp_edt", "iwpp_edt_propagate",
+    "iwpp_recon_seed_scan", "iwpp_recon_pass_workspace_bytes", "iwpp_recon_pass",
+    "iwpp_edt_workspace_bytes", "iwpp_edt", "iwpp_edt_propagate",
     "iwpp_edt_finalize", "iwpp_edt_host_workspace_bytes", "iwpp_edt_host",
     "iwpp_event_create", "iwpp_event_destroy", "iwpp_event_record", "iwpp_event_elapsed_ms",
     "iwpp_edt_slab_workspace_bytes", "iwpp_edt_slab_init", "iwpp_edt_slab_round",
@@ -56,7 +57,8 @@ class ReconOpts(ctypes.Structure):
                 ("check_contract", ctypes.c_int), ("queue_capacity", ctypes.c_int),
                 ("tile_sweeps", ctypes.c_int), ("halo_sweep_threshold", ctypes.c_int),
                 ("ev_begin", ctypes.c_void_p), ("ev_end", ctypes.c_void_p),
-                ("slab_rows", ctypes.c_int), ("pipeline_rows", ctypes.c_int), ("engine", ctypes.c_int)]
+                ("slab_rows", ctypes.c_int), ("pipeline_rows", ctypes.c_int), ("engine", ctypes.c_int),
+                ("max_rounds", ctypes.c_int)]
 
 
 _lib = None
@@ -90,6 +92,9 @@ def load_library(path: str = LIB_PATH):
             "iwpp_recon_sweep_rows": ([P, P, I64, I64, I, P], I),
             "iwpp_recon_sweep_cols": ([P, P, I64, I64, I, P, P], I),
             "iwpp_recon_seed_scan": ([P, P, I64, I64, I, I, P, ctypes.POINTER(I64), P, P], I),
+            "iwpp_recon_pass_workspace_bytes": ([I64, I64, I], ctypes.c_size_t),
+            "iwpp_recon_pass": ([P, P, I64, I64, I, I, I, P, ctypes.POINTER(I64),
+                                 ctypes.POINTER(I), P, P], I),
             "iwpp_edt_workspace_bytes": ([I64, I64, I], SZ),
             "iwpp_edt": ([P, I64, I64, I, P, P, P, SZ, I64, SP, P], I),
             "iwpp_edt_propagate": ([P, I64, I64, I, P, I64, P, SZ, I64, SP, P], I),

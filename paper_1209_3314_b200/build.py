@@ -13,7 +13,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libiwpp_b200.so")
-SOURCES = ["capi.cu", "recon_tiles.cu", "recon_sweeps.cu", "edt.cu", "edt_block.cu", "edt_slab.cu", "edt_aux.cu", "imgio.cu"]
+SOURCES = ["capi.cu", "recon_tiles.cu", "recon_sweeps.cu", "recon_passes.cu", "edt.cu", "edt_block.cu", "edt_slab.cu", "edt_aux.cu", "imgio.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

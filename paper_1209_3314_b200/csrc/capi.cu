@@ -117,6 +117,7 @@ static int fill_recon_stats(const ReconWs &w, iwpp_stats *stats, cudaStream_t st
   IWPP_CUDA_TRY(cudaStreamSynchronize(st));
   memset(stats, 0, sizeof *stats);
   stats->executions = 1;
+  stats->rounds = (int64_t)c[recon::CNT_ROUNDS];
   stats->tiles_processed = (int64_t)c[recon::CNT_TILES];
   stats->tile_reruns = (int64_t)c[recon::CNT_RERUNS];
   stats->queued_total = (int64_t)c[recon::CNT_PUSHES] + (int64_t)c[recon::CNT_SEEDS];
@@ -184,6 +185,7 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
     eo.ev_begin = opts->ev_begin;
     eo.ev_end = opts->ev_end;
     eo.rows_mode = opts->slab_rows & 3;
+    eo.max_rounds = opts->max_rounds > 0 ? opts->max_rounds : 0;
   }
   if (dtype == IWPP_BIN && recon::tile_side(IWPP_BIN, eo) != recon::TSB)
     dtype = IWPP_U8;  // a byte engine was asked for: 0 / 255 is ordinary grey data
@@ -202,6 +204,13 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
   if (opts && opts->check_contract) {
     if ((rc = recon::check_le(J, I, (size_t)W * H, dtype, &w.counters[recon::CNT_VIOL], st)))
       return rc;
+  }
+  if (eo.max_rounds > 0) {  // the round engine stopped with work left (engine.py:311-317)
+    unsigned long long lim = 0;
+    IWPP_CUDA_TRY(cudaMemcpyAsync(&lim, &w.counters[recon::CNT_LIMIT], sizeof lim,
+                                  cudaMemcpyDeviceToHost, st));
+    IWPP_CUDA_TRY(cudaStreamSynchronize(st));
+    if (lim) return set_error(IWPP_E_ENGINE_LIMIT, "no fixed point within %d rounds", eo.max_rounds);
   }
   if (stats) return fill_recon_stats(w, stats, st);
   return IWPP_OK;
@@ -587,6 +596,60 @@ int iwpp_recon_seed_scan(const void *J, const void *I, int64_t W, int64_t H, int
   IWPP_CUDA_TRY(cudaStreamSynchronize(st));
   *n_host = (int64_t)v;
   return IWPP_OK;
+}
+
+int iwpp_recon_pass(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn, int pass,
+                    int64_t *seeds, int64_t *n_seeds_host, int *changed_host, void *workspace,
+                    void *stream) {
+  int rc = check_dims(W, H);
+  if (rc) return rc;
+  if (conn != 4 && conn != 8)
+    return set_error(IWPP_E_CONTRACT, "connectivity must be 4 or 8, got %d", conn);
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long *ctr = (unsigned long long *)workspace;
+  IWPP_CUDA_TRY(cudaMemsetAsync(ctr, 0, 2 * sizeof *ctr, st));
+  if (dtype == IWPP_F32) {  // the passes on order-preserving ints, converted in place
+    const size_t n = (size_t)W * H;
+    int32_t *Io = (int32_t *)((char *)workspace + 256);
+    if ((rc = recon::f32_to_ord(J, J, n, st))) return rc;
+    if ((rc = recon::f32_to_ord(I, Io, n, st))) return rc;
+    rc = iwpp_recon_pass(J, Io, W, H, IWPP_I32, conn, pass, seeds, n_seeds_host, changed_host,
+                         workspace, stream);
+    const int rc2 = recon::ord_to_f32(J, J, n, st);
+    return rc ? rc : rc2;
+  }
+  switch (pass) {
+    case IWPP_PASS_RASTER:
+      rc = recon::line_pass(J, I, (int)W, (int)H, dtype, conn, 0, nullptr, ctr, st);
+      break;
+    case IWPP_PASS_ANTIRASTER:
+      rc = recon::line_pass(J, I, (int)W, (int)H, dtype, conn, 1, seeds, ctr, st);
+      break;
+    case IWPP_PASS_COLS_FWD:
+      rc = recon::line_pass(J, I, (int)W, (int)H, dtype, conn, 2, nullptr, ctr, st);
+      break;
+    case IWPP_PASS_COLS_BWD:
+      rc = recon::line_pass(J, I, (int)W, (int)H, dtype, conn, 3, nullptr, ctr, st);
+      break;
+    case IWPP_PASS_ROWS_FWD:
+    case IWPP_PASS_ROWS_BWD:
+      rc = recon::sweep_rows(J, I, (int)W, (int)H, dtype, st, pass == IWPP_PASS_ROWS_FWD ? 1 : 2,
+                             ctr);
+      break;
+    default:
+      return set_error(IWPP_E_CONTRACT, "unknown pass %d", pass);
+  }
+  if (rc) return rc;
+  unsigned long long v[2] = {0, 0};
+  IWPP_CUDA_TRY(cudaMemcpyAsync(v, ctr, sizeof v, cudaMemcpyDeviceToHost, st));
+  IWPP_CUDA_TRY(cudaStreamSynchronize(st));
+  if (changed_host) *changed_host = (int)v[0];
+  if (n_seeds_host) *n_seeds_host = (int64_t)v[1];
+  return IWPP_OK;
+}
+
+size_t iwpp_recon_pass_workspace_bytes(int64_t W, int64_t H, int dtype) {
+  return 256 + (dtype == IWPP_F32 ? (size_t)W * H * 4 : 0);
 }
 
 // ---------------------------------------------------------------- EDT

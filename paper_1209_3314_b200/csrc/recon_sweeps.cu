@@ -75,7 +75,8 @@ __device__ __forceinline__ void store_seg(T *Jr, int x0, int W, const int (&j)[V
 
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) row_sweep_kernel(T *__restrict__ J, const T *__restrict__ I,
-                                                        int W, int H) {
+                                                        int W, int H, int dirs,
+                                                        unsigned long long *changed) {
   constexpr int V = VecLoad<T>::V;
   constexpr int SEG = 32 * V;
   const unsigned FULL = 0xffffffffu;
@@ -85,9 +86,10 @@ __global__ void __launch_bounds__(256) row_sweep_kernel(T *__restrict__ J, const
   T *Jr = J + (size_t)row * W;
   const T *Ir = I + (size_t)row * W;
   int j[V], m[V];
+  bool ch = false;
   // forward (west neighbour)
   int carry = INT_MIN;
-  for (int s0 = 0; s0 < W; s0 += SEG) {
+  for (int s0 = 0; s0 < W && (dirs & 1); s0 += SEG) {
     int x0 = s0 + lane * V;
     load_seg<T, VEC>(Jr, Ir, x0, W, j, m);
     int l = INT_MIN, h = INT_MAX;
@@ -114,6 +116,7 @@ __global__ void __launch_bounds__(256) row_sweep_kernel(T *__restrict__ J, const
 #pragma unroll
     for (int e = 0; e < V; e++) {
       v = clampi(v, j[e], m[e]);
+      ch |= v != j[e];
       j[e] = v;
     }
     store_seg<T, VEC>(Jr, x0, W, j);
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(256) row_sweep_kernel(T *__restrict__ J, const
   // backward (east neighbour)
   carry = INT_MIN;
   int nseg = (W + SEG - 1) / SEG;
-  for (int si = nseg - 1; si >= 0; si--) {
+  for (int si = nseg - 1; si >= 0 && (dirs & 2); si--) {
     int x0 = si * SEG + lane * V;
     load_seg<T, VEC>(Jr, Ir, x0, W, j, m);
     int l = INT_MIN, h = INT_MAX;
@@ -150,11 +153,13 @@ __global__ void __launch_bounds__(256) row_sweep_kernel(T *__restrict__ J, const
 #pragma unroll
     for (int e = V - 1; e >= 0; e--) {
       v = clampi(v, j[e], m[e]);
+      ch |= v != j[e];
       j[e] = v;
     }
     store_seg<T, VEC>(Jr, x0, W, j);
     carry = __shfl_sync(FULL, v, 0);
   }
+  if (changed && __any_sync(FULL, ch) && lane == 0) *changed = 1;
 }
 
 // Column sweeps, vertical neighbour (K.142-190; the diagonal terms are left
@@ -303,25 +308,27 @@ static int grid_cap(size_t n, int threads) {
 }
 
 template <typename T>
-static int rows_impl(void *J, const void *I, int W, int H, cudaStream_t st) {
+static int rows_impl(void *J, const void *I, int W, int H, cudaStream_t st, int dirs = 3,
+                     unsigned long long *changed = nullptr) {
   constexpr int V = VecLoad<T>::V;
   bool vec = ((size_t)W * sizeof(T)) % 16 == 0 && ((uintptr_t)J % 16 == 0) && ((uintptr_t)I % 16 == 0);
   (void)V;
   int blocks = (H * 32 + 255) / 256;
   if (vec)
-    row_sweep_kernel<T, true><<<blocks, 256, 0, st>>>((T *)J, (const T *)I, W, H);
+    row_sweep_kernel<T, true><<<blocks, 256, 0, st>>>((T *)J, (const T *)I, W, H, dirs, changed);
   else
-    row_sweep_kernel<T, false><<<blocks, 256, 0, st>>>((T *)J, (const T *)I, W, H);
+    row_sweep_kernel<T, false><<<blocks, 256, 0, st>>>((T *)J, (const T *)I, W, H, dirs, changed);
   IWPP_CUDA_TRY(cudaGetLastError());
   return IWPP_OK;
 }
 
-int sweep_rows(void *J, const void *I, int W, int H, int dtype, cudaStream_t st) {
+int sweep_rows(void *J, const void *I, int W, int H, int dtype, cudaStream_t st, int dirs,
+               unsigned long long *changed) {
   switch (dtype) {
     case IWPP_U8:
-    case IWPP_BIN: return rows_impl<uint8_t>(J, I, W, H, st);
-    case IWPP_U16: return rows_impl<uint16_t>(J, I, W, H, st);
-    case IWPP_I32: return rows_impl<int32_t>(J, I, W, H, st);
+    case IWPP_BIN: return rows_impl<uint8_t>(J, I, W, H, st, dirs, changed);
+    case IWPP_U16: return rows_impl<uint16_t>(J, I, W, H, st, dirs, changed);
+    case IWPP_I32: return rows_impl<int32_t>(J, I, W, H, st, dirs, changed);
   }
   return set_error(IWPP_E_CONTRACT, "unsupported dtype %d", dtype);
 }

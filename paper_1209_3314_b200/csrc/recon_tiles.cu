@@ -1474,7 +1474,8 @@ struct ColourOrder {
 template <int CONN>
 __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     tile_rounds_reg_kernel(EngineArgs a, RoundsArgs r, unsigned long long *counters,
-                           const __grid_constant__ BoxMaps maps, int keep_counters, int rtrace) {
+                           const __grid_constant__ BoxMaps maps, int keep_counters, int rtrace,
+                           int max_rounds) {
   __shared__ TmaWarpSmem tsm[kWarpsPerCta][2];
   __shared__ unsigned s_len;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1638,8 +1639,12 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     }
     __syncthreads();
     n = s_len;
-    if (n == 0) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[CNT_ROUNDS], round + 1);
+    const bool limit = n != 0 && max_rounds > 0 && round + 1 >= (unsigned)max_rounds;
+    if (n == 0 || limit) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        atomicAdd(&counters[CNT_ROUNDS], round + 1);
+        if (limit) counters[CNT_LIMIT] = 1;
+      }
       break;
     }
   }
@@ -2709,7 +2714,8 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
       ra.list1 = ra.list0 + (ntiles + 63) / 64 * 64;
       int kc = o.keep_counters ? 1 : 0;
       static int rtrace = getenv("IWPP_RECON_RTRACE") ? 1 : 0;
-      void *args[] = {&a, &ra, &counters, &maps, &kc, &rtrace};
+      int mr = o.max_rounds;
+      void *args[] = {&a, &ra, &counters, &maps, &kc, &rtrace, &mr};
       IWPP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)tile_rounds_reg_kernel<CONN>, dim3(nb),
                                                 dim3(kCtaThreads), args, 0, st));
       if (rtrace) {  // diagnostics: per-round end times (IWPP_RECON_RTRACE)

@@ -48,6 +48,7 @@ enum {
   CNT_ROUNDS, // round engine: rounds of the last run
   // per-phase SM cycles summed over warps (lane 0's clock; diagnostics)
   CNT_PH_POP = 8, CNT_PH_LOAD, CNT_PH_SWEEP, CNT_PH_DETECT, CNT_PH_BFS, CNT_PH_STORE,
+  CNT_LIMIT = 14,  // round engine: stopped at max_rounds with work left
   CNT_N = 16
 };
 
@@ -78,6 +79,7 @@ struct EngineOpts {
   bool keep_counters = false;   // accumulate into the device counters (no reset)
   int engine = 0;               // ENGINE_AUTO / ENGINE_SMEM / ENGINE_REG / ENGINE_ROUNDS
   int sweeps_set = 0;           // the caller fixed the in-tile sweep count
+  int max_rounds = 0;           // round engine: > 0 caps the rounds (CNT_LIMIT)
 };
 // ENGINE_REG: the register engine on the tile queue; ENGINE_ROUNDS: the
 // register engine in level-synchronous tile rounds (u8; AUTO picks it when

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .engine import EngineConfig
+from .engine import EngineConfig, PropagationRule
 from .errors import ContractViolation, NoBackgroundError
 from .grid import SE8, Coord, Image2D, StructuringElement, is_device_array, pack, unpack
 
@@ -69,6 +69,59 @@ class VoronoiMap:
         if rc not in (_lib.IWPP_OK, _lib.IWPP_E_NO_BACKGROUND):
             _lib.check(rc, "squared_distances")
         return d2.cpu().numpy() if host else d2
+
+
+class DistanceRule(PropagationRule):
+    """Source adoption (edt.py:83-153): p offers its source to q; q takes it
+    when strictly closer, or equally close from a smaller packed index
+    (K.320-336).  Synchronous: offers use the round-start sources.
+    ``tiles.run_pipeline`` runs it on the device round engine; the hooks
+    below state the rule for host-side inspection (numpy ``vr``)."""
+
+    synchronous = True
+
+    def __init__(self, vr, se: StructuringElement, bounds=None):
+        h, w = vr.shape
+        super().__init__(w, h, se, bounds)
+        self.vr = vr
+
+    def sqdist(self, q: int, src: int) -> int:
+        if src < 0:
+            return FAR
+        w = self.width
+        return (q % w - src % w) ** 2 + (q // w - src // w) ** 2
+
+    def closer(self, q: int, cand: int, held: int) -> bool:
+        if cand < 0:
+            return False
+        if held < 0:
+            return True
+        dc, dh = self.sqdist(q, cand), self.sqdist(q, held)
+        return dc < dh or (dc == dh and cand < held)
+
+    def read(self, q):
+        return int(self.vr.reshape(-1)[q])
+
+    def write(self, q, value):
+        self.vr.reshape(-1)[q] = value
+
+    def condition(self, p, q):
+        return self.closer(q, self.read(p), self.read(q))
+
+    def propose(self, p, q):
+        return self.read(p)
+
+    def improves(self, q, old, new):
+        return self.closer(q, int(new), int(old))
+
+    def condition_from(self, v, p, q):
+        return self.closer(q, int(v), self.read(q))
+
+    def propose_from(self, v, p, q):
+        return int(v)
+
+    def rebound(self, bounds) -> "DistanceRule":
+        return DistanceRule(self.vr, self.se, bounds)
 
 
 def _require_binary(mask: Image2D):
@@ -237,14 +290,28 @@ def finalize_distance_map(vmap: VoronoiMap) -> Image2D:
 
 def edt_tiled(mask: Image2D, se: StructuringElement = SE8,
               tile_dims: tuple[int, int] = (64, 64), cfg=None):
-    """edt.py:297-310: cell-for-cell identical to the untiled modes, so one
-    device runs the untiled engine (multi-GPU slabs: tiles.edt_slabs)."""
-    if tile_dims[0] < 1 or tile_dims[1] < 1:
-        raise ContractViolation("tile dimensions must be >= 1")
-    out = edt(mask, se)
-    if cfg is not None:
-        cfg.bp_waves = max(getattr(cfg, "bp_waves", 0), 1)
-    return out
+    """edt.py:297-310: the rule over the pipeline (``tiles.run_pipeline``),
+    cell-for-cell identical to the untiled modes.  One device: init +
+    device rounds.  Under an initialised torch.distributed group (one rank
+    per GPU, every rank passing the full mask) the rounds run as horizontal
+    slabs with one boundary-row exchange per round
+    (``distributed.edt_slabs``); every rank returns the full result."""
+    from .tiles import PipelineConfig, _dist_world, partition, run_pipeline
+
+    _require_binary(mask)
+    world, _ = _dist_world()
+    if world > 1:
+        from .distributed import edt_slabs
+        cfg = cfg or PipelineConfig()
+        partition(mask, *tile_dims)
+        vr, dist = edt_slabs(mask.data, _conn(se))
+        cfg.bp_waves = 1
+        return (VoronoiMap(mask.width, mask.height, vr),
+                Image2D(mask.width, mask.height, "f32", dist))
+    vmap, seeds = init_packed(mask, se)
+    rule = DistanceRule(vmap.vr, se)
+    run_pipeline(vmap, rule, lambda: seeds, tile_dims, cfg)
+    return vmap, finalize_distance_map(vmap)
 
 
 def edt_exact_bruteforce(mask: Image2D) -> Image2D:

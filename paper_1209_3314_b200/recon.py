@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .engine import EngineConfig, RunStats
+from .engine import EngineConfig, PropagationRule, RunStats
 from .errors import ContractViolation
 from .grid import DEVICE_KINDS, SE8, Coord, Image2D, StructuringElement, unpack
 
@@ -59,6 +59,45 @@ class ReconInput:
         return w
 
 
+class ReconRule(PropagationRule):
+    """The reconstruction rule (recon.py:67-128) over packed indices: p
+    raises neighbour q to min(J(p), I(q)) when J(q) < J(p) and q is below
+    its mask.  ``tiles.run_pipeline`` runs it on the device tile engine;
+    the per-cell hooks below state the rule for host-side inspection and
+    small checks (numpy arrays)."""
+
+    def __init__(self, J, I, se: StructuringElement, bounds=None):
+        h, w = J.shape
+        super().__init__(w, h, se, bounds)
+        self.J, self.I = J, I
+
+    def read(self, q):
+        return self.J.reshape(-1)[q]
+
+    def write(self, q, value):
+        self.J.reshape(-1)[q] = value
+
+    def condition(self, p, q):
+        Jf, If = self.J.reshape(-1), self.I.reshape(-1)
+        return Jf[q] < Jf[p] and If[q] != Jf[q]
+
+    def propose(self, p, q):
+        return min(self.J.reshape(-1)[p], self.I.reshape(-1)[q])
+
+    def improves(self, q, old, new):
+        return old < new
+
+    def condition_from(self, v, p, q):
+        Jf, If = self.J.reshape(-1), self.I.reshape(-1)
+        return Jf[q] < v and If[q] != Jf[q]
+
+    def propose_from(self, v, p, q):
+        return min(v, self.I.reshape(-1)[q])
+
+    def rebound(self, bounds) -> "ReconRule":
+        return ReconRule(self.J, self.I, self.se, bounds)
+
+
 def _count_violations(m: Image2D, i: Image2D) -> int:
     if m.elem_kind not in DEVICE_KINDS:
         return int((m.data > i.data).sum())
@@ -79,8 +118,14 @@ ENGINE_AUTO, ENGINE_SMEM, ENGINE_REG, ENGINE_ROUNDS = 0, 1, 2, 3  # iwpp_recon_o
 
 def _opts(cfg: EngineConfig | None, sweeps: int = -1, tile_sweeps: int = -1,
           halo_sweep_threshold: int = -1, max_blocks: int = 0,
-          pipeline_rows: int = 0, engine: int = 0) -> _lib.ReconOpts:
+          pipeline_rows: int = 0, engine: int = 0,
+          max_rounds: int | None = None) -> _lib.ReconOpts:
     o = _lib.ReconOpts()
+    # EngineConfig.max_rounds (engine.py:311-317): the level-synchronous
+    # tile-rounds engine counts rounds; EngineError past the cap
+    o.max_rounds = -1 if max_rounds is None else int(max_rounds)
+    if max_rounds is not None and engine == ENGINE_AUTO:
+        engine = ENGINE_ROUNDS
     o.sweeps = sweeps
     o.max_blocks = max_blocks
     o.check_contract = 0
@@ -98,7 +143,7 @@ def _opts(cfg: EngineConfig | None, sweeps: int = -1, tile_sweeps: int = -1,
 def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
                 sweeps: int = -1, stats: dict | None = None, tile_sweeps: int = -1,
                 halo_sweep_threshold: int = -1, max_blocks: int = 0, pipeline_rows: int = 0,
-                engine: int = 0, kind: str | None = None):
+                engine: int = 0, kind: str | None = None, max_rounds: int | None = None):
     """Reconstruction of raw arrays (numpy -> numpy, CUDA tensor -> tensor).
 
     The marker is not modified.  ``stats`` (a dict) receives the device
@@ -134,7 +179,7 @@ def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
     st = _lib.Stats()
     sp = _lib.ctypes.byref(st) if stats is not None else None
     opts = _opts(cfg, sweeps, tile_sweeps, halo_sweep_threshold, max_blocks, pipeline_rows,
-                 engine)
+                 engine, max_rounds)
     with _lib.device_of(marker, mask):
         if is_device_array(marker):
             J = marker.clone()
@@ -164,7 +209,8 @@ def _run(inp: ReconInput, cfg: EngineConfig | None = None, sweeps: int = -1) -> 
     want_stats = cfg is not None
     d = {} if want_stats else None
     J = reconstruct(inp.marker.data, inp.mask.data, inp.se.connectivity, cfg, sweeps, d,
-                    kind=inp.marker.elem_kind)
+                    kind=inp.marker.elem_kind,
+                    max_rounds=cfg.max_rounds if cfg is not None else None)
     if want_stats:
         cfg.stats.add(d)
     return Image2D(inp.marker.width, inp.marker.height, inp.marker.elem_kind, J)
@@ -197,19 +243,116 @@ def recon_parallel(inp: ReconInput, cfg: EngineConfig | None = None) -> Image2D:
 
 
 def recon_tiled(inp: ReconInput, tile_dims: tuple[int, int] = (64, 64), cfg=None) -> Image2D:
-    """recon.py:308-325.  On one device the tile engine's own 64x64 tiles
-    replace ``tile_dims`` (result identical: unique fixed point).  With a
-    torch.distributed group initialised, see ``tiles.recon_slabs``."""
-    if tile_dims[0] < 1 or tile_dims[1] < 1:
-        raise ContractViolation("tile dimensions must be >= 1")
-    out = _run(inp)
-    if cfg is not None:
-        cfg.bp_waves = max(getattr(cfg, "bp_waves", 0), 1)
-    return out
+    """recon.py:308-325: the rule over the pipeline (``tiles.run_pipeline``)
+    on a working copy of the marker.  One device: the tile engine's own
+    32x32 tiles replace ``tile_dims`` (result identical: unique fixed point,
+    tiles.py:7-9).  Under an initialised torch.distributed group (one rank
+    per GPU, every rank passing the full image) the pipeline runs as
+    horizontal slabs, one per rank, with border-row exchange waves
+    (``distributed.recon_slabs``); every rank returns the full result."""
+    from .tiles import run_pipeline
+
+    if inp.marker.elem_kind not in DEVICE_KINDS:
+        raise ContractViolation(f"no B200 engine for elem_kind {inp.marker.elem_kind!r}")
+    work = inp.working_copy()
+    rule = ReconRule(work.marker.data, work.mask.data, work.se)
+    rule.elem_kind = work.marker.elem_kind
+    run_pipeline(work.marker, rule, lambda: None, tile_dims, cfg)
+    return work.marker
 
 
 # ---------------------------------------------------------------------------
-# scan passes / regional maxima (host helpers kept for API parity)
+# the reference's individual scan passes (recon.py:134-161, 260-305) on the
+# device, cell for cell (libiwpp_b200.so: iwpp_recon_pass)
+
+PASS_RASTER, PASS_ANTIRASTER, PASS_ROWS_FWD, PASS_COLS_FWD, PASS_ROWS_BWD, PASS_COLS_BWD = range(6)
+_PASS_CODES = {np.dtype(np.uint8): 0, np.dtype(np.uint16): 1, np.dtype(np.int32): 2,
+               np.dtype(np.float32): 3}
+
+
+def _run_pass(J, I, conn: int, pas: int, collect: bool = False):
+    """One pass in place on J (numpy or CUDA tensor); returns (changed,
+    seeds or None) with seeds packed y*W+x in the order the sweep met them."""
+    from .grid import np_dtype_of, is_device_array
+    L = _lib.lib()
+    torch = _lib._torch()
+    code = _PASS_CODES.get(np_dtype_of(J))
+    if code is None:
+        raise ContractViolation(f"no device pass for dtype {np_dtype_of(J)}")
+    H, W = J.shape
+    host = not is_device_array(J)
+    with _lib.device_of(J, I):
+        dJ = torch.from_numpy(np.ascontiguousarray(J)).cuda() if host else J
+        dI = torch.from_numpy(np.ascontiguousarray(I)).cuda() if host else I.contiguous()
+        work = dJ if dJ.is_contiguous() else dJ.contiguous()
+        seeds = torch.empty(max(W * H, 1) if collect else 1, dtype=torch.int64, device=work.device)
+        n = _lib.ctypes.c_int64(0)
+        ch = _lib.ctypes.c_int(0)
+        ws = _lib.workspace(L.iwpp_recon_pass_workspace_bytes(W, H, code))
+        _lib.check(L.iwpp_recon_pass(_lib.ptr(work), _lib.ptr(dI), W, H, code, conn, pas,
+                                     _lib.ptr(seeds) if collect else None, _lib.ctypes.byref(n),
+                                     _lib.ctypes.byref(ch), _lib.ptr(ws), _lib.stream_ptr()),
+                   "recon_pass")
+        if work is not dJ:
+            dJ.copy_(work)
+        if host:
+            J[...] = dJ.cpu().numpy()
+    out = seeds[:n.value] if collect else None
+    if collect and host:
+        out = out.cpu().numpy()
+    return bool(ch.value), out
+
+
+def raster_pass(inp: ReconInput) -> bool:
+    """recon.py:134-139 (K.38-74): one in-place top-left to bottom-right
+    sweep of inp.marker; returns whether any cell changed."""
+    return _run_pass(inp.marker.data, inp.mask.data, inp.se.connectivity, PASS_RASTER)[0]
+
+
+def _antiraster_packed(inp: ReconInput, collect_seeds: bool):
+    """recon.py:151-161: (changed, packed seeds) of the mirror sweep."""
+    ch, seeds = _run_pass(inp.marker.data, inp.mask.data, inp.se.connectivity, PASS_ANTIRASTER,
+                          collect_seeds)
+    if seeds is None:
+        seeds = np.empty(0, np.int64)
+    return ch, seeds
+
+
+def antiraster_pass(inp: ReconInput, collect_seeds: bool = False):
+    """recon.py:142-148 (K.77-112): the bottom-right to top-left sweep;
+    returns (changed, seeds as Coord) -- the cells that may still raise a
+    scan-order successor, in the order the sweep met them (empty unless
+    requested)."""
+    ch, packed = _antiraster_packed(inp, collect_seeds)
+    w = inp.marker.width
+    seq = packed.tolist() if not isinstance(packed, np.ndarray) else packed
+    return ch, [unpack(int(p), w) for p in seq]
+
+
+def parallel_sweeps(J, I, se: StructuringElement, n_workers: int = 1, pool=None,
+                    bounds=None) -> None:
+    """recon.py:275-305: rows forward, columns forward, rows backward,
+    columns backward (K.115-190), in place on J.  With several bands the
+    reference's diagonal reads race across band edges (results vary with
+    timing, recon.py:280-286); the device runs the single-band order, one of
+    those outcomes, exactly.  ``bounds`` = (x0, y0, x1, y1) restricts the
+    sweeps to a window (neighbours outside it are not read)."""
+    if n_workers < 1:
+        raise ContractViolation("n_workers must be >= 1")
+    H, W = J.shape
+    x0, y0, x1, y1 = bounds if bounds is not None else (0, 0, W, H)
+    win = (x0, y0, x1, y1) != (0, 0, W, H)
+    Jw, Iw = (J[y0:y1, x0:x1], I[y0:y1, x0:x1]) if win else (J, I)
+    if win:
+        Jw = Jw.copy() if isinstance(Jw, np.ndarray) else Jw.contiguous()
+    for pas in (PASS_ROWS_FWD, PASS_COLS_FWD, PASS_ROWS_BWD, PASS_COLS_BWD):
+        _run_pass(Jw, Iw, se.connectivity, pas)
+    if win:
+        J[y0:y1, x0:x1] = Jw
+
+
+# ---------------------------------------------------------------------------
+# regional maxima (host helper kept for API parity)
 
 def regional_maxima(img: Image2D, se: StructuringElement = SE8) -> list[Coord]:
     """Cells on plateaus with no strictly greater neighbour, raster order

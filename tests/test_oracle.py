@@ -80,3 +80,25 @@ def test_oracle_seed_scan_finds_leftover_work():
     J2 = J.copy()
     oracle.recon_wavefront(J2, I, 8, s)
     assert np.array_equal(J2, oracle.recon_by_dilation(J, I, 8))
+
+
+def test_single_passes_match_reference_golden():
+    """oracle.recon_pass (K.38-190) against the reference's own raster_pass,
+    _antiraster_packed (seeds in sweep order) and one-band parallel_sweeps
+    (tests/golden/make_pass_golden.py)."""
+    g = np.load(os.path.join(GOLD, "pass_golden.npz"))
+    n = len({k[:4] for k in g.files})
+    assert n == 24
+    for c in range(n):
+        p = f"c{c:03d}_"
+        J, I, conn = g[p + "J"], g[p + "I"], int(g[p + "conn"])
+        a = J.copy()
+        ch, _ = oracle.recon_pass(a, I, conn, 0)
+        assert np.array_equal(a, g[p + "raster"]) and ch == bool(g[p + "raster_changed"])
+        ch, seeds = oracle.recon_pass(a, I, conn, 1)
+        assert np.array_equal(a, g[p + "anti"]) and ch == bool(g[p + "anti_changed"])
+        assert np.array_equal(seeds, g[p + "anti_seeds"])
+        b = J.copy()
+        for pas in (2, 3, 4, 5):
+            oracle.recon_pass(b, I, conn, pas)
+        assert np.array_equal(b, g[p + "sweeps"])
