@@ -145,6 +145,14 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W,
 int iwpp_recon_engine_counters(const void *workspace, int64_t W, int64_t H, uint64_t *out,
                                int n, void *stream);
 
+/* Diagnostics (no reference counterpart): the register engine's activation
+ * trace, compiled in only with -DIWPP_ATRACE (development builds; otherwise
+ * returns IWPP_E_CONTRACT).  buf != NULL arms the trace with a device buffer
+ * of cap 32-byte records (recon_tiles.cu ATraceRec) and resets the count;
+ * n_out != NULL receives the number of records written so far.  Returns the
+ * record size. */
+int iwpp_debug_atrace(void *buf, uint32_t cap, uint32_t *n_out);
+
 /* marker <= mask check (recon.py:60): *n_violations_host = count. Syncs. */
 int iwpp_check_le(const void *J, const void *I, int64_t n, int dtype,
                   void *workspace, int64_t *n_violations_host, void *stream);

@@ -39,7 +39,7 @@ EXPORTS = (
     "iwpp_edt_slab_workspace_bytes", "iwpp_edt_slab_init", "iwpp_edt_slab_round",
     "iwpp_edt_slab_finalize", "iwpp_pgm_decode", "iwpp_pgm_encode", "iwpp_gen_marker",
     "iwpp_quantize_u8", "iwpp_edt_init_workspace_bytes", "iwpp_edt_init",
-    "iwpp_edt_exact_workspace_bytes", "iwpp_edt_exact",
+    "iwpp_edt_exact_workspace_bytes", "iwpp_edt_exact", "iwpp_debug_atrace",
 )
 
 
@@ -119,6 +119,7 @@ def load_library(path: str = LIB_PATH):
             "iwpp_edt_init": ([P, I64, I64, I, P, P, ctypes.POINTER(I64), P, SZ, P], I),
             "iwpp_edt_exact_workspace_bytes": ([I64, I64], SZ),
             "iwpp_edt_exact": ([P, I64, I64, P, P, P, SZ, P], I),
+            "iwpp_debug_atrace": ([P, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32)], I),
         }
         for name, (args, res) in proto.items():
             fn = getattr(L, name)

@@ -543,6 +543,10 @@ int iwpp_event_elapsed_ms(void *begin, void *end, float *ms) {
   return IWPP_OK;
 }
 
+int iwpp_debug_atrace(void *buf, uint32_t cap, uint32_t *n_out) {
+  return recon::atrace_control(buf, cap, n_out);
+}
+
 int iwpp_recon_engine_counters(const void *workspace, int64_t W, int64_t H, uint64_t *out,
                                int n, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;

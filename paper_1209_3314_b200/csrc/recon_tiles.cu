@@ -166,12 +166,13 @@ constexpr unsigned kPopMaxSleepNs = IWPP_POP_MAX_SLEEP_NS;
 constexpr unsigned kPendingPollNs = IWPP_PENDING_POLL_NS;
 
 template <unsigned PollNs = kPendingPollNs>
-__device__ __forceinline__ int ring_pop(const TileQueue &q) {
+__device__ __forceinline__ int ring_pop(const TileQueue &q, unsigned long long *idle = nullptr) {
   unsigned ticket = atomicAdd(q.head, 1u);
   unsigned long long *slot = &q.ring[ticket & q.mask];
   for (unsigned ns = 32;; ns = ns < kPopMaxSleepNs ? ns * 2 : kPopMaxSleepNs) {
     unsigned long long v = ld_acquire64(slot);
     if ((unsigned)(v >> 32) == ticket) return (int)(v & 0xffffffffu);
+    if (idle) ++*idle;  // queue-occupancy evidence: polls that found the slot empty
     // the termination test reads the hot pending line: only once the
     // slot has stayed empty for a few polls (PollNs; the binary engine's
     // narrow fronts keep most warps idle and measured best polling at once)
@@ -183,6 +184,34 @@ __device__ __forceinline__ int ring_pop(const TileQueue &q) {
     __nanosleep(ns);
   }
 }
+
+// Activation trace (development builds with -DIWPP_ATRACE; queue-occupancy
+// and concurrency evidence): lane 0 of the register engine appends one
+// record per tile activation -- globaltimer at pop start / tile taken / boxes
+// loaded / fixed point / activation end (ns, low 32 bits), the tile, the
+// SM, the Jacobi steps and the ring depth (tail - ticket) seen at the pop.
+struct ATraceRec {
+  unsigned t_pop, t_take, t_load, t_fix, t_end, tile, sm_steps, depth;
+};
+#ifdef IWPP_ATRACE
+__device__ ATraceRec *g_atrace;
+__device__ unsigned g_atrace_n, g_atrace_cap;
+__device__ __forceinline__ unsigned gtime32() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (unsigned)t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+constexpr bool kATrace = true;
+#else
+__device__ __forceinline__ unsigned gtime32() { return 0; }
+__device__ __forceinline__ unsigned smid() { return 0; }
+constexpr bool kATrace = false;
+#endif
 
 // Tile state bits: Q = queued, or re-run requested while running; R =
 // running; V = never processed (set only by the initial fill).
@@ -1200,17 +1229,27 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
   const bool edge = lane == 0 || lane == 31;
   const int sel = lane == 31;
   RegWarpSmem &ws = wsm[threadIdx.x >> 5];
-  unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0;
+  unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0, n_idle = 0;
   unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
   int next_tile = -1;
   for (;;) {
     long long c_pop = pclock(l0);
+    ATraceRec rec;
+    if (kATrace) {
+      rec.t_pop = gtime32();
+      rec.depth = kATrace && l0 ? *(volatile unsigned *)a.q.tail - *(volatile unsigned *)a.q.head : 0u;
+    }
     int t = -1;
     if (l0) {
-      t = next_tile >= 0 ? next_tile : ring_pop(a.q);
+      t = next_tile >= 0 ? next_tile : ring_pop(a.q, &n_idle);
       if (t >= 0) state_take(&a.q.state[t]);
     }
     t = __shfl_sync(FULL, t, 0);
+    if (kATrace) {
+      rec.t_take = gtime32();
+      rec.tile = (unsigned)t | (next_tile >= 0 ? 0x80000000u : 0u);  // top bit: continuation
+      rec.sm_steps = smid() << 16;
+    }
     next_tile = -1;
     if (t < 0) break;
     int tx, ty;
@@ -1256,6 +1295,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     unsigned obl = j[0] & 0xffu, obr = j[7] >> 24;
     __syncwarp();
     if (kPhases && l0) ph[1] += clock64() - c_load;
+    if (kATrace) rec.t_load = gtime32();
     bool rerun = false;
     for (;;) {  // re-run while neighbours request it
       n_tiles += l0;
@@ -1264,6 +1304,10 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
       bool changed = false;
       const int steps = reg_fixpoint<CONN>(j, m, h, lane, changed);
       if (l0) n_steps += steps;
+      if (kATrace) {
+        rec.t_fix = gtime32();
+        rec.sm_steps += steps;
+      }
       changed = __any_sync(FULL, changed);
       long long c_st = pclock(l0);
       if (kPhases && l0) ph[2] += c_st - c_fix;
@@ -1371,6 +1415,13 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
       }
       done = __shfl_sync(FULL, done, 0);
       if (kPhases && l0) ph[5] += clock64() - c_st;
+#ifdef IWPP_ATRACE
+      if (l0 && done) {
+        rec.t_end = gtime32();
+        const unsigned i = atomicAdd(&g_atrace_n, 1u);
+        if (i < g_atrace_cap) g_atrace[i] = rec;
+      }
+#endif
       if (done) break;
       if (use_tma) {  // the interior is ours and current: refresh the J halo only
         tma_stage(tmJ, tmI, ts, x0, y0, false, tphase, lane);
@@ -1390,6 +1441,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     atomicAdd(&counters[CNT_TILES], n_tiles);
     atomicAdd(&counters[CNT_RERUNS], n_reruns);
     atomicAdd(&counters[CNT_STEPS], n_steps);
+    atomicAdd(&counters[CNT_IDLE_POLLS], n_idle);
     if (kPhases)
       for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
   }
@@ -2542,6 +2594,25 @@ static bool use_bin_engine(bool binary, const EngineOpts &o) {
 }
 
 bool f32_in_engine(const EngineOpts &o) { return use_reg_engine<int32_t>(o); }
+
+// activation trace control (IWPP_ATRACE builds only; see ATraceRec)
+int atrace_control(void *buf, unsigned cap, unsigned *n_out) {
+#ifdef IWPP_ATRACE
+  if (buf) {
+    ATraceRec *p = (ATraceRec *)buf;
+    unsigned z = 0;
+    if (cudaMemcpyToSymbol(g_atrace, &p, sizeof p) != cudaSuccess ||
+        cudaMemcpyToSymbol(g_atrace_cap, &cap, sizeof cap) != cudaSuccess ||
+        cudaMemcpyToSymbol(g_atrace_n, &z, sizeof z) != cudaSuccess)
+      return IWPP_E_CUDA;
+  }
+  if (n_out && cudaMemcpyFromSymbol(n_out, g_atrace_n, sizeof *n_out) != cudaSuccess) return IWPP_E_CUDA;
+  return (int)sizeof(ATraceRec);
+#else
+  (void)buf, (void)cap, (void)n_out;
+  return IWPP_E_CONTRACT;
+#endif
+}
 
 int tile_side(int dtype, const EngineOpts &o) {
   return use_bin_engine(dtype == IWPP_BIN, o) ? TSB : TS;

@@ -49,6 +49,7 @@ enum {
   // per-phase SM cycles summed over warps (lane 0's clock; diagnostics)
   CNT_PH_POP = 8, CNT_PH_LOAD, CNT_PH_SWEEP, CNT_PH_DETECT, CNT_PH_BFS, CNT_PH_STORE,
   CNT_LIMIT = 14,  // round engine: stopped at max_rounds with work left
+  CNT_IDLE_POLLS = 15,  // register engine: ring polls that found their slot empty
   CNT_N = 16
 };
 
@@ -97,6 +98,8 @@ int run_tile_engine(void *J, const void *I, int W, int H, int dtype, int conn, T
 // side of the square tiles the engine run_tile_engine picks for (dtype, o)
 // works on: sel_lo / sel_hi and the dirty flags count rows of these tiles
 int tile_side(int dtype, const EngineOpts &o);
+// activation trace (development builds with -DIWPP_ATRACE; else IWPP_E_CONTRACT)
+int atrace_control(void *buf, unsigned cap, unsigned *n_out);
 // binary kind: J / I as bit planes (ceil(W/32) words per row) for the engine
 size_t bin_plane_words(int64_t W, int64_t H);
 int bin_pack(const void *src, int W, int H, uint32_t *bits, cudaStream_t st);

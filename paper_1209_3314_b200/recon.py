@@ -356,41 +356,40 @@ def parallel_sweeps(J, I, se: StructuringElement, n_workers: int = 1, pool=None,
 
 def regional_maxima(img: Image2D, se: StructuringElement = SE8) -> list[Coord]:
     """Cells on plateaus with no strictly greater neighbour, raster order
-    (recon.py:211-254).  Host-side helper (not on the hot path)."""
-    from scipy import ndimage
+    (recon.py:211-254).  Host-side helper (not on the hot path).
+
+    One pass for every value at once: the equal-valued neighbour pairs are
+    the edges of a graph whose connected components are the plateaus
+    (scipy.sparse.csgraph), and a plateau is vetoed iff one of its cells
+    has a strictly greater neighbour -- O(pixels), whatever the number of
+    distinct values."""
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
 
     a = img.numpy()
-    struct = np.ones((3, 3), bool) if se.connectivity == 8 else \
-        np.array([[0, 1, 0], [1, 1, 1], [0, 1, 0]], bool)
-    # a plateau is a regional maximum iff none of its cells has a greater
-    # neighbour: label equal-valued components, then veto components that
-    # touch a greater neighbour
     H, W = a.shape
+    n = H * W
+    idx = np.arange(n, dtype=np.int64).reshape(H, W)
     greater = np.zeros(a.shape, bool)
-    P = np.pad(a, 1, mode="edge")
+    src, dst = [], []
     for dx, dy in se.offsets:
-        nb = P[1 + dy:1 + dy + H, 1 + dx:1 + dx + W]
-        valid = np.ones(a.shape, bool)
-        if dy < 0:
-            valid[0, :] = False
-        if dy > 0:
-            valid[-1, :] = False
-        if dx < 0:
-            valid[:, 0] = False
-        if dx > 0:
-            valid[:, -1] = False
-        greater |= valid & (nb > a)
-    keep = np.zeros(a.shape, bool)
-    for v in np.unique(a):
-        lab, k = ndimage.label(a == v, structure=struct)
-        if k == 0:
-            continue
-        bad = np.unique(lab[greater & (lab > 0)])
-        ok = np.ones(k + 1, bool)
-        ok[0] = False
-        ok[bad] = False
-        keep |= ok[lab]
-    ys, xs = np.nonzero(keep)
+        # cells p whose neighbour p + (dx, dy) lies on the image
+        ys = slice(max(0, -dy), H - max(0, dy))
+        xs = slice(max(0, -dx), W - max(0, dx))
+        nys = slice(max(0, dy), H - max(0, -dy))
+        nxs = slice(max(0, dx), W - max(0, -dx))
+        c, nb = a[ys, xs], a[nys, nxs]
+        greater[ys, xs] |= nb > c
+        eq = c == nb
+        src.append(idx[ys, xs][eq])
+        dst.append(idx[nys, nxs][eq])
+    src = np.concatenate(src) if src else np.zeros(0, np.int64)
+    dst = np.concatenate(dst) if dst else np.zeros(0, np.int64)
+    g = coo_matrix((np.ones(src.size, np.int8), (src, dst)), shape=(n, n))
+    k, lab = connected_components(g, directed=False)
+    vetoed = np.bincount(lab, weights=greater.ravel(), minlength=k) > 0
+    keep = ~vetoed[lab]
+    ys, xs = np.divmod(np.nonzero(keep)[0], W)
     return [Coord(int(x), int(y)) for y, x in zip(ys, xs)]
 
 

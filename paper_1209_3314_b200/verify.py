@@ -91,10 +91,39 @@ def _le(a, b, kind) -> bool:
                              Image2D(b.shape[1], b.shape[0], kind, b)) == 0
 
 
+def _dilation_recon(marker, I, conn):
+    """recon_by_dilation (the reference's oracles.py restated with torch
+    pooling ops on the device, none of this package's kernels): repeat
+    J <- min(I, max(J, dilate(J))) until nothing changes.  Small images only
+    (one pass per unit of propagation distance)."""
+    torch = _t()
+    F = torch.nn.functional
+    J, M = marker.to(torch.float32)[None, None], I.to(torch.float32)[None, None]
+    for _ in range(4 * (J.shape[-1] + J.shape[-2]) * 8):
+        if conn == 8:
+            D = F.max_pool2d(J, 3, 1, 1)
+        else:
+            P = F.pad(J, (1, 1, 1, 1), value=-1.0)
+            D = torch.maximum(torch.maximum(P[..., 1:-1, :-2], P[..., 1:-1, 2:]),
+                              torch.maximum(P[..., :-2, 1:-1], P[..., 2:, 1:-1]))
+            D = torch.maximum(D, J)
+        N = torch.minimum(M, D)
+        if torch.equal(N, J):
+            break
+        J = N
+    return J[0, 0].to(marker.dtype)
+
+
 def _fixed_point_ok(marker, J, I, conn, kind="u8") -> bool:
-    """marker <= J <= mask and no seed left (a separate scan kernel)."""
+    """marker <= J <= mask, no seed left (a separate scan kernel), and -- up
+    to 64K pixels -- J equals an independent iterated-dilation
+    reconstruction, which also proves minimality (J = mask passes the first
+    two checks)."""
     n = int(seed_scan(J, I, conn).numel())
-    return _le(marker, J, kind) and _le(J, I, kind) and n == 0
+    ok = _le(marker, J, kind) and _le(J, I, kind) and n == 0
+    if ok and J.numel() <= 65536 and kind in ("u8", "binary"):
+        ok = bool(_t().equal(_dilation_recon(marker, I, conn), J))
+    return ok
 
 
 class _edt_engine:

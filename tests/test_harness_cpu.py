@@ -6,7 +6,7 @@ import json
 
 import pytest
 
-from paper_1209_3314_b200.cli import _parse_dims, build_parser
+from paper_1209_3314_b200.cli import build_parser, dims as _parse_dims
 from paper_1209_3314_b200.errors import ContractViolation
 from paper_1209_3314_b200.experiments import CSV_COLUMNS, EXPERIMENTS, BenchReport, to_csv, to_json
 from paper_1209_3314_b200.verify import SUITES, SuiteResult
