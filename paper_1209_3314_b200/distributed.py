@@ -265,7 +265,7 @@ class SlabEDT:
         h2, W = mask_ext.shape
         self.h, self.W, self.y0, self.H, self.conn = h2 - 2, W, y0, H, conn
         self.has_up, self.has_down = has_up, has_down
-        dev = mask_ext.device
+        dev = self.device = mask_ext.device
         self.ws = torch.empty(self.L.iwpp_edt_slab_workspace_bytes(W, self.h), dtype=torch.uint8,
                               device=dev)
         self.out = [torch.empty(W, dtype=torch.int64, device=dev) for _ in range(2)]
@@ -347,7 +347,7 @@ def run_edt_slab_dist(slab: SlabEDT, group=None, max_rounds: int | None = None) 
     import torch.distributed as dist
 
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    dev = slab.ws.device
+    dev = slab.device
     while True:
         if max_rounds is not None and slab.rounds >= max_rounds:
             from .errors import EngineError
@@ -372,6 +372,37 @@ def run_edt_slab_dist(slab: SlabEDT, group=None, max_rounds: int | None = None) 
             return slab.rounds
 
 
+def finalize_agreed(slab, group=None):
+    """slab.finalize() on every rank, with the ranks agreeing on the outcome
+    before anyone moves on: a rank whose finalize raises (no background,
+    key-range overflow) would otherwise leave the others blocked in the
+    all-gather that follows.  The error codes are all-reduced (max) and
+    every rank raises the same exception."""
+    import torch
+    import torch.distributed as dist
+    from .errors import EngineError, NoBackgroundError
+
+    out, code, msg = None, 0, ""
+    try:
+        out = slab.finalize()
+    except NoBackgroundError as e:
+        code, msg = 1, str(e)
+    except EngineError as e:
+        code, msg = 2, str(e)
+    except RuntimeError as e:  # IWPP_E_OVERFLOW: a d2 beyond the 32-bit key field
+        code, msg = 3, str(e)
+    flag = torch.tensor([code], dtype=torch.int64, device=slab.device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    code = int(flag.item())
+    if code == 1:
+        raise NoBackgroundError(msg or "no background reachable: distance map undefined")
+    if code == 2:
+        raise EngineError(msg or "engine limit reached on another slab")
+    if code == 3:
+        raise RuntimeError(msg or "a squared distance exceeded the 32-bit key range (another slab)")
+    return out
+
+
 def edt_slabs(mask, conn: int = 8, group=None, max_rounds: int | None = None):
     """Distributed EDT: every rank passes the full binary mask; returns the
     full (vr int64, dist f32) on every rank (all-gather)."""
@@ -384,7 +415,7 @@ def edt_slabs(mask, conn: int = 8, group=None, max_rounds: int | None = None):
     dev = torch.device("cuda", torch.cuda.current_device())
     slab = SlabEDT(mask_ext_rows(mask, y0, y1).to(dev), y0, H, rank > 0, rank + 1 < world, conn)
     run_edt_slab_dist(slab, group, max_rounds)
-    vr, dist_ = slab.finalize()
+    vr, dist_ = finalize_agreed(slab, group)
     outs = []
     for t in (vr, dist_):
         hmax = max(b - a for a, b in (slab_bounds(H, world, r) for r in range(world)))
