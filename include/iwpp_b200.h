@@ -259,6 +259,37 @@ int iwpp_edt_slab_round(void *workspace, int64_t W, int64_t h, int64_t y0, int c
 int iwpp_edt_slab_finalize(void *workspace, int64_t W, int64_t h, int64_t y0, int64_t rounds,
                            int64_t *vr, float *dist, void *stream);
 
+/* ---- multi-GPU EDT, device-resident rounds ------------------------------
+ * Replaces the per-round host loop of the slab protocol (tiles.py:305-331,
+ * edt_bp_sweep K.493-522: one boundary exchange per synchronous round) with
+ * one persistent kernel per GPU.  Every rank owns a mailbox (size
+ * iwpp_edt_mg_mailbox_bytes, in its own device memory, zeroed by its owner
+ * before any rank calls iwpp_edt_mg_init); the neighbours write the
+ * boundary frontier items into it and every rank adds its frontier counts,
+ * with system-scope stores / atomics -- so mailbox[] must hold pointers
+ * that are valid on the calling GPU: its own memory, or peer memory mapped
+ * over NVLink (CUDA IPC / symmetric memory).  Several slabs of one GPU
+ * (n_local > 1) run as CTA groups of one launch: the single-GPU form of the
+ * same protocol.  The result is identical to iwpp_edt on the whole image. */
+typedef struct iwpp_edt_mg_slab {
+  void *workspace;    /* iwpp_edt_mg_workspace_bytes(W, h), set up by iwpp_edt_mg_init */
+  int64_t W, h, y0, H;
+  int has_up, has_down, rank, world;
+  void *mailbox[16];  /* every rank's mailbox (rank order), valid on this GPU */
+} iwpp_edt_mg_slab;
+size_t iwpp_edt_mg_workspace_bytes(int64_t W, int64_t h);
+size_t iwpp_edt_mg_mailbox_bytes(int64_t W);
+/* slab init (as iwpp_edt_slab_init) + the initial boundary items into the
+ * neighbours' mailboxes (NULL at the image edge) */
+int iwpp_edt_mg_init(const uint8_t *mask_ext, int64_t W, int64_t h, int64_t y0, int64_t H, int conn,
+                     int has_up, int has_down, void *workspace, void *mailbox_up, void *mailbox_down,
+                     void *stream);
+/* all rounds to the global fixed point; *rounds = rounds run (the same on
+ * every rank).  IWPP_E_ENGINE_LIMIT past max_rounds (< 0: no cap).  Syncs.
+ * The slabs are then finalized with iwpp_edt_slab_finalize(workspace, ...). */
+int iwpp_edt_mg_run(const iwpp_edt_mg_slab *slabs, int n_local, int conn, int64_t max_rounds,
+                    int64_t *rounds, void *stream);
+
 /* Host-buffer variant: mask host -> device, edt, vr/dist device -> host. */
 size_t iwpp_edt_host_workspace_bytes(int64_t W, int64_t H, int conn);
 int iwpp_edt_host(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *vr,

@@ -40,6 +40,7 @@ EXPORTS = (
     "iwpp_edt_slab_finalize", "iwpp_pgm_decode", "iwpp_pgm_encode", "iwpp_gen_marker",
     "iwpp_quantize_u8", "iwpp_edt_init_workspace_bytes", "iwpp_edt_init",
     "iwpp_edt_exact_workspace_bytes", "iwpp_edt_exact", "iwpp_debug_atrace",
+    "iwpp_edt_mg_workspace_bytes", "iwpp_edt_mg_mailbox_bytes", "iwpp_edt_mg_init", "iwpp_edt_mg_run",
 )
 
 
@@ -50,6 +51,14 @@ class Stats(ctypes.Structure):
 
     def as_dict(self) -> dict:
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class MgSlab(ctypes.Structure):
+    """iwpp_edt_mg_slab (include/iwpp_b200.h)."""
+    _fields_ = [("workspace", ctypes.c_void_p), ("W", ctypes.c_int64), ("h", ctypes.c_int64),
+                ("y0", ctypes.c_int64), ("H", ctypes.c_int64), ("has_up", ctypes.c_int),
+                ("has_down", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
+                ("mailbox", ctypes.c_void_p * 16)]
 
 
 class ReconOpts(ctypes.Structure):
@@ -120,6 +129,10 @@ def load_library(path: str = LIB_PATH):
             "iwpp_edt_exact_workspace_bytes": ([I64, I64], SZ),
             "iwpp_edt_exact": ([P, I64, I64, P, P, P, SZ, P], I),
             "iwpp_debug_atrace": ([P, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32)], I),
+            "iwpp_edt_mg_workspace_bytes": ([I64, I64], SZ),
+            "iwpp_edt_mg_mailbox_bytes": ([I64], SZ),
+            "iwpp_edt_mg_init": ([P, I64, I64, I64, I64, I, I, I, P, P, P, P], I),
+            "iwpp_edt_mg_run": ([ctypes.POINTER(MgSlab), I, I, I64, ctypes.POINTER(I64), P], I),
         }
         for name, (args, res) in proto.items():
             fn = getattr(L, name)

@@ -863,4 +863,29 @@ int iwpp_edt_slab_finalize(void *workspace, int64_t W, int64_t h, int64_t y0, in
   return IWPP_OK;
 }
 
+size_t iwpp_edt_mg_workspace_bytes(int64_t W, int64_t h) { return edt::mg_slab_bytes(W, h); }
+size_t iwpp_edt_mg_mailbox_bytes(int64_t W) { return edt::mg_mailbox_bytes(W); }
+
+int iwpp_edt_mg_init(const uint8_t *mask_ext, int64_t W, int64_t h, int64_t y0, int64_t H, int conn,
+                     int has_up, int has_down, void *workspace, void *mailbox_up, void *mailbox_down,
+                     void *stream) {
+  int rc = check_dims(W, h);
+  if (rc) return rc;
+  if (W > 65536 || H > 65536 || y0 < 0 || y0 + h > H)
+    return set_error(IWPP_E_CONTRACT, "bad slab geometry");
+  if (conn != 4 && conn != 8) return set_error(IWPP_E_CONTRACT, "connectivity must be 4 or 8");
+  if ((has_up && !mailbox_up) || (has_down && !mailbox_down))
+    return set_error(IWPP_E_CONTRACT, "a neighbour's mailbox is missing");
+  return edt::mg_init(mask_ext, W, h, y0, H, conn, has_up, has_down, workspace, nullptr,
+                      has_up ? mailbox_up : nullptr, has_down ? mailbox_down : nullptr,
+                      (cudaStream_t)stream);
+}
+
+int iwpp_edt_mg_run(const iwpp_edt_mg_slab *slabs, int n_local, int conn, int64_t max_rounds,
+                    int64_t *rounds, void *stream) {
+  if (!slabs) return set_error(IWPP_E_CONTRACT, "no slabs");
+  if (conn != 4 && conn != 8) return set_error(IWPP_E_CONTRACT, "connectivity must be 4 or 8");
+  return edt::mg_run(slabs, n_local, conn, max_rounds, rounds, (cudaStream_t)stream);
+}
+
 }  // extern "C"

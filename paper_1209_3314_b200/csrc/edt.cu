@@ -453,10 +453,6 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
 
 // ---- raster-frontier key engine ---------------------------------------------
 // rounds whose frontier is smaller than this run as queue rounds (below)
-#ifndef IWPP_RASTER_MIN
-#define IWPP_RASTER_MIN 262144
-#endif
-constexpr unsigned kRasterMinFrontier = IWPP_RASTER_MIN;
 constexpr int kRtraceRounds = 32768;
 __device__ __forceinline__ void rtrace_stamp(const EdtState &s, int r, int slot) {
   if (s.rtrace && blockIdx.x == 0 && threadIdx.x == 0 && r < kRtraceRounds) {

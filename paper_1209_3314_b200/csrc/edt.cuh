@@ -16,6 +16,12 @@ constexpr uint32_t SEED_STAMP = 0xFFFFFFFEu;
 constexpr int kRoundThreads = IWPP_EDT_ROUND_THREADS;
 constexpr int kRoundBlocksPerSm = IWPP_EDT_ROUND_BLOCKS;
 constexpr int kEdtBq = 6144;  // per-block next-frontier buffer (shared memory, 24 KB)
+// rounds whose frontier is smaller than this run as queue rounds (returned
+// atomics + block queues) instead of raster rounds (bitmap + compaction)
+#ifndef IWPP_RASTER_MIN
+#define IWPP_RASTER_MIN 262144
+#endif
+constexpr unsigned kRasterMinFrontier = IWPP_RASTER_MIN;
 
 enum { EC_ROUNDS = 0, EC_VISITS, EC_NINF, EC_LIMIT, EC_FINAL, EC_BAD, EC_RANGE, EC_LASTCHG, EC_N = 8 };
 
@@ -133,6 +139,13 @@ int slab_round(void *ws, int64_t W, int64_t h, int64_t y0, int conn, int64_t r,
                cudaStream_t st);
 int slab_finalize(void *ws, int64_t W, int64_t h, int64_t y0, int64_t rounds, int64_t *vr,
                   float *dist, int64_t *n_inf_host, int64_t *range_err_host, cudaStream_t st);
+// device-resident multi-slab rounds (edt_slab.cu; iwpp_edt_mg_*)
+size_t mg_slab_bytes(int64_t W, int64_t h);
+size_t mg_mailbox_bytes(int64_t W);
+int mg_init(const uint8_t *mask_ext, int64_t W, int64_t h, int64_t y0, int64_t H, int conn, int has_up,
+            int has_down, void *ws, void *mailbox, void *mb_up, void *mb_dn, cudaStream_t st);
+int mg_run(const iwpp_edt_mg_slab *slabs, int nlocal, int conn, long long max_rounds, int64_t *rounds_host,
+           cudaStream_t st);
 EdtState carve_state(Carver &c, int64_t W, int64_t H, bool cas = false);
 int read_counters(const EdtState &s, unsigned long long *c, cudaStream_t st);
 int reset_control(const EdtState &s, cudaStream_t st);

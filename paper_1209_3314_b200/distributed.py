@@ -403,9 +403,16 @@ def finalize_agreed(slab, group=None):
     return out
 
 
-def edt_slabs(mask, conn: int = 8, group=None, max_rounds: int | None = None):
+def edt_slabs(mask, conn: int = 8, group=None, max_rounds: int | None = None,
+              engine: str = "auto"):
     """Distributed EDT: every rank passes the full binary mask; returns the
-    full (vr int64, dist f32) on every rank (all-gather)."""
+    full (vr int64, dist f32) on every rank (all-gather).
+
+    engine="device" runs all rounds in one kernel per GPU with the
+    boundary items and counts going through NVLink mailboxes
+    (run_edt_slab_device); engine="host" runs the per-round host loop
+    (NCCL send/recv + all-reduce per round, run_edt_slab_dist); "auto"
+    takes the device protocol when the symmetric-memory rendezvous works."""
     import torch
     import torch.distributed as dist
 
@@ -413,9 +420,19 @@ def edt_slabs(mask, conn: int = 8, group=None, max_rounds: int | None = None):
     H, W = mask.shape
     y0, y1 = slab_bounds(H, world, rank)
     dev = torch.device("cuda", torch.cuda.current_device())
-    slab = SlabEDT(mask_ext_rows(mask, y0, y1).to(dev), y0, H, rank > 0, rank + 1 < world, conn)
-    run_edt_slab_dist(slab, group, max_rounds)
-    vr, dist_ = finalize_agreed(slab, group)
+    use_dev = engine == "device"
+    if engine == "auto":
+        try:
+            import torch.distributed._symmetric_memory  # noqa: F401
+            use_dev = True
+        except Exception:  # noqa: BLE001 - no symmetric memory in this build
+            use_dev = False
+    if use_dev:
+        vr, dist_, _, _ = run_edt_slab_device(mask, conn, group, max_rounds)
+    else:
+        slab = SlabEDT(mask_ext_rows(mask, y0, y1).to(dev), y0, H, rank > 0, rank + 1 < world, conn)
+        run_edt_slab_dist(slab, group, max_rounds)
+        vr, dist_ = finalize_agreed(slab, group)
     outs = []
     for t in (vr, dist_):
         hmax = max(b - a for a, b in (slab_bounds(H, world, r) for r in range(world)))
@@ -427,3 +444,169 @@ def edt_slabs(mask, conn: int = 8, group=None, max_rounds: int | None = None):
                           for r in range(world)])
         outs.append(full.cpu().numpy() if isinstance(mask, np.ndarray) else full)
     return outs[0], outs[1]
+
+
+# ---------------------------------------------------------------------------
+# EDT, device-resident rounds (iwpp_edt_mg_*: one persistent kernel per GPU,
+# boundary items and frontier counts through per-rank mailboxes)
+
+def _mg_setup(L, mask_ext, W, h, y0, H, conn, rank, world, mailboxes, dev):
+    import torch
+    from . import _lib
+    ws = torch.empty(L.iwpp_edt_mg_workspace_bytes(W, h), dtype=torch.uint8, device=dev)
+    up = _lib.ptr(mailboxes[rank - 1]) if rank > 0 else None
+    dn = _lib.ptr(mailboxes[rank + 1]) if rank + 1 < world else None
+    _lib.check(L.iwpp_edt_mg_init(_lib.ptr(mask_ext), W, h, y0, H, conn, int(rank > 0),
+                                  int(rank + 1 < world), _lib.ptr(ws), up, dn, _lib.stream_ptr()),
+               "edt_mg_init")
+    d = _lib.MgSlab()
+    d.workspace, d.W, d.h, d.y0, d.H = _lib.ptr(ws), W, h, y0, H
+    d.has_up, d.has_down, d.rank, d.world = int(rank > 0), int(rank + 1 < world), rank, world
+    for g, mb in enumerate(mailboxes):
+        d.mailbox[g] = _lib.ptr(mb)
+    return ws, d
+
+
+def _mg_finalize(L, ws, W, h, y0, rounds, dev):
+    import torch
+    from . import _lib
+    vr = torch.empty((h, W), dtype=torch.int64, device=dev)
+    dist = torch.empty((h, W), dtype=torch.float32, device=dev)
+    _lib.check(L.iwpp_edt_slab_finalize(_lib.ptr(ws), W, h, y0, rounds, _lib.ptr(vr), _lib.ptr(dist),
+                                        _lib.stream_ptr()), "edt_slab_finalize")
+    return vr, dist
+
+
+def edt_slabs_local_device(mask, G: int, conn: int = 8, max_rounds: int | None = None,
+                           timing: dict | None = None):
+    """G horizontal slabs of one mask on ONE GPU through the device-resident
+    multi-slab protocol: the slabs are CTA groups of one launch and their
+    mailboxes live in this GPU's memory -- the same kernel, mailbox protocol
+    and count exchange the multi-GPU run uses over NVLink (edt_slabs with
+    engine="device").  Returns (vr, dist, rounds)."""
+    import torch
+    from . import _lib
+    L = _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    m = torch.as_tensor(mask)
+    H, W = m.shape
+    if not 1 <= G <= 16 or G > H:
+        raise ValueError("1 <= G <= min(16, H) slabs")
+    mbb = L.iwpp_edt_mg_mailbox_bytes(W)
+    mailboxes = [torch.zeros(mbb, dtype=torch.uint8, device=dev) for _ in range(G)]
+    keep, descs = [], (_lib.MgSlab * G)()
+    md = m.to(dev)
+    for r in range(G):
+        y0, y1 = slab_bounds(H, G, r)
+        ext = torch.zeros((y1 - y0 + 2, W), dtype=torch.uint8, device=dev)
+        ext[1:-1] = md[y0:y1]
+        if y0 > 0:
+            ext[0] = md[y0 - 1]
+        if y1 < H:
+            ext[-1] = md[y1]
+        ws, d = _mg_setup(L, ext, W, y1 - y0, y0, H, conn, r, G, mailboxes, dev)
+        keep.append((ext, ws))
+        descs[r] = d
+    rounds = _lib.ctypes.c_int64(0)
+    if timing is not None:  # diagnostics: CUDA events around the rounds kernel alone
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+    _lib.check(L.iwpp_edt_mg_run(descs, G, conn, -1 if max_rounds is None else max_rounds,
+                                 _lib.ctypes.byref(rounds), _lib.stream_ptr()), "edt_mg_run")
+    if timing is not None:
+        ev[1].record()
+        ev[1].synchronize()
+        timing["rounds_ms"] = ev[0].elapsed_time(ev[1])
+    parts = [_mg_finalize(L, keep[r][1], W, descs[r].h, descs[r].y0, rounds.value, dev) for r in range(G)]
+    vr = torch.cat([p[0] for p in parts])
+    dist = torch.cat([p[1] for p in parts])
+    if isinstance(mask, np.ndarray):
+        return vr.cpu().numpy(), dist.cpu().numpy(), rounds.value
+    return vr, dist, rounds.value
+
+
+def symmetric_mailboxes(nbytes: int, group=None):
+    """Every rank's mailbox as a tensor valid on this GPU: this rank's own
+    buffer plus the peers' buffers mapped over NVLink (torch symmetric
+    memory, the CUDA IPC rendezvous).  Zeroed, and every rank has zeroed its
+    own before this returns."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+
+    world = dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    buf = symm.empty(nbytes, dtype=torch.uint8, device=dev)
+    buf.zero_()
+    torch.cuda.synchronize()
+    hdl = symm.rendezvous(buf, group if group is not None else dist.group.WORLD)
+    peers = [buf if g == dist.get_rank(group) else hdl.get_buffer(g, (nbytes,), torch.uint8)
+             for g in range(world)]
+    dist.barrier(group=group)
+    return peers, hdl
+
+
+class DeviceSlabEDT:
+    """One rank's slab of a multi-GPU EDT on the device-resident protocol
+    (iwpp_edt_mg_*): ``run()`` zeroes this rank's mailbox, seeds the
+    neighbours' mailboxes with the initial boundary items and runs every
+    round in one kernel; ``finalize()`` returns this rank's (vr, dist) rows,
+    with the ranks agreeing on errors.  ``mask_ext`` = the rank's rows plus
+    one neighbour row above / below (device tensor, zeros past the edge)."""
+
+    def __init__(self, mask_ext, y0: int, H: int, conn: int = 8, group=None, mailboxes=None):
+        import torch
+        import torch.distributed as dist
+        from . import _lib
+        self._lib, self.L = _lib, _lib.lib()
+        self.group = group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.ext = mask_ext
+        self.h, self.W = mask_ext.shape[0] - 2, mask_ext.shape[1]
+        self.y0, self.H, self.conn = y0, H, conn
+        self.device = mask_ext.device
+        if mailboxes is None:
+            mailboxes, self._hdl = symmetric_mailboxes(self.L.iwpp_edt_mg_mailbox_bytes(self.W), group)
+        self.mailboxes = mailboxes
+        self.rounds = 0
+        self.ws = None
+
+    def run(self, max_rounds: int | None = None) -> int:
+        import torch
+        import torch.distributed as dist
+        _lib, L = self._lib, self.L
+        dist.barrier(group=self.group)            # everyone is done with the previous run
+        self.mailboxes[self.rank].zero_()
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)            # all mailboxes are clean
+        self.ws, d = _mg_setup(L, self.ext, self.W, self.h, self.y0, self.H, self.conn, self.rank,
+                               self.world, self.mailboxes, self.device)
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)            # every rank's initial items are in place
+        descs = (_lib.MgSlab * 1)(d)
+        rounds = _lib.ctypes.c_int64(0)
+        _lib.check(L.iwpp_edt_mg_run(descs, 1, self.conn, -1 if max_rounds is None else max_rounds,
+                                     _lib.ctypes.byref(rounds), _lib.stream_ptr()), "edt_mg_run")
+        self.rounds = rounds.value
+        return self.rounds
+
+    def finalize(self):
+        return _mg_finalize(self.L, self.ws, self.W, self.h, self.y0, self.rounds, self.device)
+
+
+def run_edt_slab_device(mask, conn: int = 8, group=None, max_rounds: int | None = None):
+    """One slab per rank, all rounds in one kernel per GPU (no host round
+    trip per round): boundary items and frontier counts go straight into
+    the neighbours' / everyone's mailboxes over NVLink.  Returns (vr rows,
+    dist rows, rounds, (y0, y1)) of this rank."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    H, W = mask.shape
+    y0, y1 = slab_bounds(H, world, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    slab = DeviceSlabEDT(mask_ext_rows(mask, y0, y1).to(dev), y0, H, conn, group)
+    slab.run(max_rounds)
+    vr, dist_ = finalize_agreed(slab, group)
+    return vr, dist_, slab.rounds, (y0, y1)

@@ -121,3 +121,73 @@ def test_edt_virtual_slabs_random_and_thin():
         run_edt_slabs_local(slabs)
         parts = [s.finalize() for s in slabs]
         assert np.array_equal(np.concatenate([p[0].cpu().numpy() for p in parts]), vr_ref)
+
+
+# ---------------------------------------------------------------------------
+# device-resident multi-slab EDT (iwpp_edt_mg_*): all rounds in one kernel,
+# boundary items and frontier counts through the ranks' mailboxes
+
+@pytest.mark.parametrize("conn", [4, 8])
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+def test_edt_mg_local_device_matches_oracle(conn, G):
+    from paper_1209_3314_b200.distributed import edt_slabs_local_device
+    rng = np.random.default_rng(11 + G)
+    masks = [oracle.gen_synthetic_mask(300, 256, 50, 7),                  # blob: ~100 rounds
+             (rng.random((97, 131)) < 0.9).astype(np.uint8) * 255,        # sparse background
+             oracle.gen_nuclei_mask(512, 512, 30.0, 3)]
+    for m in masks:
+        vr_ref, d_ref, (rounds, _) = oracle.edt(m, conn, stats=True)
+        vr, d, r = edt_slabs_local_device(m, G, conn)
+        assert np.array_equal(vr, vr_ref)
+        assert d.tobytes() == d_ref.tobytes()
+        assert r == rounds  # the reference's round count, whatever the cut
+
+
+def test_edt_mg_local_device_4k_blob_rounds():
+    """The bench's 4K blob mask (314 rounds, raster and queue rounds both)
+    over 4 slabs: bit-exact, same rounds."""
+    from paper_1209_3314_b200.distributed import edt_slabs_local_device
+    m = oracle.gen_synthetic_mask(4096, 4096, 50, 7)
+    vr_ref, d_ref, (rounds, _) = oracle.edt(m, 8, stats=True)
+    vr, d, r = edt_slabs_local_device(m, 4, 8)
+    assert r == rounds
+    assert np.array_equal(vr, vr_ref)
+    assert d.tobytes() == d_ref.tobytes()
+
+
+def test_edt_mg_local_device_errors():
+    from paper_1209_3314_b200 import EngineError, NoBackgroundError
+    from paper_1209_3314_b200.distributed import edt_slabs_local_device
+    m = oracle.gen_synthetic_mask(200, 160, 50, 7)
+    with pytest.raises(EngineError):
+        edt_slabs_local_device(m, 3, 8, max_rounds=2)
+    with pytest.raises(NoBackgroundError):
+        edt_slabs_local_device(np.full((64, 48), 255, np.uint8), 2, 8)
+    vr, d, r = edt_slabs_local_device(np.zeros((33, 17), np.uint8), 3, 8)  # all background
+    assert r == 0 and np.array_equal(vr, np.arange(33 * 17).reshape(33, 17))
+
+
+def test_edt_mg_nccl_single_rank_device_protocol():
+    """The multi-GPU driver (symmetric-memory mailboxes, one kernel per GPU)
+    on a one-rank NCCL group."""
+    import torch
+    import torch.distributed as dist
+    from paper_1209_3314_b200.distributed import edt_slabs
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        m = oracle.gen_synthetic_mask(256, 300, 50, 7)
+        vr_ref, d_ref = oracle.edt(m, 8)
+        for engine in ("device", "host"):
+            vr, d = edt_slabs(m, 8, engine=engine)
+            assert np.array_equal(vr, vr_ref), engine
+            assert d.tobytes() == d_ref.tobytes(), engine
+    finally:
+        dist.destroy_process_group()
