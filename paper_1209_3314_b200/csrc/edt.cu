@@ -283,6 +283,91 @@ __global__ void edt_init_key_kernel(const uint8_t *__restrict__ mask, int W, int
   }
 }
 
+// The same init, restructured for whole-slide sizes (the per-cell version
+// spent 105 ms of a 64K^2 EDT: one division per cell and, above all, one
+// global atomic per warp on the seed counter -- ~10^8 atomics on one
+// address when 8% of the cells are contour seeds).  A warp takes a
+// 128-pixel row segment (lane + 32 j, j < 4: every key store instruction
+// writes 32 consecutive cells, 512 contiguous bytes), reads the three mask
+// rows once (neighbours by shuffle, the two edge bytes by lanes 0 / 31) and
+// stages its seeds in a per-warp shared-memory buffer that is flushed with
+// one global atomic per ~384 seeds.
+constexpr int kInitWarps = 8, kInitBuf = 512;
+template <int CONN>
+__global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows_kernel(const uint8_t *__restrict__ mask,
+                                                                            int W, int H, EdtState s) {
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  __shared__ uint32_t buf[kInitWarps][kInitBuf];
+  unsigned nbuf = 0;  // warp-uniform
+  const long long segs_per_row = (W + 127) / 128;
+  const long long nseg = segs_per_row * H;
+  auto flush = [&]() {
+    unsigned base = 0;
+    if (lane == 0 && nbuf) base = atomicAdd(&s.cnt[0], nbuf);
+    base = __shfl_sync(FULL, base, 0);
+    for (unsigned i = lane; i < nbuf; i += 32) s.F[0][base + i] = buf[wib][i];
+    __syncwarp();
+    nbuf = 0;
+  };
+  for (long long g = (long long)blockIdx.x * kInitWarps + wib; g < nseg; g += (long long)gridDim.x * kInitWarps) {
+    const int y = (int)(g / segs_per_row);
+    const int x0 = (int)(g - (long long)y * segs_per_row) * 128;
+    // rows y-1, y, y+1: 4 bytes per lane (x0 + lane + 32 j) + the edge bytes;
+    // outside the image: 0 = background, never a foreground neighbour
+    unsigned v[3][4], eL[3], eR[3];
+#pragma unroll
+    for (int rr = 0; rr < 3; rr++) {
+      const int yy = y + rr - 1;
+      const bool rin = yy >= 0 && yy < H;
+      const uint8_t *row = mask + (size_t)(rin ? yy : 0) * W;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int x = x0 + lane + 32 * j;
+        v[rr][j] = (rin && x < W) ? (unsigned)__ldg(row + x) : 0u;
+      }
+      eL[rr] = (rin && lane == 0 && x0 > 0) ? (unsigned)__ldg(row + x0 - 1) : 0u;
+      eR[rr] = (rin && lane == 31 && x0 + 128 < W) ? (unsigned)__ldg(row + x0 + 128) : 0u;
+      eL[rr] = __shfl_sync(FULL, eL[rr], 0);
+      eR[rr] = __shfl_sync(FULL, eR[rr], 31);
+    }
+    unsigned seeds = 0;  // bit j: pixel j of this lane is a contour seed
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int x = x0 + lane + 32 * j;
+      unsigned l[3], r[3];
+#pragma unroll
+      for (int rr = 0; rr < 3; rr++) {
+        const unsigned up = __shfl_up_sync(FULL, v[rr][j], 1), dn = __shfl_down_sync(FULL, v[rr][j], 1);
+        const unsigned prevw = __shfl_sync(FULL, v[rr][j > 0 ? j - 1 : 0], 31);
+        const unsigned nextw = __shfl_sync(FULL, v[rr][j < 3 ? j + 1 : 3], 0);
+        l[rr] = lane > 0 ? up : (j > 0 ? prevw : eL[rr]);
+        r[rr] = lane < 31 ? dn : (j < 3 ? nextw : eR[rr]);
+      }
+      if (x >= W) continue;
+      const bool bg = v[1][j] == 0;
+      // neighbours off the image were loaded as 0 (never foreground)
+      const bool near = CONN == 8 ? (l[0] | v[0][j] | r[0] | l[1] | r[1] | l[2] | v[2][j] | r[2]) != 0
+                                  : (v[0][j] | l[1] | r[1] | v[2][j]) != 0;
+      const uint32_t yx = ((uint32_t)y << 16) | (uint32_t)x;
+      const unsigned long long k = bg ? (unsigned long long)yx : KINF;
+      reinterpret_cast<ulonglong2 *>(s.keys)[(size_t)y * W + x] = make_ulonglong2(k, k);
+      if (bg && near) seeds |= 1u << j;
+    }
+    // stage the seeds (warp-aggregated), flush before the buffer can overflow
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const bool p = (seeds >> j) & 1u;
+      const unsigned bal = __ballot_sync(FULL, p);
+      if (p) buf[wib][nbuf + __popc(bal & lanemask_lt())] = ((uint32_t)y << 16) | (uint32_t)(x0 + lane + 32 * j);
+      nbuf += __popc(bal);
+    }
+    __syncwarp();
+    if (nbuf > kInitBuf - 128) flush();
+  }
+  flush();
+}
+
 __global__ void edt_import_key_kernel(const int64_t *__restrict__ vr, int W, int H, EdtState s) {
   size_t n = (size_t)W * H;
   for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
@@ -822,10 +907,15 @@ int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, 
   size_t n = (size_t)W * H;
   int g = grid_for(n, 256);
   if (s.keymode) {
+    // row segments of 128 cells, 8 warps per CTA, 8 CTAs per SM
+    const long long nseg = (long long)((W + 127) / 128) * H;
+    long long gb = (nseg + kInitWarps - 1) / kInitWarps;
+    const long long cap = (long long)device_sm_count() * 8;
+    if (gb > cap) gb = cap;
     if (conn == 8)
-      edt_init_key_kernel<8><<<g, 256, 0, st>>>(mask, W, H, s);
+      edt_init_key_rows_kernel<8><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s);
     else
-      edt_init_key_kernel<4><<<g, 256, 0, st>>>(mask, W, H, s);
+      edt_init_key_rows_kernel<4><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s);
   } else {
     if (conn == 8)
       edt_init_kernel<8><<<g, 256, 0, st>>>(mask, W, H, s);

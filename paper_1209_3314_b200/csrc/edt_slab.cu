@@ -324,7 +324,6 @@ int slab_finalize(void *ws, int64_t W, int64_t h, int64_t y0, int64_t rounds, in
 // mailboxes mapped over NVLink (peer pointers).  The code is the same:
 // every mailbox access is system-scoped.
 constexpr int kMgMaxRanks = 16;
-constexpr int kMgLine = 32;  // u32 words per 128-byte line
 
 struct MgSlab {
   Slab s;
