@@ -239,6 +239,33 @@ __global__ void edt_finalize_vr_kernel(const int64_t *__restrict__ vr, int W, in
   if ((threadIdx.x & 31) == 0 && ninf) atomicAdd(&counters[EC_NINF], ninf);
 }
 
+// Key layout: the two key buffers of a cell (round start / being built)
+// either interleaved (16 B per cell: one sector holds both; the queue
+// engine's resync and read then share a sector) or as two planes (a warp's
+// neighbour-key reads -- the raster rounds' main traffic -- then use every
+// byte of the sectors they fetch).  IWPP_KEY_PLANAR selects; one switch for
+// every key kernel (init, import, rounds, finalize).
+#ifndef IWPP_KEY_PLANAR
+#define IWPP_KEY_PLANAR 1
+#endif
+__device__ __forceinline__ unsigned long long *kslot(unsigned long long *K, size_t p, int b, size_t n) {
+#if IWPP_KEY_PLANAR
+  return K + (size_t)b * n + p;
+#else
+  (void)n;
+  return K + 2 * p + b;
+#endif
+}
+__device__ __forceinline__ void kput2(unsigned long long *K, size_t p, size_t n, unsigned long long k) {
+#if IWPP_KEY_PLANAR
+  K[p] = k;
+  K[n + p] = k;
+#else
+  (void)n;
+  reinterpret_cast<ulonglong2 *>(K)[p] = make_ulonglong2(k, k);
+#endif
+}
+
 // ===========================================================================
 // Key engine (default whenever every d^2 fits 32 bits, i.e. up to ~46K^2).
 //
@@ -269,7 +296,7 @@ __global__ void edt_init_key_kernel(const uint8_t *__restrict__ mask, int W, int
       yx = ((uint32_t)py << 16) | (uint32_t)px;
       bool bg = mask[p] == 0;
       unsigned long long k = bg ? (unsigned long long)yx : KINF;  // d2 = 0 for itself
-      reinterpret_cast<ulonglong2 *>(s.keys)[p] = make_ulonglong2(k, k);
+      kput2(s.keys, p, (size_t)W * H, k);
       if (bg) {
 #pragma unroll
         for (int k8 = 0; k8 < Nbr<CONN>::N; k8++) {
@@ -351,7 +378,7 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows_kernel(cons
                                   : (v[0][j] | l[1] | r[1] | v[2][j]) != 0;
       const uint32_t yx = ((uint32_t)y << 16) | (uint32_t)x;
       const unsigned long long k = bg ? (unsigned long long)yx : KINF;
-      reinterpret_cast<ulonglong2 *>(s.keys)[(size_t)y * W + x] = make_ulonglong2(k, k);
+      kput2(s.keys, (size_t)y * W + x, (size_t)W * H, k);
       if (bg && near) seeds |= 1u << j;
     }
     // stage the seeds (warp-aggregated), flush before the buffer can overflow
@@ -386,7 +413,7 @@ __global__ void edt_import_key_kernel(const int64_t *__restrict__ vr, int W, int
         s.counters[EC_RANGE] = 1;
       }
     }
-    reinterpret_cast<ulonglong2 *>(s.keys)[p] = make_ulonglong2(k, k);
+    kput2(s.keys, p, (size_t)W * H, k);
   }
 }
 
@@ -429,6 +456,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
   __shared__ unsigned bq_n, bq_base;
   unsigned long long visits = 0;
   unsigned long long *K = s.keys;
+  const size_t NN = (size_t)W * H;
   int r = 0;
   for (;; r++) {
     unsigned n = ld_acquire(&s.cnt[r % 3]);
@@ -459,8 +487,8 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
         py = (int)(pyx >> 16);
         px = (int)(pyx & 0xffffu);
         size_t p = (size_t)py * W + px;
-        unsigned long long kp = __ldcg(K + 2 * p + kr);
-        atomicMin(K + 2 * p + kw, kp);  // the building key lags on the frontier
+        unsigned long long kp = __ldcg(kslot(K, p, kr, NN));
+        atomicMin(kslot(K, p, kw, NN), kp);  // the building key lags on the frontier
         if (kp != KINF) {
           const uint32_t src = (uint32_t)kp;
           unsigned long long rq[Nbr<CONN>::N], nk[Nbr<CONN>::N];
@@ -469,7 +497,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
           for (int k = 0; k < Nbr<CONN>::N; k++) {  // loads first (independent)
             int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
             bool in = qx >= 0 && qx < W && qy >= 0 && qy < H;
-            rq[k] = in ? __ldcg(K + 2 * ((size_t)qy * W + qx) + kr) : 0ull;
+            rq[k] = in ? __ldcg(kslot(K, (size_t)qy * W + qx, kr, NN)) : 0ull;
           }
 #pragma unroll
           for (int k = 0; k < Nbr<CONN>::N; k++) {
@@ -492,7 +520,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_key_kernel(int W, in
             int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
             unsigned on = (cand >> k) & 1u;
             unsigned long long old =
-                gmem_atomic_min_if(K + 2 * ((size_t)qy * W + qx) + kw, nk[k], on);
+                gmem_atomic_min_if(kslot(K, (size_t)qy * W + qx, kw, NN), nk[k], on);
             if (on && old >= rq[k]) mask |= 1u << k;  // this offer made q change
           }
         }
@@ -578,6 +606,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
   uint32_t *Fb = s.fbits[0];
   unsigned long long visits = 0;
   unsigned long long *K = s.keys;
+  const size_t NN = (size_t)W * H;
   // this CTA's run of bitmap words (phase 2)
   const unsigned per = ((nwords + gridDim.x - 1) / gridDim.x + kRasterWpt - 1) / kRasterWpt * kRasterWpt;
   const unsigned w_lo = min(nwords, blockIdx.x * per), w_hi = min(nwords, w_lo + per);
@@ -620,15 +649,15 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
         if (i < n) {
           const size_t p = (size_t)py * W + px;
           // the cell's key and its neighbours' round-start keys in flight together
-          const unsigned long long kp = __ldcg(K + 2 * p + kr);
+          const unsigned long long kp = __ldcg(kslot(K, p, kr, NN));
           unsigned long long rq[Nbr<CONN>::N], nk[Nbr<CONN>::N];
 #pragma unroll
           for (int k = 0; k < Nbr<CONN>::N; k++) {
             const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
             const bool in = qx >= 0 && qx < W && qy >= 0 && qy < H;
-            rq[k] = in ? __ldcg(K + 2 * ((size_t)qy * W + qx) + kr) : 0ull;
+            rq[k] = in ? __ldcg(kslot(K, (size_t)qy * W + qx, kr, NN)) : 0ull;
           }
-          atomicMin(K + 2 * p + kw, kp);
+          atomicMin(kslot(K, p, kw, NN), kp);
           if (kp != KINF) {
             const uint32_t src = (uint32_t)kp;
             unsigned cand = 0;
@@ -649,7 +678,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
               const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
               const unsigned on = (cand >> k) & 1u;
               const unsigned long long old =
-                  gmem_atomic_min_if(K + 2 * ((size_t)qy * W + qx) + kw, nk[k], on);
+                  gmem_atomic_min_if(kslot(K, (size_t)qy * W + qx, kw, NN), nk[k], on);
               if (on && old >= rq[k]) mask |= 1u << k;
             }
           }
@@ -688,15 +717,15 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
       const int py = (int)(pyx >> 16), px = (int)(pyx & 0xffffu);
       const size_t p = (size_t)py * W + px;
       // the cell's key and its neighbours' round-start keys, all in flight at once
-      const unsigned long long kp = act ? K[2 * p + kr] : KINF;
+      const unsigned long long kp = act ? *kslot(K, p, kr, NN) : KINF;
       unsigned long long rq[Nbr<CONN>::N];
 #pragma unroll
       for (int k = 0; k < Nbr<CONN>::N; k++) {
         const int qx = px + Nbr<CONN>::dx(k), qy = py + Nbr<CONN>::dy(k);
         const bool in = act && qx >= 0 && qx < W && qy >= 0 && qy < H;
-        rq[k] = in ? K[2 * ((size_t)qy * W + qx) + kr] : 0ull;
+        rq[k] = in ? *kslot(K, (size_t)qy * W + qx, kr, NN) : 0ull;
       }
-      if (act) atomicMin(K + 2 * p + kw, kp);  // the building key lags on the frontier (RED)
+      if (act) atomicMin(kslot(K, p, kw, NN), kp);  // the building key lags on the frontier (RED)
       const uint32_t src = (uint32_t)kp;
 #pragma unroll
       for (int k = 0; k < Nbr<CONN>::N; k++) {
@@ -710,7 +739,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
           nk = make_key(qx, qy, src);
         }
         const bool push = kp != KINF && ok && nk < rq[k];  // rq = 0 off the image / inactive
-        if (push) atomicMin(K + 2 * ((size_t)qy * W + qx) + kw, nk);
+        if (push) atomicMin(kslot(K, (size_t)qy * W + qx, kw, NN), nk);
         const unsigned waddr = push ? (unsigned)qy * (unsigned)WW + ((unsigned)qx >> 5) : 0xffffffffu;
         const unsigned grp = __match_any_sync(FULL, waddr);
         const unsigned orb = __reduce_or_sync(grp, push ? (1u << (qx & 31)) : 0u);
@@ -794,7 +823,7 @@ __global__ void edt_finalize_key_kernel(EdtState s, int W, int H, int64_t *vr, f
   unsigned long long ninf = 0;
   for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
        p += (size_t)gridDim.x * blockDim.x) {
-    unsigned long long k = __ldcg(s.keys + 2 * p + fb);
+    unsigned long long k = __ldcg(kslot(s.keys, p, fb, n));
     if (k == KINF) {
       ninf++;
       if (vr) vr[p] = -1;

@@ -2416,10 +2416,21 @@ __device__ __forceinline__ void tile_queue_init(const TileQueue &q, int ntx, int
     cy[c] = (nty - (c >> 1) + 1) / 2;
     base[c] = c == 0 ? 0 : base[c - 1] + cx[c - 1] * cy[c - 1];
   }
+  // banded: the colour order runs band by band (B tile rows, B even), so the
+  // four colour passes over a band find its boxes in L2 on a whole slide
+  const unsigned B = (q.band && q.band < (unsigned)nty) ? q.band : (unsigned)nty;
   for (unsigned t = i; t < ntiles; t += stride) {
     unsigned tx = t % ntx, ty = t / ntx;
     unsigned c = (tx & 1) | ((ty & 1) << 1);
-    unsigned slot = base[c] + (ty >> 1) * cx[c] + (tx >> 1);
+    unsigned slot;
+    if (B == (unsigned)nty) {
+      slot = base[c] + (ty >> 1) * cx[c] + (tx >> 1);
+    } else {
+      const unsigned r0 = ty / B * B, rows = min(B, (unsigned)nty - r0);
+      unsigned bb = 0;
+      for (unsigned k = 0; k < c; k++) bb += cx[k] * ((rows - (k >> 1) + 1) / 2);
+      slot = r0 * (unsigned)ntx + bb + ((ty - r0) >> 1) * cx[c] + (tx >> 1);
+    }
     q.state[t] = ST_Q | ST_V;
     q.ring[slot] = ((unsigned long long)slot << 32) | t;
   }
@@ -2716,6 +2727,26 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   const unsigned long long ntx_m =
       (ntx < (1 << 14) && nty < (1 << 23) && ntiles < (1u << 26)) ? ((1ull << 40) + ntx - 1) / ntx
                                                                   : 0ull;
+  // whole slides: colour order band by band (IWPP_BAND = tile rows per band,
+  // 0 = image-wide).  Auto, when marker + mask exceed 2 x L2: the smallest
+  // band whose colour classes still hold 2x the resident warps (smaller
+  // bands put neighbours in flight together: re-runs), measured 64K^2 u8 c8
+  // 24.9 -> 23.9 ms (band 16), 16K^2 1.55 -> 1.50 ms (band 32 ~ auto 48)
+  {
+    static int band_env = -2;
+    if (band_env == -2) band_env = getenv("IWPP_BAND") ? atoi(getenv("IWPP_BAND")) : -1;
+    const size_t img2 = (size_t)W * H * sizeof(T) * 2;
+    unsigned band = 0;
+    if (band_env >= 0) {
+      band = (unsigned)(band_env & ~1);
+    } else if (img2 > ((size_t)256 << 20) && !use_bin_engine(binary, o)) {  // (bit planes fit L2)
+      const unsigned warps = (unsigned)device_sm_count() * 20u;
+      band = (8u * warps + (unsigned)ntx - 1) / (unsigned)ntx;
+      band = (band + 1) & ~1u;
+      if (band < 8) band = 8;
+    }
+    q.band = band;
+  }
   EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, o.dirty, (W + 31) / 32, q, ntx_m};
   if (o.ev_begin) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_begin, st));
   if (use_bin_engine(binary, o)) {

@@ -59,6 +59,8 @@ struct TileQueue {
   unsigned mask;             // ring capacity - 1
   unsigned *head, *tail, *pending;
   void *tmaps;               // 2 TMA descriptors (register engine), in device memory
+  unsigned band = 0;         // initial queue order: 2x2 colour order within bands of this
+                             // many tile rows (even; 0 = over the whole image)
 };
 
 struct EngineOpts {
