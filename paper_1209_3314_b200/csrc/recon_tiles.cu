@@ -1240,10 +1240,12 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
       rec.depth = kATrace && l0 ? *(volatile unsigned *)a.q.tail - *(volatile unsigned *)a.q.head : 0u;
     }
     int t = -1;
+    unsigned took = 0;  // (diagnostics) the state word the take consumed
     if (l0) {
       t = next_tile >= 0 ? next_tile : ring_pop(a.q, &n_idle);
-      if (t >= 0) state_take(&a.q.state[t]);
+      if (t >= 0) took = state_take(&a.q.state[t]);
     }
+    (void)took;
     t = __shfl_sync(FULL, t, 0);
     if (kATrace) {
       rec.t_take = gtime32();
@@ -1304,6 +1306,17 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
       bool changed = false;
       const int steps = reg_fixpoint<CONN>(j, m, h, lane, changed);
       if (l0) n_steps += steps;
+#ifdef IWPP_COUNT_NOCHANGE
+      // diagnostics: [8] first visits, [9] later activations, [10] re-runs
+      // that changed nothing; [11] later activations that changed something
+      {
+        const bool ch = __any_sync(FULL, changed);
+        if (l0 && !rerun && (took & ST_V)) ph[0] += 1;
+        if (l0 && !rerun && !(took & ST_V)) ph[1] += 1;
+        if (l0 && rerun && !ch) ph[2] += 1;
+        if (l0 && !rerun && !(took & ST_V) && ch) ph[3] += 1;
+      }
+#endif
       if (kATrace) {
         rec.t_fix = gtime32();
         rec.sm_steps += steps;
@@ -1442,6 +1455,9 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     atomicAdd(&counters[CNT_RERUNS], n_reruns);
     atomicAdd(&counters[CNT_STEPS], n_steps);
     atomicAdd(&counters[CNT_IDLE_POLLS], n_idle);
+#ifdef IWPP_COUNT_NOCHANGE
+    for (int i = 0; i < 4; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
+#endif
     if (kPhases)
       for (int i = 0; i < 6; i++) atomicAdd(&counters[CNT_PH_POP + i], ph[i]);
   }

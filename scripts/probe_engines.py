@@ -49,6 +49,6 @@ for n in sizes:
         ntiles = ((n + 31) // 32) ** 2
         print(f"{n}^2 c{conn} engine={eng}: kernel median {np.median(ts):.4f} ms min {min(ts):.4f}; "
               f"activations {cnt[0]} ({cnt[0] / ntiles:.2f}/tile) reruns {cnt[1]} "
-              f"steps/act {cnt[6] / max(cnt[0], 1):.2f} rounds {cnt[7]}; agree={same}", flush=True)
+              f"steps/act {cnt[6] / max(cnt[0], 1):.2f} rounds {cnt[7]} diag {list(cnt)[8:12]}; agree={same}", flush=True)
     del M, I, ws, out, ref
     torch.cuda.empty_cache()
