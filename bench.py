@@ -735,6 +735,11 @@ def whole_slide(dev, rank: int, world: int, flush, peak: float, check: bool = Tr
         except Exception as e:  # noqa: BLE001 - no symmetric memory: host loop
             slab = None
             info["protocol"] = f"host loop per round (NCCL); device protocol unavailable: {type(e).__name__}"
+        okt = torch.tensor([1 if slab is not None else 0], device=dev, dtype=torch.int64)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)  # every rank takes the same protocol
+        if int(okt.item()) == 0 and slab is not None:
+            slab = None
+            info["protocol"] = "host loop per round (NCCL); device protocol unavailable on another rank"
 
         def run():
             info.pop("out", None)

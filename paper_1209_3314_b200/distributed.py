@@ -420,15 +420,21 @@ def edt_slabs(mask, conn: int = 8, group=None, max_rounds: int | None = None,
     H, W = mask.shape
     y0, y1 = slab_bounds(H, world, rank)
     dev = torch.device("cuda", torch.cuda.current_device())
-    use_dev = engine == "device"
-    if engine == "auto":
-        try:
-            import torch.distributed._symmetric_memory  # noqa: F401
-            use_dev = True
-        except Exception:  # noqa: BLE001 - no symmetric memory in this build
-            use_dev = False
-    if use_dev:
-        vr, dist_, _, _ = run_edt_slab_device(mask, conn, group, max_rounds)
+    dslab = None
+    if engine in ("auto", "device"):
+        try:  # the mailbox rendezvous (symmetric memory over NVLink)
+            dslab = DeviceSlabEDT(mask_ext_rows(mask, y0, y1).to(dev), y0, H, conn, group)
+        except Exception:  # noqa: BLE001 - no symmetric memory / peer access here
+            if engine == "device":
+                raise
+        # every rank takes the same protocol
+        ok = torch.tensor([1 if dslab is not None else 0], dtype=torch.int64, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            dslab = None
+    if dslab is not None:
+        dslab.run(max_rounds)
+        vr, dist_ = finalize_agreed(dslab, group)
     else:
         slab = SlabEDT(mask_ext_rows(mask, y0, y1).to(dev), y0, H, rank > 0, rank + 1 < world, conn)
         run_edt_slab_dist(slab, group, max_rounds)
