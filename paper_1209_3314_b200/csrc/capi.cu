@@ -427,15 +427,18 @@ static int recon_host_pipelined(char *out, const char *marker, const char *mask,
     if ((rc = recon::run_tile_engine(dJ, dI, (int)W, (int)y1, dtype, conn, w.q, w.counters, so, st)))
       return rc;
     tr.mark(st, "engine done", k);
-    if (k == 0) continue;
-    // slab k-1 (and, after the last slab, slab k) is final unless a later
-    // run reaches it: clear its flags, then copy it back
-    const int64_t p0 = bnd[k - 1], p1 = k == S - 1 ? H : y0;
+    // slab k as this run left it goes back now: clear its flags first, so
+    // every tile row a later run rewrites (the row above the next cut, and
+    // any raise that runs on upward) is flagged and copied again at the end
+    // (a copy that races with such a run is superseded by that recopy).
+    // Copying right after the slab's own run, not after the next one, takes
+    // one run off the transfer tail.
+    const int64_t p0 = y0, p1 = k == S - 1 ? H : y1;
     IWPP_CUDA_TRY(cudaMemsetAsync(dirty + p0 / TS, 0, (size_t)((p1 + TS - 1) / TS - p0 / TS), st));
     IWPP_CUDA_TRY(cudaEventRecord(hp->ready[k], st));
     IWPP_CUDA_TRY(cudaStreamWaitEvent(hp->d2h, hp->ready[k], 0));
     if ((rc = copy_back(p0, p1))) return rc;
-    tr.mark(hp->d2h, "d2h done", k - 1);
+    tr.mark(hp->d2h, "d2h done", k);
   }
   // tile rows written after their slab was copied: copy them again
   std::vector<uint8_t> flags((size_t)nty);
