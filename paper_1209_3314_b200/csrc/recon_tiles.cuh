@@ -57,10 +57,12 @@ struct TileQueue {
   unsigned *state;           // per-tile state bits (recon_tiles.cu: Q, R, V)
   unsigned long long *ring;  // (pos << 32) | tile
   unsigned mask;             // ring capacity - 1
+  unsigned band = 0;         // initial queue order: 2x2 colour order within bands of this
+                             // many tile rows (even; 0 = over the whole image).  (It sits in
+                             // the padding after `mask`: a larger struct shifts the engines'
+                             // kernel parameters and measurably changed their code.)
   unsigned *head, *tail, *pending;
   void *tmaps;               // 2 TMA descriptors (register engine), in device memory
-  unsigned band = 0;         // initial queue order: 2x2 colour order within bands of this
-                             // many tile rows (even; 0 = over the whole image)
 };
 
 struct EngineOpts {
