@@ -9,6 +9,8 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "edt.cuh"
 #include "iwpp_common.cuh"
 #include "recon_sweeps.cuh"
@@ -17,6 +19,14 @@
 namespace iwpp {
 
 static thread_local char g_err[512] = "";
+
+// NVTX ranges around every public entry point (header-only NVTX 3: free
+// unless a profiler is attached; `ncu --nvtx --nvtx-include "iwpp_recon/"`
+// selects the engine launches of one call)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 constexpr int kMaxSlabs = 256;
 
 int set_error(int status, const char *fmt, ...) {
@@ -130,6 +140,7 @@ static int fill_recon_stats(const ReconWs &w, iwpp_stats *stats, cudaStream_t st
 int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn,
                void *workspace, size_t workspace_bytes, const iwpp_recon_opts *opts,
                iwpp_stats *stats, void *stream) {
+  NvtxRange nvtx_range("iwpp_recon");
   int rc = check_dims(W, H);
   if (rc) return rc;
   if (conn != 4 && conn != 8)
@@ -471,6 +482,7 @@ extern "C" {
 int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, int64_t H,
                     int dtype, int conn, void *workspace, size_t workspace_bytes,
                     const iwpp_recon_opts *opts, iwpp_stats *stats, void *stream) {
+  NvtxRange nvtx_range("iwpp_recon_host");
   int rc = check_dims(W, H);
   if (rc) return rc;
   size_t es = elem_size(dtype);
@@ -608,6 +620,7 @@ int iwpp_recon_seed_scan(const void *J, const void *I, int64_t W, int64_t H, int
 int iwpp_recon_pass(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn, int pass,
                     int64_t *seeds, int64_t *n_seeds_host, int *changed_host, void *workspace,
                     void *stream) {
+  NvtxRange nvtx_range("iwpp_recon_pass");
   int rc = check_dims(W, H);
   if (rc) return rc;
   if (conn != 4 && conn != 8)
@@ -761,6 +774,7 @@ int iwpp_edt_set_engine(int mode) {
 int iwpp_edt(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *vr, float *dist,
              void *workspace, size_t workspace_bytes, int64_t max_rounds, iwpp_stats *stats,
              void *stream) {
+  NvtxRange nvtx_range("iwpp_edt");
   int rc = edt_check(W, H, conn, workspace_bytes, edt::state_bytes(W, H));
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -774,6 +788,7 @@ int iwpp_edt(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *vr, f
 int iwpp_edt_propagate(int64_t *vr, int64_t W, int64_t H, int conn, const int64_t *seeds,
                        int64_t n_seeds, void *workspace, size_t workspace_bytes,
                        int64_t max_rounds, iwpp_stats *stats, void *stream) {
+  NvtxRange nvtx_range("iwpp_edt_propagate");
   int rc = edt_check(W, H, conn, workspace_bytes, edt::state_bytes(W, H));
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -807,6 +822,7 @@ size_t iwpp_edt_host_workspace_bytes(int64_t W, int64_t H, int conn) {
 int iwpp_edt_host(const uint8_t *mask, int64_t W, int64_t H, int conn, int64_t *vr, float *dist,
                   void *workspace, size_t workspace_bytes, int64_t max_rounds, iwpp_stats *stats,
                   void *stream) {
+  NvtxRange nvtx_range("iwpp_edt_host");
   int rc = edt_check(W, H, conn, workspace_bytes, iwpp_edt_host_workspace_bytes(W, H, conn));
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -849,6 +865,7 @@ int iwpp_edt_slab_init(const uint8_t *mask_ext, int64_t W, int64_t h, int64_t y0
 int iwpp_edt_slab_round(void *workspace, int64_t W, int64_t h, int64_t y0, int conn, int64_t r,
                         const uint64_t *halo_up, const uint64_t *halo_dn, uint64_t *out_up,
                         uint64_t *out_dn, int64_t *n_next_host, void *stream) {
+  NvtxRange nvtx_range("iwpp_edt_slab_round");
   return edt::slab_round(workspace, W, h, y0, conn, r, (const unsigned long long *)halo_up,
                          (const unsigned long long *)halo_dn, (unsigned long long *)out_up,
                          (unsigned long long *)out_dn, n_next_host, (cudaStream_t)stream);
@@ -886,6 +903,7 @@ int iwpp_edt_mg_init(const uint8_t *mask_ext, int64_t W, int64_t h, int64_t y0, 
 
 int iwpp_edt_mg_run(const iwpp_edt_mg_slab *slabs, int n_local, int conn, int64_t max_rounds,
                     int64_t *rounds, void *stream) {
+  NvtxRange nvtx_range("iwpp_edt_mg_run");
   if (!slabs) return set_error(IWPP_E_CONTRACT, "no slabs");
   if (conn != 4 && conn != 8) return set_error(IWPP_E_CONTRACT, "connectivity must be 4 or 8");
   return edt::mg_run(slabs, n_local, conn, max_rounds, rounds, (cudaStream_t)stream);
