@@ -13,7 +13,10 @@ run the engine to the fixed point.  Inputs are resident in HBM; the L2
 (126 MB > the 48 MB of state) is flushed between timed steps by writing a
 256 MB buffer outside the timed events.  With N GPUs every rank processes
 its own tile (independent tiles, no data-path collective): weak scaling,
-value = all ranks' pixels / max-over-ranks device time.
+value = all ranks' pixels / max-over-ranks device time.  (N > 1: the
+headline is BASELINE configs[4] instead -- the 64K^2 whole slide as
+horizontal slabs with NCCL border exchange, strong scaling; see
+slide_headline.)
 
 Extra keys: ``e2e`` (the same metric through the host-buffer C-ABI call,
 H2D + D2H inside the timed region), ``roofline`` (the tile-engine kernel vs
@@ -215,6 +218,9 @@ def main():
                     help="skip the 64K^2 whole-slide extras (recon + EDT)")
     ap.add_argument("--whole-slide-only", action="store_true",
                     help="(diagnostics) skip the 4K/16K extras, keep the whole slide")
+    ap.add_argument("--slide-headline", choices=("auto", "on", "off"), default="auto",
+                    help="headline = the 64K^2 whole slide over the ranks' slabs (BASELINE configs[4]); "
+                         "auto: for N > 1 (configs[1], the 4K tile, at N = 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -224,6 +230,9 @@ def main():
 
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    # NCCL's version banner goes to stdout, which must carry only the JSON line
+    if not os.environ.get("IWPP_KEEP_NCCL_DEBUG"):
+        os.environ["NCCL_DEBUG"] = "WARN"
 
     import torch
     import torch.distributed as dist
@@ -237,6 +246,8 @@ def main():
 
     L = _lib.lib()
     dev = torch.device(f"cuda:{local}")
+    if args.slide_headline == "on" or (args.slide_headline == "auto" and world > 1):
+        return slide_headline(args, rank, world, local, dev)
     Jh, Ih = gray_pair(N_PX, rank)
     dJ = torch.from_numpy(Jh).to(dev)
     dI = torch.from_numpy(Ih).to(dev)
@@ -760,6 +771,152 @@ def whole_slide(dev, rank: int, world: int, flush, peak: float, check: bool = Tr
                                          parallelism=f"slabs x{world}", protocol=info["protocol"],
                                          parity_blocks_vs_oracle=all_ok(ok))
     return res
+
+
+def slide_headline(args, rank: int, world: int, local: int, dev):
+    """The N > 1 headline: BASELINE configs[4], the 64K x 64K whole slide
+    (the counter-hash random pair of slide_rows, identical for every N) as
+    horizontal slabs, one per rank, reconstructed by the slab protocol --
+    the tile engine on each slab, changed border rows to the neighbours
+    over NCCL, waves until an all-reduce of the halo changes is 0 (north
+    star; distributed.run_slab_dist).  Strong scaling: the slide is fixed.
+    One step = restore the slab's marker rows + the protocol to the fixed
+    point.  e2e: the same through host buffers -- H2D of the rank's marker
+    and mask rows from pinned memory, the protocol, D2H of its result rows.
+    Parity: every rank compares its rows with a single-GPU reconstruction of
+    the whole slide on its own GPU."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1209_3314_b200 import _lib
+    from paper_1209_3314_b200 import distributed as D
+    from paper_1209_3314_b200.build import LIB
+
+    if not dist.is_initialized():  # (--slide-headline on, one GPU: a one-rank group)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    N = WS_PX
+    y0, y1 = D.slab_bounds(N, world, rank)
+    M, I = slide_rows(y0, y1, N, dev)
+    J = torch.empty_like(M)
+    info = {"waves": []}
+
+    def step():
+        J.copy_(M)
+        slab = D.SlabRecon(J, I, rank > 0, rank + 1 < world, 8, D.device_solver)
+        info["waves"].append(D.run_slab_dist(slab).waves)
+        return slab
+
+    def barrier():
+        dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    info["waves"].clear()
+    ts = []
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):  # 8 GiB of inputs per slide: beyond L2 by itself
+            s0.record()
+            slab = step()
+            s1.record()
+            s1.synchronize()
+            ts.append(s0.elapsed_time(s1))
+    torch.cuda.synchronize()
+    barrier()
+    total = torch.tensor([sum(ts)], device=dev, dtype=torch.float64)
+    dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    total_ms = float(total.item())
+    value = args.steps * N * N / (total_ms / 1e3) / 1e6
+    res = slab.result().clone()
+
+    # e2e: pinned host rows in, protocol, result rows out
+    hM = M.cpu().pin_memory()
+    hI = I.cpu().pin_memory()
+    hO = torch.empty_like(hM).pin_memory()
+    dM, dI = torch.empty_like(M), torch.empty_like(I)
+
+    def e2e_step():
+        dM.copy_(hM, non_blocking=True)
+        dI.copy_(hI, non_blocking=True)
+        slab = D.SlabRecon(dM, dI, rank > 0, rank + 1 < world, 8, D.device_solver)
+        D.run_slab_dist(slab)
+        hO.copy_(slab.result(), non_blocking=True)
+        torch.cuda.synchronize()
+
+    e2e_step()
+    barrier()
+    te = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_step()
+        te.append(time.perf_counter() - t0)
+    barrier()
+    et = torch.tensor([sum(te)], device=dev, dtype=torch.float64)
+    dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_val = args.steps * N * N / float(et.item()) / 1e6
+    e2e_ok = bool(torch.equal(hO.to(dev), res))
+
+    # parity: the slab rows against a single-GPU run of the whole slide
+    ok = None
+    if not args.no_cpu:
+        del hM, hI, hO, dM, dI
+        torch.cuda.empty_cache()
+        Mf, If = slide_rows(0, N, N, dev)
+        import paper_1209_3314_b200 as gw
+        ok = bool(torch.equal(gw.reconstruct(Mf, If, 8)[y0:y1], res)) and e2e_ok
+        del Mf, If
+        t = torch.tensor([0 if ok else 1], device=dev, dtype=torch.int32)
+        dist.all_reduce(t)
+        ok = int(t.item()) == 0
+    peak, peak_kind = measured_peak_gbs()
+    ms = total_ms / args.steps
+    ach = ALG_BYTES_PER_PX * N * N / (ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "Mpx/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (counter-hash uniform mask, marker = max(mask-40, 0); the same slide for every N)",
+        "config": {"workload": "recon_by_dilation 65536x65536 u8 whole slide, 8-connectivity, horizontal "
+                               f"slabs x{world} with NCCL border exchange (BASELINE configs[4])",
+                   "shape": [N, N], "conn": 8, "parallelism": f"slabs x{world}",
+                   "waves_per_step": sorted(set(info["waves"])),
+                   "l2": "inputs (8 GiB per slide) exceed L2; no flush needed"},
+        "clocks": clk.summary(),
+        "e2e": {"value": round(e2e_val, 2), "unit": "Mpx/s",
+                "h2d_bytes_per_step": 2 * N * N, "d2h_bytes_per_step": N * N,
+                "path": "pinned host slab rows -> SlabRecon / run_slab_dist -> host rows (per rank)"},
+        # per step on this rank: the first wave's engine launch (queue built in
+        # the kernel), then the queue-init + engine pair of every later wave
+        "gpu_launches": int(sum(1 + 2 * (w - 1) for w in info["waves"])),
+        "roofline": {"bound": "hbm", "achieved": round(ach, 2), "peak": round(peak * world, 1),
+                     "unit": "GB/s", "frac": round(ach / (peak * world), 4), "traffic": None,
+                     "kernel": "whole step (tile engine waves + exchange), all ranks",
+                     "alg_bytes_per_px": ALG_BYTES_PER_PX,
+                     "peak_kind": f"{peak_kind} x {world} GPUs"},
+        "library": os.path.relpath(LIB, ROOT),
+        "parity_vs_single_gpu": ok,
+    }
+    if not args.no_extras and not args.no_whole_slide:
+        # the whole-slide block of the N = 1 line, at this N: recon (timed as
+        # above, plus waves) and the EDT on the device-resident slab protocol
+        del M, I, J, res, slab
+        torch.cuda.empty_cache()
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        try:
+            ws_line = whole_slide(dev, rank, world, flush, peak, check=not args.no_cpu)
+        except Exception as e:  # the headline line must still print
+            ws_line = {"whole_slide_error": f"{type(e).__name__}: {e}"[:300]}
+        line["whole_slide"] = {"scaling": "strong", "n_gpus": world, **ws_line}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
