@@ -60,6 +60,16 @@ def gray_pair(n: int, seed: int, h: int = H_MARKER):
     return J, I
 
 
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    """The one JSON line, to the real stdout (see main)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def measured_peak_gbs():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -199,7 +209,7 @@ def run_reference(args, rank: int, world: int):
         "e2e": {"value": round(value, 3), "unit": "Mpx/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -223,6 +233,13 @@ def main():
                          "auto: for N > 1 (configs[1], the 4K tile, at N = 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    # stdout carries exactly one JSON line: everything else any library
+    # writes to fd 1 (NCCL / torch banners at communicator creation) goes
+    # to stderr; the line itself goes to the saved stdout (emit())
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -389,7 +406,7 @@ def main():
                 "scaling": "strong", "n_gpus": world, **ws_line}
 
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -799,14 +816,14 @@ def slide_headline(args, rank: int, world: int, local: int, dev):
     N = WS_PX
     y0, y1 = D.slab_bounds(N, world, rank)
     M, I = slide_rows(y0, y1, N, dev)
-    J = torch.empty_like(M)
     info = {"waves": []}
 
-    def step():
-        J.copy_(M)
-        slab = D.SlabRecon(J, I, rank > 0, rank + 1 < world, 8, D.device_solver)
-        info["waves"].append(D.run_slab_dist(slab).waves)
-        return slab
+    slab0 = D.SlabRecon(M, I, rank > 0, rank + 1 < world, 8, D.device_solver)
+
+    def step():  # restore the marker rows (the mask rows stay), then the protocol
+        slab0.reset(M)
+        info["waves"].append(D.run_slab_dist(slab0).waves)
+        return slab0
 
     def barrier():
         dist.barrier()
@@ -905,7 +922,7 @@ def slide_headline(args, rank: int, world: int, local: int, dev):
     if not args.no_extras and not args.no_whole_slide:
         # the whole-slide block of the N = 1 line, at this N: recon (timed as
         # above, plus waves) and the EDT on the device-resident slab protocol
-        del M, I, J, res, slab
+        del M, I, res, slab, slab0
         torch.cuda.empty_cache()
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
         try:
@@ -914,7 +931,7 @@ def slide_headline(args, rank: int, world: int, local: int, dev):
             ws_line = {"whole_slide_error": f"{type(e).__name__}: {e}"[:300]}
         line["whole_slide"] = {"scaling": "strong", "n_gpus": world, **ws_line}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
     return 0
 

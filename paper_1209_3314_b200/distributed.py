@@ -77,6 +77,18 @@ class SlabRecon:
         self.I[1:h + 1] = I_rows
         self.first = True
 
+    def reset(self, J_rows):
+        """Start over from a new marker (same mask): the rows are copied in,
+        the halo rows return to the min(T) sentinel until the next exchange
+        (no reallocation, the mask rows stay)."""
+        h = self.h
+        lo = _LO[_np_dtype(self.J) if self.is_torch else np.dtype(self.J.dtype)]
+        self.J[1:h + 1] = J_rows
+        for r in (0, h + 1):
+            self.J[r] = lo
+            self.I[r] = lo
+        self.first = True
+
     # -- protocol pieces --------------------------------------------------
     def border_rows(self):
         """(my first row, my last row) to send up / down."""
