@@ -726,17 +726,18 @@ static int edt_solve(edt::EdtState &s, void *workspace, int64_t W, int64_t H, in
     Carver c(workspace);
     s = edt::carve_state(c, W, H, attempt == 1);
     if ((rc = edt::reset_control(s, st))) return rc;
+    int r0 = 0;  // 1: round 0 ran inside the init
     if (s.block)
       rc = edt::block_init(mask, vr_in, seeds, n_seeds, (int)W, (int)H, conn, s, st);
     else if (mask)
-      rc = edt::launch_init(mask, (int)W, (int)H, conn, s, st);
+      rc = edt::launch_init(mask, (int)W, (int)H, conn, s, st, &r0);
     else
       rc = edt::launch_import(vr_in, seeds, n_seeds, (int)W, (int)H, s, st);
     if (rc) return rc;
     if (s.block)
       rc = edt::block_rounds((int)W, (int)H, conn, s, (long long)max_rounds, st);
     else
-      rc = edt::launch_rounds((int)W, (int)H, conn, s, (long long)max_rounds, st);
+      rc = edt::launch_rounds((int)W, (int)H, conn, s, (long long)max_rounds, st, r0);
     if (rc) return rc;
     if (s.block && getenv("IWPP_TRACE") && getenv("IWPP_TRACE")[0] == '1') {
       unsigned long long d[16];

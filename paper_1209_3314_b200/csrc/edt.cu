@@ -319,21 +319,34 @@ __global__ void edt_init_key_kernel(const uint8_t *__restrict__ mask, int W, int
 // rows once (neighbours by shuffle, the two edge bytes by lanes 0 / 31) and
 // stages its seeds in a per-warp shared-memory buffer that is flushed with
 // one global atomic per ~384 seeds.
+// ROUND0 (the raster engine's init): round 0 is computed here as well.  Its
+// frontier is exactly the contour seeds, whose sources are themselves, so
+// round 0 gives every foreground cell next to the background the best of its
+// background neighbours -- (d2 = 1, then 2 for 8-conn; the smaller packed
+// index on ties: up, left, right, down; up-left, up-right, down-left,
+// down-right) -- and leaves everything else unchanged; its next frontier is
+// those foreground cells.  Both key planes get the post-round-0 keys and the
+// list goes to F[1] / cnt[1]: the rounds start at r = 1 (K.403-433 rounds and
+// counts unchanged: round 0's frontier size is added to the visits).  The
+// rounds' biggest frontier -- 8% of a nuclei slide -- never becomes a list.
 constexpr int kInitWarps = 8, kInitBuf = 512;
-template <int CONN>
+constexpr unsigned kOff = 0x100u;  // a mask sample outside the image
+template <int CONN, bool ROUND0 = false>
 __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows_kernel(const uint8_t *__restrict__ mask,
                                                                             int W, int H, EdtState s) {
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
   __shared__ uint32_t buf[kInitWarps][kInitBuf];
   unsigned nbuf = 0;  // warp-uniform
+  unsigned long long nseed = 0;  // (ROUND0) round 0's frontier, lane 0's count
+  const int li = ROUND0 ? 1 : 0;  // the list the rounds start from
   const long long segs_per_row = (W + 127) / 128;
   const long long nseg = segs_per_row * H;
   auto flush = [&]() {
     unsigned base = 0;
-    if (lane == 0 && nbuf) base = atomicAdd(&s.cnt[0], nbuf);
+    if (lane == 0 && nbuf) base = atomicAdd(&s.cnt[li], nbuf);
     base = __shfl_sync(FULL, base, 0);
-    for (unsigned i = lane; i < nbuf; i += 32) s.F[0][base + i] = buf[wib][i];
+    for (unsigned i = lane; i < nbuf; i += 32) s.F[li][base + i] = buf[wib][i];
     __syncwarp();
     nbuf = 0;
   };
@@ -351,10 +364,10 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows_kernel(cons
 #pragma unroll
       for (int j = 0; j < 4; j++) {
         const int x = x0 + lane + 32 * j;
-        v[rr][j] = (rin && x < W) ? (unsigned)__ldg(row + x) : 0u;
+        v[rr][j] = (rin && x < W) ? (unsigned)__ldg(row + x) : kOff;
       }
-      eL[rr] = (rin && lane == 0 && x0 > 0) ? (unsigned)__ldg(row + x0 - 1) : 0u;
-      eR[rr] = (rin && lane == 31 && x0 + 128 < W) ? (unsigned)__ldg(row + x0 + 128) : 0u;
+      eL[rr] = (rin && lane == 0 && x0 > 0) ? (unsigned)__ldg(row + x0 - 1) : kOff;
+      eR[rr] = (rin && lane == 31 && x0 + 128 < W) ? (unsigned)__ldg(row + x0 + 128) : kOff;
       eL[rr] = __shfl_sync(FULL, eL[rr], 0);
       eR[rr] = __shfl_sync(FULL, eR[rr], 31);
     }
@@ -373,13 +386,33 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows_kernel(cons
       }
       if (x >= W) continue;
       const bool bg = v[1][j] == 0;
-      // neighbours off the image were loaded as 0 (never foreground)
-      const bool near = CONN == 8 ? (l[0] | v[0][j] | r[0] | l[1] | r[1] | l[2] | v[2][j] | r[2]) != 0
-                                  : (v[0][j] | l[1] | r[1] | v[2][j]) != 0;
+      // foreground = a nonzero sample inside the image (off-image: kOff)
+      auto fg = [](unsigned a) { return (a & 0xffu) != 0u; };
+      const bool near = CONN == 8 ? (fg(l[0]) || fg(v[0][j]) || fg(r[0]) || fg(l[1]) || fg(r[1]) ||
+                                     fg(l[2]) || fg(v[2][j]) || fg(r[2]))
+                                  : (fg(v[0][j]) || fg(l[1]) || fg(r[1]) || fg(v[2][j]));
       const uint32_t yx = ((uint32_t)y << 16) | (uint32_t)x;
-      const unsigned long long k = bg ? (unsigned long long)yx : KINF;
+      unsigned long long k = bg ? (unsigned long long)yx : KINF;
+      if (ROUND0) {
+        if (bg && near) nseed += 1;
+        if (!bg) {  // round 0's offers from the background neighbours
+          const uint32_t yu = (uint32_t)(y - 1) << 16, yc = (uint32_t)y << 16, yd = (uint32_t)(y + 1) << 16;
+          if (v[0][j] == 0) k = (1ull << 32) | (yu | (uint32_t)x);
+          else if (l[1] == 0) k = (1ull << 32) | (yc | (uint32_t)(x - 1));
+          else if (r[1] == 0) k = (1ull << 32) | (yc | (uint32_t)(x + 1));
+          else if (v[2][j] == 0) k = (1ull << 32) | (yd | (uint32_t)x);
+          else if (CONN == 8) {
+            if (l[0] == 0) k = (2ull << 32) | (yu | (uint32_t)(x - 1));
+            else if (r[0] == 0) k = (2ull << 32) | (yu | (uint32_t)(x + 1));
+            else if (l[2] == 0) k = (2ull << 32) | (yd | (uint32_t)(x - 1));
+            else if (r[2] == 0) k = (2ull << 32) | (yd | (uint32_t)(x + 1));
+          }
+          if (k != KINF) seeds |= 1u << j;  // changed in round 0: round 1's frontier
+        }
+      } else if (bg && near) {
+        seeds |= 1u << j;
+      }
       kput2(s.keys, (size_t)y * W + x, (size_t)W * H, k);
-      if (bg && near) seeds |= 1u << j;
     }
     // stage the seeds (warp-aggregated), flush before the buffer can overflow
 #pragma unroll
@@ -393,6 +426,10 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows_kernel(cons
     if (nbuf > kInitBuf - 128) flush();
   }
   flush();
+  if (ROUND0) {  // round 0's frontier size joins the visits (queued_total)
+    for (int o = 16; o; o >>= 1) nseed += __shfl_xor_sync(FULL, nseed, o);
+    if (lane == 0 && nseed) atomicAdd(&s.counters[EC_VISITS], nseed);
+  }
 }
 
 __global__ void edt_import_key_kernel(const int64_t *__restrict__ vr, int W, int H, EdtState s) {
@@ -594,7 +631,7 @@ constexpr unsigned kRasterWpt = 4;  // bitmap words per thread per compaction pa
 // Two grid barriers per round.
 template <int CONN, bool CHECK>
 __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W, int H, EdtState s,
-                                                                          long long max_rounds) {
+                                                                          long long max_rounds, int r0) {
   unsigned bar_g = grid_barrier_gen(&s.bar[kBarGen]);
   const unsigned FULL = 0xffffffffu;
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -610,7 +647,7 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
   // this CTA's run of bitmap words (phase 2)
   const unsigned per = ((nwords + gridDim.x - 1) / gridDim.x + kRasterWpt - 1) / kRasterWpt * kRasterWpt;
   const unsigned w_lo = min(nwords, blockIdx.x * per), w_hi = min(nwords, w_lo + per);
-  int r = 0;
+  int r = r0;  // 1: round 0 ran in the init (edt_init_key_rows_kernel<CONN, true>)
   for (;; r++) {
     const unsigned n = ld_acquire(&s.cnt[r % 3]);
     if (n == 0) break;
@@ -810,8 +847,9 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
     grid_barrier(&s.bar[0], &s.bar[kBarGen], gridDim.x, bar_g);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    s.counters[EC_ROUNDS] = (unsigned long long)r;
-    s.counters[EC_VISITS] = visits;
+    // (r0 = 1 with nothing to do: there were no seeds, so no round 0 either)
+    s.counters[EC_ROUNDS] = (unsigned long long)(r == r0 ? 0 : r);
+    s.counters[EC_VISITS] += visits;  // (+ round 0's frontier, added by the init)
     s.counters[EC_FINAL] = (unsigned long long)(r & 1);
   }
 }
@@ -932,7 +970,9 @@ int reset_control(const EdtState &s, cudaStream_t st) {
   return IWPP_OK;
 }
 
-int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, cudaStream_t st) {
+int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, cudaStream_t st,
+                int *r0) {
+  if (r0) *r0 = 0;
   size_t n = (size_t)W * H;
   int g = grid_for(n, 256);
   if (s.keymode) {
@@ -941,10 +981,17 @@ int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, 
     long long gb = (nseg + kInitWarps - 1) / kInitWarps;
     const long long cap = (long long)device_sm_count() * 8;
     if (gb > cap) gb = cap;
+    // the raster engine takes round 0 from the init (IWPP_EDT_ROUND0=0: off)
+    static int round0_env = -1;
+    if (round0_env < 0) round0_env = getenv("IWPP_EDT_ROUND0") ? atoi(getenv("IWPP_EDT_ROUND0")) : 1;
+    const bool round0 = s.raster && round0_env && r0;
+    if (round0) *r0 = 1;
     if (conn == 8)
-      edt_init_key_rows_kernel<8><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s);
+      round0 ? edt_init_key_rows_kernel<8, true><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s)
+             : edt_init_key_rows_kernel<8><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s);
     else
-      edt_init_key_rows_kernel<4><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s);
+      round0 ? edt_init_key_rows_kernel<4, true><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s)
+             : edt_init_key_rows_kernel<4><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s);
   } else {
     if (conn == 8)
       edt_init_kernel<8><<<g, 256, 0, st>>>(mask, W, H, s);
@@ -977,7 +1024,7 @@ int launch_import(const int64_t *vr, const int64_t *seeds, int64_t n_seeds, int 
 }
 
 int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_rounds,
-                  cudaStream_t st) {
+                  cudaStream_t st, int r0) {
   const int qm = g_engine_override == ENGINE_QUEUE_PF ? QM_PF
                  : g_engine_override == ENGINE_QUEUE_NAIVE ? QM_NAIVE : QM_BQ;
   if (s.raster) {  // the raster-frontier engine
@@ -998,7 +1045,7 @@ int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_round
     IWPP_CUDA_TRY(cudaMemsetAsync(s.fbits[0], 0, sizeof(uint32_t) * ((W + 31) / 32) * (size_t)H, st));
     int w = W, h = H;
     EdtState ss = s;
-    void *args[] = {&w, &h, &ss, &max_rounds};
+    void *args[] = {&w, &h, &ss, &max_rounds, &r0};
     static unsigned long long *rtrace = nullptr;  // diagnostics: IWPP_EDT_RTRACE=1
     const char *tr = getenv("IWPP_EDT_RTRACE");
     if (tr && tr[0] == '1') {

@@ -149,11 +149,14 @@ int mg_run(const iwpp_edt_mg_slab *slabs, int nlocal, int conn, long long max_ro
 EdtState carve_state(Carver &c, int64_t W, int64_t H, bool cas = false);
 int read_counters(const EdtState &s, unsigned long long *c, cudaStream_t st);
 int reset_control(const EdtState &s, cudaStream_t st);
-int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, cudaStream_t st);
+// r0 (out, may be null): 1 when round 0 ran in the init (raster engine) --
+// then launch_rounds must start at r0
+int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, cudaStream_t st,
+                int *r0 = nullptr);
 int launch_import(const int64_t *vr, const int64_t *seeds, int64_t n_seeds, int W, int H,
                   const EdtState &s, cudaStream_t st);
 int launch_rounds(int W, int H, int conn, const EdtState &s, long long max_rounds,
-                  cudaStream_t st);
+                  cudaStream_t st, int r0 = 0);
 int launch_finalize_auto(const EdtState &s, int W, int H, int64_t *vr, float *dist, int64_t *d2,
                          cudaStream_t st);
 // block engine (edt_block.cu)
