@@ -18,6 +18,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROF = os.path.join(ROOT, "profiles")
 SRC = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "r02")
+TAG = sys.argv[2] if len(sys.argv) > 2 else "r02"  # output prefix (r02b: the re-captures)
 
 KEYS = [
     ("gpu__time_duration.sum", "time"),
@@ -102,8 +103,8 @@ def main():
     os.makedirs(PROF, exist_ok=True)
     summary_path = os.path.join(PROF, "ncu_summary.json")
     summary = json.load(open(summary_path)) if os.path.exists(summary_path) else {}
-    lines = ["# Round-2 ncu captures (B200, --set full + L2 atomic counters, --clock-control none;",
-             "# scripts/prof_r02.sh, workloads scripts/prof_r02.py). One block per captured launch.", ""]
+    lines = [f"# Round-2 ncu captures ({TAG}; B200, --set full + L2 atomic counters, --clock-control none;",
+             "# scripts/prof_r02.sh / prof_r02b.sh, workloads scripts/prof_r02.py). One block per captured launch.", ""]
     for f in sorted(os.listdir(SRC)):
         if not f.endswith(".raw.csv"):
             continue
@@ -118,7 +119,7 @@ def main():
                 lines.append(f"    {'dram GB/s':24s} {(rb + wb) / (t / 1e3) / 1e9:,.1f}")
             for skey, sub, alg in SUMMARY_KEYS.get(case, []):
                 if sub in d["kernel"]:
-                    ent = {"kernel": d["kernel"][:120], "report": f"r02/{case}",
+                    ent = {"kernel": d["kernel"][:120], "report": f"{TAG}/{case}",
                            "time_ms": t, "dram_bytes_per_launch": int((rb or 0) + (wb or 0)),
                            "l2_atom_requests": val(d, "lts__t_requests_op_atom.sum"),
                            "l2_red_requests": val(d, "lts__t_requests_op_red.sum"),
@@ -134,8 +135,8 @@ def main():
         for ext in (".lines.txt", ".sass.txt"):
             p = os.path.join(SRC, case + ext)
             if os.path.exists(p) and os.path.getsize(p):
-                shutil.copy(p, os.path.join(PROF, f"r02_stalls_{case}{ext.replace('.txt', '')}.txt"))
-    open(os.path.join(PROF, "r02_ncu.txt"), "w").write("\n".join(lines) + "\n")
+                shutil.copy(p, os.path.join(PROF, f"{TAG}_stalls_{case}{ext.replace('.txt', '')}.txt"))
+    open(os.path.join(PROF, f"{TAG}_ncu.txt"), "w").write("\n".join(lines) + "\n")
     json.dump(summary, open(summary_path, "w"), indent=1, sort_keys=True)
     # launch list of the headline bench command
     lp = os.path.join(SRC, "launches.csv")
