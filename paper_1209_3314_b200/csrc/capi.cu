@@ -725,6 +725,10 @@ static int edt_solve(edt::EdtState &s, void *workspace, int64_t W, int64_t H, in
   for (int attempt = 0; attempt < 2; attempt++) {
     Carver c(workspace);
     s = edt::carve_state(c, W, H, attempt == 1);
+    if (!s.keymode && !edt::cas_supported(W, H))  // (a forced CAS run at 65536^2)
+      return set_error(IWPP_E_CONTRACT,
+                       "the 32-bit-source engine has no free 'no source' code at %lld x %lld",
+                       (long long)W, (long long)H);
     if ((rc = edt::reset_control(s, st))) return rc;
     int r0 = 0;  // 1: round 0 ran inside the init
     if (s.block)
