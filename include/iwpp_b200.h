@@ -113,6 +113,10 @@ typedef struct iwpp_recon_opts {
                         of the tile-rounds engine (engine 3; auto picks it when set):
                         IWPP_E_ENGINE_LIMIT if the fixed point needs more.  0 / -1: no cap.
                         Other engines have no rounds and ignore it */
+  const void *marker;/* optional device marker (nullptr: J already holds it).  When set, J is
+                        output only: the u8 register engine copies the marker into J in its
+                        own prologue (one pass less over HBM, one launch less); other paths
+                        copy it first.  May equal J.  iwpp_recon_host ignores it */
 } iwpp_recon_opts;
 
 /* Timing helpers (events live in this library's CUDA runtime). */

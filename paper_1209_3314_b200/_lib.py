@@ -67,7 +67,7 @@ class ReconOpts(ctypes.Structure):
                 ("tile_sweeps", ctypes.c_int), ("halo_sweep_threshold", ctypes.c_int),
                 ("ev_begin", ctypes.c_void_p), ("ev_end", ctypes.c_void_p),
                 ("slab_rows", ctypes.c_int), ("pipeline_rows", ctypes.c_int), ("engine", ctypes.c_int),
-                ("max_rounds", ctypes.c_int)]
+                ("max_rounds", ctypes.c_int), ("marker", ctypes.c_void_p)]
 
 
 _lib = None

@@ -152,6 +152,13 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
   cudaStream_t st = (cudaStream_t)stream;
   Carver c(workspace);
   ReconWs w = carve_recon(c, W, H);
+  // a separate marker: the plain u8 path hands it to the engine (copied in
+  // the fused kernel's prologue); everything else starts from a copy in J
+  const void *msrc = opts && opts->marker != J ? opts->marker : nullptr;
+  if (msrc && !(dtype == IWPP_U8 && (!opts || (opts->sweeps <= 0 && !opts->slab_rows)))) {
+    IWPP_CUDA_TRY(cudaMemcpyAsync(J, msrc, (size_t)W * H * elem_size(dtype), cudaMemcpyDeviceToDevice, st));
+    msrc = nullptr;
+  }
   // f32: the 32-bit register engine orders the float bits as it stages its
   // boxes (no conversion passes); other engine choices run the int32 engine
   // on converted copies
@@ -173,6 +180,7 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
     iwpp_recon_opts o{};
     if (opts) o = *opts;
     else o.sweeps = o.tile_sweeps = o.halo_sweep_threshold = -1;
+    o.marker = nullptr;  // (copied above)
     rc = iwpp_recon(J, Io, W, H, IWPP_I32, conn, workspace, recon_ws_bytes(W, H), &o, stats, stream);
     int rc2 = recon::ord_to_f32(J, J, n, st);
     return rc ? rc : rc2;
@@ -198,6 +206,7 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
     eo.rows_mode = opts->slab_rows & 3;
     eo.max_rounds = opts->max_rounds > 0 ? opts->max_rounds : 0;
   }
+  eo.src = msrc;
   if (dtype == IWPP_BIN && recon::tile_side(IWPP_BIN, eo) != recon::TSB)
     dtype = IWPP_U8;  // a byte engine was asked for: 0 / 255 is ordinary grey data
   if (dtype == IWPP_BIN) {  // the bit-plane engine: pack, propagate, unpack
@@ -522,6 +531,7 @@ int iwpp_recon_host(void *out, const void *marker, const void *mask, int64_t W, 
   if (opts) o = *opts;
   else o.sweeps = o.tile_sweeps = o.halo_sweep_threshold = -1;
   o.check_contract = 0;
+  o.marker = nullptr;  // (the marker is the host buffer, uploaded into dJ)
   int edtype = dtype;
   if (dtype == IWPP_F32) {  // our own device copies: convert in place
     if ((rc = recon::f32_to_ord(dJ, dJ, (size_t)W * H, st))) return rc;

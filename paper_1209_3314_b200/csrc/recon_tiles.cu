@@ -91,6 +91,7 @@ struct EngineArgs {
   int WW;                // binary engine: words per bit-plane row
   TileQueue q;
   unsigned long long ntx_m;  // ceil(2^40 / ntx) (0: divide): tile id -> (tx, ty)
+  const void *M;             // fused init: copy this marker into J first (nullable)
 };
 
 // tile id -> (tx, ty) without an integer division (exact while ntx < 2^14
@@ -1203,6 +1204,34 @@ struct alignas(64) BoxMaps {
 __device__ __forceinline__ void tile_queue_init(const TileQueue &q, int ntx, int nty,
                                                 unsigned long long *counters, int keep);
 
+// fused init with a separate marker: the grid copies it into J before the
+// grid-wide sync (16-byte vectors, 4 in flight per thread; the marker is read
+// once, so streaming loads; J stays in L2 for the first box reads)
+__device__ __forceinline__ void copy_marker(const EngineArgs &a) {
+  const size_t n = (size_t)a.W * a.H;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+  const uint8_t *src = static_cast<const uint8_t *>(a.M);
+  uint8_t *dst = static_cast<uint8_t *>(a.J);
+  size_t done = 0;
+  if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+    const size_t nv = n / 16;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    size_t i = tid;
+    for (; i + 3 * nt < nv; i += 4 * nt) {
+      const uint4 v0 = __ldcs(s4 + i), v1 = __ldcs(s4 + i + nt), v2 = __ldcs(s4 + i + 2 * nt),
+                  v3 = __ldcs(s4 + i + 3 * nt);
+      d4[i] = v0;
+      d4[i + nt] = v1;
+      d4[i + 2 * nt] = v2;
+      d4[i + 3 * nt] = v3;
+    }
+    for (; i < nv; i += nt) d4[i] = __ldcs(s4 + i);
+    done = nv * 16;
+  }
+  for (size_t i = done + tid; i < n; i += nt) dst[i] = src[i];
+}
+
 // fused_init: the launch is cooperative and the kernel builds the initial
 // queue itself (all tiles, INIT_FULL) before one grid-wide sync, instead of
 // a separate init kernel
@@ -1211,6 +1240,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     tile_engine_reg_kernel(EngineArgs a, unsigned long long *counters,
                            const __grid_constant__ BoxMaps maps, int use_tma, int fused_init) {
   if (fused_init) {
+    if (a.M) copy_marker(a);
     tile_queue_init(a.q, a.ntx, a.nty, counters, 0);
     cooperative_groups::this_grid().sync();
   }
@@ -2723,6 +2753,11 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   const int fused_init = IWPP_FUSED_INIT && !use_bin_engine(binary, o) &&
                          use_reg_engine<T>(o) && o.init_mode != INIT_CONTINUE && !o.rows_mode &&
                          !o.keep_counters && ntiles >= kFusedInitMinTiles;
+  // a separate marker (o.src): the fused u8 register engine (not the rounds
+  // engine) copies it in its prologue; every other path copies it here
+  bool src_in_kernel = o.src && fused_init && sizeof(T) == 1 && !use_bin_engine(binary, o);
+  if (o.src && !src_in_kernel)
+    IWPP_CUDA_TRY(cudaMemcpyAsync(J, o.src, (size_t)W * H * sizeof(T), cudaMemcpyDeviceToDevice, st));
   if (fused_init) {
     // (the engine kernel initialises the queue)
   } else if (o.init_mode == INIT_CONTINUE) {
@@ -2810,6 +2845,11 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
     if (rounds_env < 0) rounds_env = getenv("IWPP_RECON_ROUNDS") ? atoi(getenv("IWPP_RECON_ROUNDS")) : 0;
     const bool rounds = use_tma && ntx_m && o.init_mode != INIT_CONTINUE && !o.rows_mode && !o.dirty &&
                         (o.engine == ENGINE_ROUNDS || (o.engine == ENGINE_AUTO && rounds_env));
+    if (src_in_kernel && rounds) {  // (the rounds engine has no marker prologue)
+      IWPP_CUDA_TRY(cudaMemcpyAsync(J, o.src, (size_t)W * H, cudaMemcpyDeviceToDevice, st));
+      src_in_kernel = false;
+    }
+    if (src_in_kernel) a.M = o.src;
     if (rounds) {
       static int rd_per_sm = 0;
       if (rd_per_sm == 0) {

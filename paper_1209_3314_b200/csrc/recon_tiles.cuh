@@ -85,6 +85,8 @@ struct EngineOpts {
   int engine = 0;               // ENGINE_AUTO / ENGINE_SMEM / ENGINE_REG / ENGINE_ROUNDS
   int sweeps_set = 0;           // the caller fixed the in-tile sweep count
   int max_rounds = 0;           // round engine: > 0 caps the rounds (CNT_LIMIT)
+  const void *src = nullptr;    // marker to copy into J first (the fused u8 engine
+                                // copies it in its prologue)
 };
 // ENGINE_REG: the register engine on the tile queue; ENGINE_ROUNDS: the
 // register engine in level-synchronous tile rounds (u8; AUTO picks it when

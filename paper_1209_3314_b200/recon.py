@@ -182,7 +182,9 @@ def reconstruct(marker, mask, conn: int = 8, cfg: EngineConfig | None = None,
                  engine, max_rounds)
     with _lib.device_of(marker, mask):
         if is_device_array(marker):
-            J = marker.clone()
+            M = marker.contiguous()
+            J = M.new_empty(M.shape)
+            opts.marker = _lib.ptr(M)  # copied into J by the engine (not modified)
             I = mask.contiguous()
             nbytes = L.iwpp_recon_workspace_bytes(W, H, code, conn)
             ws = _lib.workspace(nbytes)

@@ -432,3 +432,53 @@ def test_reconstruct_validates_raw_inputs(gw):
     with pytest.raises(gw.ContractViolation):
         gw.reconstruct(dJ, dI, 6)
     assert np.array_equal(gw.reconstruct(dJ, dI, 8).cpu().numpy(), oracle.recon_fh(J, I, 8))
+
+
+# ---------------------------------------------------------------------------
+# iwpp_recon_opts.marker: J is output only (its old contents never matter),
+# the marker is not modified; the fused u8 engine copies it in its prologue,
+# every other path copies it first.  Unaligned views take the byte path.
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_marker_option_every_path(gw, conn):
+    t = _torch()
+    from paper_1209_3314_b200 import _lib
+    L = _lib.lib()
+    rng = np.random.default_rng(1300 + conn)
+    cases = []
+    for shape, dt, h, code, eng in [((64, 64), np.uint8, 40, 0, 0),        # few tiles: init kernel
+                                    ((1040, 2048), np.uint8, 40, 0, 0),    # fused prologue copy
+                                    ((1000, 999), np.uint8, 40, 0, 0),     # unaligned rows
+                                    ((1040, 2048), np.uint8, 40, 0, 3),    # rounds engine
+                                    ((520, 512), np.uint8, 40, 0, 1),      # shared-memory engine
+                                    ((300, 256), np.uint16, 9000, 1, 0),
+                                    ((300, 256), np.int32, 1 << 27, 2, 0)]:
+        J, I = oracle.gray_pair(shape, int(rng.integers(1 << 30)), h=h, dtype=dt)
+        cases.append((J, I, code, eng, 0))
+        cases.append((J, I, code, eng, 1))  # views one element off the allocation start
+    bw = oracle.gen_synthetic_mask(700, 530, 50, 7)
+    Jb, Ib = oracle.imfill_pair(bw)
+    cases.append((Jb, Ib, 4, 0, 0))
+    If = rng.standard_normal((200, 256)).astype(np.float32)
+    cases.append(((If - 0.7).astype(np.float32), If, 3, 0, 0))
+    for J, I, code, eng, off in cases:
+        H, W = J.shape
+        want = oracle.recon_fh(J, I, conn)
+        dt = t.from_numpy(J).dtype
+        bufs = [t.empty(W * H + off, dtype=dt, device="cuda") for _ in range(3)]
+        dM, dI, dO = (b[off:].view(H, W) for b in bufs)
+        dM.copy_(t.from_numpy(J))
+        dI.copy_(t.from_numpy(I))
+        dO.fill_(0x5A if code != 3 else 1e30)  # garbage: J is output only
+        ws = _lib.workspace(L.iwpp_recon_workspace_bytes(W, H, code, conn))
+        o = gw.recon._opts(None, engine=eng)
+        o.marker = _lib.ptr(dM)
+        _lib.check(L.iwpp_recon(_lib.ptr(dO), _lib.ptr(dI), W, H, code, conn, _lib.ptr(ws), ws.numel(),
+                                _lib.ctypes.byref(o), None, _lib.stream_ptr()), "recon")
+        assert np.array_equal(dO.cpu().numpy(), want), (J.shape, J.dtype, code, eng, off)
+        assert np.array_equal(dM.cpu().numpy(), J), "marker modified"
+        # marker == J: in place, as without the option
+        o.marker = _lib.ptr(dM)
+        _lib.check(L.iwpp_recon(_lib.ptr(dM), _lib.ptr(dI), W, H, code, conn, _lib.ptr(ws), ws.numel(),
+                                _lib.ctypes.byref(o), None, _lib.stream_ptr()), "recon")
+        assert np.array_equal(dM.cpu().numpy(), want), (J.shape, code, eng, off, "in place")
