@@ -1,44 +1,46 @@
-"""Per-round timeline of the raster EDT engine (IWPP_EDT_RTRACE=1): one run,
-then a fit of round time against frontier size."""
+"""Per-round trace of the raster EDT engine on a bench mask
+(IWPP_EDT_RTRACE=1): python scripts/edt_rtrace.py blob|nuclei [conn]
+Prints the library's per-round lines (frontier size, round time, and for
+raster rounds the work / barrier / compaction split) on stderr, then a
+summary by frontier-size bucket."""
 import os
 import re
 import subprocess
 import sys
 
-import numpy as np
-
-kind = sys.argv[1] if len(sys.argv) > 1 else "blob"
-env = dict(os.environ, IWPP_EDT_RTRACE="1")
-code = f"""
-import sys; sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
-import torch, oracle, paper_1209_3314_b200 as gw
-n = 4096
-m = oracle.gen_synthetic_mask(n, n, 50, 7) if {kind!r} == "blob" else oracle.gen_nuclei_mask(n, n, 30.0, 7)
-img = gw.Image2D(n, n, "binary", torch.from_numpy(m).cuda())
-gw.edt(img, gw.SE8)
-"""
-out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True).stderr
-rows = [(int(a), int(b), float(c)) for a, b, c in
-        re.findall(r"round (\d+) n (\d+) dt_us ([0-9.]+)", out)]
-ph = np.array([(float(a), float(b), float(c)) for a, b, c in
-               re.findall(r"work_us ([0-9.]+) bar_us ([0-9.]+) comp_us ([0-9.]+)", out)])
-rows = rows[-(len(rows) // 2):] if len(rows) > 400 else rows  # last run only
-n = np.array([r[1] for r in rows], float)
-t = np.array([r[2] for r in rows])
-print(f"{kind}: rounds {len(rows)} total {t.sum() / 1e3:.2f} ms, median {np.median(t):.1f} us/round")
-for lo, hi in [(0, 1e3), (1e3, 1e4), (1e4, 5e4), (5e4, 1.5e5), (1.5e5, 2.62e5), (2.62e5, 1e9)]:
-    sel = (n >= lo) & (n < hi)
-    if sel.any():
-        print(f"  n in [{lo:.0f},{hi:.0f}): {sel.sum():4d} rounds, mean n {n[sel].mean():9.0f}, "
-              f"mean {t[sel].mean():6.1f} us, total {t[sel].sum() / 1e3:.2f} ms")
-rs = ph[:, 0] > 0 if ph.ndim == 2 else np.zeros(0, bool)
-if rs.any():
-    w, b, c3 = ph[rs].mean(0)
-    print(f"  raster rounds (block 0): work {w:.1f} us, phase-1 barrier wait {b:.1f} us, compaction {c3:.1f} us")
-A = np.vstack([np.ones_like(n), n]).T
-q = n < 262144
-c = np.linalg.lstsq(A[q], t[q], rcond=None)[0]
-print(f"  queue rounds fit: {c[0]:.1f} us + {c[1] * 1e3:.2f} us per 1000 items")
-if (~q).any():
-    c2 = np.linalg.lstsq(A[~q], t[~q], rcond=None)[0]
-    print(f"  raster rounds fit: {c2[0]:.1f} us + {c2[1] * 1e3:.2f} us per 1000 items")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if os.environ.get("_RT_CHILD"):
+    sys.path.insert(0, ROOT)
+    import torch
+    import oracle
+    import paper_1209_3314_b200 as gw
+    name, conn = sys.argv[1], int(sys.argv[2])
+    m = (oracle.gen_nuclei_mask(4096, 4096, 30.0, 7) if name == "nuclei"
+         else oracle.gen_synthetic_mask(4096, 4096, 50, 7))
+    img = gw.Image2D(4096, 4096, "binary", torch.from_numpy(m).cuda())
+    for _ in range(3):
+        gw.edt(img, gw.StructuringElement(conn))
+    torch.cuda.synchronize()
+    sys.exit(0)
+name = sys.argv[1] if len(sys.argv) > 1 else "blob"
+conn = sys.argv[2] if len(sys.argv) > 2 else "8"
+env = dict(os.environ, _RT_CHILD="1", IWPP_EDT_RTRACE="1")
+p = subprocess.run([sys.executable, __file__, name, conn], env=env, capture_output=True, text=True)
+lines = [l for l in p.stderr.splitlines() if l.startswith("[edt rtrace]")]
+# the last call's rounds
+starts = [i for i, l in enumerate(lines) if " round 0 " in l]
+last = lines[starts[-1]:] if starts else lines
+rx = re.compile(r"round (\d+) n (\d+) dt_us ([\d.]+) work_us ([\d.]+) bar_us ([\d.]+) comp_us ([\d.]+)")
+rows = [tuple(float(x) for x in rx.search(l).groups()) for l in last if rx.search(l)]
+rows = [r for r in rows if r[1] > 0]  # (round 0 runs inside the init: no stamp)
+buckets = [(0, 1024), (1024, 16384), (16384, 65536), (65536, 262144), (262144, 1 << 40)]
+print(f"{name} c{conn}: {len(rows)} rounds traced, total {sum(r[2] for r in rows) / 1e3:.3f} ms")
+for lo, hi in buckets:
+    sel = [r for r in rows if lo <= r[1] < hi]
+    if sel:
+        t = sum(r[2] for r in sel)
+        print(f"  frontier [{lo}, {hi}): {len(sel)} rounds, {t / 1e3:.3f} ms, {t / len(sel):.2f} us/round, "
+              f"mean n {sum(r[1] for r in sel) / len(sel):.0f}, work {sum(r[3] for r in sel) / len(sel):.2f} "
+              f"bar {sum(r[4] for r in sel) / len(sel):.2f} comp {sum(r[5] for r in sel) / len(sel):.2f}")
+if os.environ.get("RT_ALL"):
+    print("\n".join(last))
