@@ -332,6 +332,27 @@ static bool host_slabs(int64_t W, int64_t H, size_t es, int64_t rows, std::vecto
 // Optional timeline of the pipelined host path (IWPP_TRACE=1 in the
 // environment): a one-thread kernel on each stream stamps %globaltimer when
 // the stream reaches it; printed to stderr at the end (diagnostics only).
+// The host path's last transfer, when the output buffer is page-locked and
+// mapped: the last slab's rows and every tile row a later run re-wrote
+// (dirty), written straight into host memory by the SMs.  One kernel
+// instead of a D2H copy, a host read of the dirty flags and the recopies.
+// gridDim.x = tile rows, gridDim.y CTAs share one; 16-byte stores when rows
+// allow.
+__global__ void recopy_mapped_kernel(const char *__restrict__ dJ, char *out, const uint8_t *__restrict__ dirty,
+                                     int64_t H, int64_t TS, size_t row_bytes, int64_t y_last) {
+  const int64_t t = blockIdx.x, r0 = t * TS, r1 = r0 + TS < H ? r0 + TS : H;
+  if (r1 <= y_last && !dirty[t]) return;
+  const size_t off = (size_t)r0 * row_bytes, nb = (size_t)(r1 - r0) * row_bytes;
+  const size_t tid = (size_t)blockIdx.y * blockDim.x + threadIdx.x, nt = (size_t)gridDim.y * blockDim.x;
+  if (((uintptr_t)(dJ + off) | (uintptr_t)(out + off) | nb) % 16 == 0) {
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(dJ + off);
+    uint4 *d4 = reinterpret_cast<uint4 *>(out + off);
+    for (size_t i = tid; i < nb / 16; i += nt) d4[i] = __ldcg(s4 + i);
+  } else {
+    for (size_t i = tid; i < nb; i += nt) out[off + i] = dJ[off + i];
+  }
+}
+
 __global__ void trace_stamp_kernel(unsigned long long *slot) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -406,6 +427,18 @@ static int recon_host_pipelined(char *out, const char *marker, const char *mask,
   }
   // the engine's tile rows: slab cuts (multiples of TSB) fall on them
   const int64_t TS = recon::tile_side(dtype, eo), nty = (H + TS - 1) / TS;
+  // a page-locked, mapped output takes the last transfer from the SMs
+  // (IWPP_E2E_MAPPED=0: copies only)
+  char *out_dev = nullptr;
+  {
+    static int mapped_env = -1;
+    if (mapped_env < 0) mapped_env = getenv("IWPP_E2E_MAPPED") ? atoi(getenv("IWPP_E2E_MAPPED")) : 1;
+    cudaPointerAttributes pa;
+    if (mapped_env && cudaPointerGetAttributes(&pa, out) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer)
+      out_dev = static_cast<char *>(pa.devicePointer);
+    (void)cudaGetLastError();
+  }
   Trace tr;
   tr.mark(st, "start", 0);
   IWPP_CUDA_TRY(cudaEventRecord(hp->start, st));
@@ -454,15 +487,39 @@ static int recon_host_pipelined(char *out, const char *marker, const char *mask,
     // Copying right after the slab's own run, not after the next one, takes
     // one run off the transfer tail.
     const int64_t p0 = y0, p1 = k == S - 1 ? H : y1;
+    if (out_dev && k == S - 1) {
+      // the last slab and the re-written rows, from the SMs, after every
+      // earlier copy of those rows has landed (a stale copy must not
+      // overwrite a recopy)
+      IWPP_CUDA_TRY(cudaEventRecord(hp->ready[k], hp->d2h));
+      IWPP_CUDA_TRY(cudaStreamWaitEvent(st, hp->ready[k], 0));
+      {
+        static int gy = 0;
+        if (!gy) gy = getenv("IWPP_MAPPED_SPLIT") ? atoi(getenv("IWPP_MAPPED_SPLIT")) : 8;
+        recopy_mapped_kernel<<<dim3((unsigned)nty, (unsigned)gy), 256, 0, st>>>(dJ, out_dev, dirty, H, TS,
+                                                                                 row_bytes, y0);
+      }
+      IWPP_CUDA_TRY(cudaGetLastError());
+      tr.mark(st, "mapped copy done", k);
+      break;
+    }
     IWPP_CUDA_TRY(cudaMemsetAsync(dirty + p0 / TS, 0, (size_t)((p1 + TS - 1) / TS - p0 / TS), st));
     IWPP_CUDA_TRY(cudaEventRecord(hp->ready[k], st));
     IWPP_CUDA_TRY(cudaStreamWaitEvent(hp->d2h, hp->ready[k], 0));
     if ((rc = copy_back(p0, p1))) return rc;
     tr.mark(hp->d2h, "d2h done", k);
   }
+  unsigned long long viol = 0;
+  if (out_dev) {
+    IWPP_CUDA_TRY(cudaMemcpyAsync(&viol, vctr, sizeof viol, cudaMemcpyDeviceToHost, st));
+    IWPP_CUDA_TRY(cudaStreamSynchronize(st));
+    tr.mark(st, "done", 0);
+    if (viol) return set_error(IWPP_E_CONTRACT, "marker exceeds mask somewhere (%llu cells)", viol);
+    if (stats) return fill_recon_stats(w, stats, st);
+    return IWPP_OK;
+  }
   // tile rows written after their slab was copied: copy them again
   std::vector<uint8_t> flags((size_t)nty);
-  unsigned long long viol = 0;
   IWPP_CUDA_TRY(cudaMemcpyAsync(flags.data(), dirty, (size_t)nty, cudaMemcpyDeviceToHost, st));
   IWPP_CUDA_TRY(cudaMemcpyAsync(&viol, vctr, sizeof viol, cudaMemcpyDeviceToHost, st));
   IWPP_CUDA_TRY(cudaStreamSynchronize(st));

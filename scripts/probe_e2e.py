@@ -1,53 +1,46 @@
-"""Development probe: host-buffer (e2e) reconstruction through iwpp_recon_host,
-pipelined (auto / given slab heights) vs unpipelined.  Pinned host buffers."""
+"""The e2e call as bench.py times it (iwpp_recon_host, pinned host buffers,
+4096^2 u8 c8): median of 20 calls.  IWPP_TRACE=1 adds the library's
+timeline of the last call.  python scripts/probe_e2e.py [n]"""
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 import numpy as np
 import torch
 
-import oracle
+from bench import gray_pair
 from paper_1209_3314_b200 import _lib
 
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 L = _lib.lib()
-torch.cuda.set_device(0)
-sizes = [int(a) for a in sys.argv[1:]] or [4096, 16384]
-for n in sizes:
-    J, I = oracle.gray_pair(n, 0, h=40) if n <= 8192 else (None, None)
-    if J is None:
-        g = torch.Generator().manual_seed(0)
-        It = torch.randint(0, 256, (n, n), dtype=torch.uint8, generator=g)
-        Jt = torch.clamp(It.to(torch.int16) - 40, min=0).to(torch.uint8)
-        J, I = Jt.numpy(), It.numpy()
-    pJ = torch.from_numpy(J).pin_memory()
-    pI = torch.from_numpy(I).pin_memory()
-    pO = torch.empty_like(pJ).pin_memory()
-    ws = _lib.workspace(L.iwpp_recon_host_workspace_bytes(n, n, 0, 8))
-    stream = _lib.stream_ptr()
-    ref = None
-    for rows in [int(r) for r in os.environ.get("ROWS", "-1,0,512,1024").split(",")]:
-        o = _lib.ReconOpts()
-        o.sweeps, o.tile_sweeps, o.halo_sweep_threshold = -1, -1, -1
-        o.pipeline_rows = rows
-
-        def step():
-            _lib.check(L.iwpp_recon_host(_lib.ptr(pO.numpy()), _lib.ptr(pJ.numpy()),
-                                         _lib.ptr(pI.numpy()), n, n, 0, 8, _lib.ptr(ws),
-                                         ws.numel(), _lib.ctypes.byref(o), None, stream),
-                       "recon_host")
-        for _ in range(3):
-            step()
-        ts = []
-        for _ in range(10):
-            t0 = time.perf_counter()
-            step()
-            ts.append(time.perf_counter() - t0)
-        out = pO.numpy().copy()
-        if ref is None:
-            ref = out
-        same = np.array_equal(out, ref)
-        med = float(np.median(ts)) * 1e3
-        print(f"e2e {n}^2 u8 c8 pipeline_rows={rows}: median {med:.3f} ms min {min(ts)*1e3:.3f} "
-              f"-> {n*n/med/1e3:.0f} Mpx/s  same={same}", flush=True)
+Jh, Ih = gray_pair(n, 0)
+pin_J = torch.from_numpy(Jh).pin_memory()
+pin_I = torch.from_numpy(Ih).pin_memory()
+pin_O = torch.empty_like(pin_J).pin_memory()
+ws = _lib.workspace(L.iwpp_recon_host_workspace_bytes(n, n, 0, 8))
+o = _lib.ReconOpts()
+o.sweeps, o.max_blocks, o.check_contract, o.queue_capacity = -1, 0, 0, 0
+o.tile_sweeps, o.halo_sweep_threshold = -1, -1
+o.pipeline_rows = int(os.environ.get("ROWS", "0"))
+st = _lib.stream_ptr()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+trace = os.environ.pop("IWPP_TRACE", None)
+ts = []
+for i in range(22):
+    flush.fill_(i & 255)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _lib.check(L.iwpp_recon_host(_lib.ptr(pin_O.numpy()), _lib.ptr(pin_J.numpy()), _lib.ptr(pin_I.numpy()),
+                                 n, n, 0, 8, _lib.ptr(ws), ws.numel(), _lib.ctypes.byref(o), None, st))
+    if i >= 2:
+        ts.append(time.perf_counter() - t0)
+ms = np.median(ts) * 1e3
+print(f"e2e {n}^2 rows={o.pipeline_rows} slab_mb={os.environ.get('IWPP_SLAB_MB', 'auto')}: median {ms:.3f} ms "
+      f"min {min(ts) * 1e3:.3f} -> {n * n / ms / 1e3:.0f} Mpx/s", flush=True)
+if trace:
+    os.environ["IWPP_TRACE"] = trace
+    # (the library reads IWPP_TRACE per call)
+    _lib.check(L.iwpp_recon_host(_lib.ptr(pin_O.numpy()), _lib.ptr(pin_J.numpy()), _lib.ptr(pin_I.numpy()),
+                                 n, n, 0, 8, _lib.ptr(ws), ws.numel(), _lib.ctypes.byref(o), None, st))

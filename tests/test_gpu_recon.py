@@ -482,3 +482,56 @@ def test_marker_option_every_path(gw, conn):
         _lib.check(L.iwpp_recon(_lib.ptr(dM), _lib.ptr(dI), W, H, code, conn, _lib.ptr(ws), ws.numel(),
                                 _lib.ctypes.byref(o), None, _lib.stream_ptr()), "recon")
         assert np.array_equal(dM.cpu().numpy(), want), (J.shape, code, eng, off, "in place")
+
+
+# ---------------------------------------------------------------------------
+# iwpp_recon_host into a page-locked output: the last transfer (the last slab
+# and every re-written tile row) is written by the SMs into mapped host
+# memory instead of copies after a host read of the dirty flags.
+
+def _recon_host_pinned(M, I, conn, rows, code=0):
+    import torch
+    from paper_1209_3314_b200 import _lib
+    L = _lib.lib()
+    H, W = M.shape
+    pm, pi = torch.from_numpy(M.copy()).pin_memory(), torch.from_numpy(I.copy()).pin_memory()
+    po = torch.from_numpy(np.full_like(M, 0x5A)).pin_memory()
+    ws = _lib.workspace(L.iwpp_recon_host_workspace_bytes(W, H, code, conn))
+    o = gw_opts(rows)
+    st = _lib.Stats()
+    _lib.check(L.iwpp_recon_host(_lib.ptr(po.numpy()), _lib.ptr(pm.numpy()), _lib.ptr(pi.numpy()), W, H, code,
+                                 conn, _lib.ptr(ws), ws.numel(), _lib.ctypes.byref(o), _lib.ctypes.byref(st),
+                                 _lib.stream_ptr()), "recon_host")
+    return po.numpy().copy(), st.as_dict()
+
+
+def gw_opts(rows):
+    from paper_1209_3314_b200.recon import _opts
+    return _opts(None, pipeline_rows=rows)
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_host_pipeline_pinned_output(gw, conn):
+    cases = [oracle.gray_pair((1000, 300), 11, h=40), oracle.gray_pair((513, 704), 12, h=40),
+             oracle.gray_pair(4096, 0, h=40)]
+    cases.append(oracle.imfill_pair(oracle.gen_synthetic_mask(512, 2048, 50, 7)))
+    I = np.full((1024, 256), 200, np.uint8)
+    I[::3, 1:] = 0  # serpentine corridor: every cut re-written after its slab went back
+    M = np.zeros_like(I)
+    M[-1, 0] = 200
+    cases.append((M, I))
+    for M, I in cases:
+        want = oracle.recon_fh(M, I, conn)
+        for rows in (0, 64, 128):
+            got, st = _recon_host_pinned(M, I, conn, rows)
+            assert np.array_equal(got, want), (M.shape, rows)
+            assert st["contract_violations"] == 0
+    # the contract check still raises (violation in the first and in the last slab)
+    M, I = oracle.gray_pair((1024, 256), 13, h=40)
+    for row in (0, 1023):
+        bad = M.copy()
+        bad[row, 7] = 255
+        I2 = I.copy()
+        I2[row, 7] = 0
+        with pytest.raises(Exception):
+            _recon_host_pinned(bad, I2, conn, 64)
