@@ -91,7 +91,6 @@ struct EngineArgs {
   int WW;                // binary engine: words per bit-plane row
   TileQueue q;
   unsigned long long ntx_m;  // ceil(2^40 / ntx) (0: divide): tile id -> (tx, ty)
-  const void *M;             // fused init: copy this marker into J first (nullable)
 };
 
 // tile id -> (tx, ty) without an integer division (exact while ntx < 2^14
@@ -1207,10 +1206,10 @@ __device__ __forceinline__ void tile_queue_init(const TileQueue &q, int ntx, int
 // fused init with a separate marker: the grid copies it into J before the
 // grid-wide sync (16-byte vectors, 4 in flight per thread; the marker is read
 // once, so streaming loads; J stays in L2 for the first box reads)
-__device__ __forceinline__ void copy_marker(const EngineArgs &a) {
+__device__ __forceinline__ void copy_marker(const EngineArgs &a, const void *M) {
   const size_t n = (size_t)a.W * a.H;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
-  const uint8_t *src = static_cast<const uint8_t *>(a.M);
+  const uint8_t *src = static_cast<const uint8_t *>(M);
   uint8_t *dst = static_cast<uint8_t *>(a.J);
   size_t done = 0;
   if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
@@ -1238,9 +1237,10 @@ __device__ __forceinline__ void copy_marker(const EngineArgs &a) {
 template <int CONN>
 __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
     tile_engine_reg_kernel(EngineArgs a, unsigned long long *counters,
-                           const __grid_constant__ BoxMaps maps, int use_tma, int fused_init) {
+                           const __grid_constant__ BoxMaps maps, int use_tma, int fused_init,
+                           const void *M) {
   if (fused_init) {
-    if (a.M) copy_marker(a);
+    if (M) copy_marker(a, M);
     tile_queue_init(a.q, a.ntx, a.nty, counters, 0);
     cooperative_groups::this_grid().sync();
   }
@@ -2849,7 +2849,7 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
       IWPP_CUDA_TRY(cudaMemcpyAsync(J, o.src, (size_t)W * H, cudaMemcpyDeviceToDevice, st));
       src_in_kernel = false;
     }
-    if (src_in_kernel) a.M = o.src;
+    const void *msrc = src_in_kernel ? o.src : nullptr;
     if (rounds) {
       static int rd_per_sm = 0;
       if (rd_per_sm == 0) {
@@ -2886,11 +2886,11 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
       }
     } else if (fused_init) {
       int fi = fused_init;
-      void *args[] = {&a, &counters, &maps, &use_tma, &fi};
+      void *args[] = {&a, &counters, &maps, &use_tma, &fi, &msrc};
       IWPP_CUDA_TRY(cudaLaunchCooperativeKernel((const void *)tile_engine_reg_kernel<CONN>, dim3(rb),
                                                 dim3(kCtaThreads), args, 0, st));
     } else {
-      tile_engine_reg_kernel<CONN><<<rb, kCtaThreads, 0, st>>>(a, counters, maps, use_tma, 0);
+      tile_engine_reg_kernel<CONN><<<rb, kCtaThreads, 0, st>>>(a, counters, maps, use_tma, 0, nullptr);
     }
   } else {
     kern<<<blocks, kCtaThreads, smem, st>>>(a, counters);

@@ -1,4 +1,9 @@
-"""imfill 16K^2 timing (the bench's C4 rows) for A/B: python scripts/probe_imfill.py"""
+"""imfill 16K^2 timing (the bench's C4 rows) for A/B:
+python scripts/probe_imfill.py.  Two forms of the same call through the C
+ABI: the marker copied by torch into the output first ("copy"), and the
+marker handed over in iwpp_recon_opts.marker ("marker", what reconstruct()
+does).  IWPP_B200_LIB selects another build (an older build ignores
+opts.marker, so only its "copy" line is meaningful)."""
 import os
 import sys
 
@@ -7,18 +12,30 @@ import numpy as np
 import torch
 
 import oracle
-import paper_1209_3314_b200 as gw
+from paper_1209_3314_b200 import _lib
+from paper_1209_3314_b200.recon import _opts
 
+L = _lib.lib()
 bw = np.tile(oracle.gen_synthetic_mask(4096, 4096, 50, 7), (4, 4))
 J, I = (torch.from_numpy(a).cuda() for a in oracle.imfill_pair(bw))
+H, W = J.shape
+out = torch.empty_like(J)
 for conn in (4, 8):
-    ts = []
-    for r in range(7):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        gw.reconstruct(J, I, conn, kind="binary")
-        b.record()
-        torch.cuda.synchronize()
-        if r >= 2:
-            ts.append(a.elapsed_time(b))
-    print(f"imfill 16K c{conn}: {np.median(ts):.3f} ms (min {min(ts):.3f})", flush=True)
+    ws = _lib.workspace(L.iwpp_recon_workspace_bytes(W, H, 4, conn))
+    for form in ("copy", "marker"):
+        o = _opts(None)
+        ts = []
+        for r in range(7):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            if form == "copy":
+                out.copy_(J)
+            else:
+                o.marker = _lib.ptr(J)
+            _lib.check(L.iwpp_recon(_lib.ptr(out), _lib.ptr(I), W, H, 4, conn, _lib.ptr(ws), ws.numel(),
+                                    _lib.ctypes.byref(o), None, _lib.stream_ptr()), "recon")
+            b.record()
+            torch.cuda.synchronize()
+            if r >= 2:
+                ts.append(a.elapsed_time(b))
+        print(f"imfill 16K c{conn} {form}: {np.median(ts):.3f} ms (min {min(ts):.3f})", flush=True)
