@@ -1363,7 +1363,12 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
             reinterpret_cast<uint4 *>(p)[0] = make_uint4(j[0], j[1], j[2], j[3]);
             reinterpret_cast<uint4 *>(p)[1] = make_uint4(j[4], j[5], j[6], j[7]);
           } else {
-            for (int x = 0; x < TS && x0 + x < a.W; x++) p[x] = (uint8_t)(j[x >> 2] >> (8 * (x & 3)));
+            // (static indices: a dynamic j[] index puts the tile row in local memory)
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+#pragma unroll
+              for (int b = 0; b < 4; b++)
+                if (x0 + 4 * k + b < a.W) p[4 * k + b] = (uint8_t)(j[k] >> (8 * b));
           }
         }
         if (a.dirty && l0) a.dirty[ty] = 1;
@@ -2457,6 +2462,7 @@ __device__ __forceinline__ void tile_queue_init(const TileQueue &q, int ntx, int
   unsigned stride = gridDim.x * blockDim.x;
   unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned cx[4], cy[4], base[4];
+#pragma unroll
   for (int c = 0; c < 4; c++) {
     cx[c] = (ntx - (c & 1) + 1) / 2;
     cy[c] = (nty - (c >> 1) + 1) / 2;
@@ -2469,13 +2475,20 @@ __device__ __forceinline__ void tile_queue_init(const TileQueue &q, int ntx, int
     unsigned tx = t % ntx, ty = t / ntx;
     unsigned c = (tx & 1) | ((ty & 1) << 1);
     unsigned slot;
+    // (selects, not dynamic indices: the arrays stay in registers)
+    unsigned bc = base[0], xc = cx[0];
+#pragma unroll
+    for (int k = 1; k < 4; k++)
+      if (c == (unsigned)k) bc = base[k], xc = cx[k];
     if (B == (unsigned)nty) {
-      slot = base[c] + (ty >> 1) * cx[c] + (tx >> 1);
+      slot = bc + (ty >> 1) * xc + (tx >> 1);
     } else {
       const unsigned r0 = ty / B * B, rows = min(B, (unsigned)nty - r0);
       unsigned bb = 0;
-      for (unsigned k = 0; k < c; k++) bb += cx[k] * ((rows - (k >> 1) + 1) / 2);
-      slot = r0 * (unsigned)ntx + bb + ((ty - r0) >> 1) * cx[c] + (tx >> 1);
+#pragma unroll
+      for (int k = 0; k < 3; k++)
+        if ((unsigned)k < c) bb += cx[k] * ((rows - (k >> 1) + 1) / 2);
+      slot = r0 * (unsigned)ntx + bb + ((ty - r0) >> 1) * xc + (tx >> 1);
     }
     q.state[t] = ST_Q | ST_V;
     q.ring[slot] = ((unsigned long long)slot << 32) | t;
