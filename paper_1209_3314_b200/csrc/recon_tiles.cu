@@ -1558,6 +1558,7 @@ struct ColourOrder {
   unsigned long long m[4];  // ceil(2^40 / cx): exact for cx < 2^14, r < 2^26
   __device__ ColourOrder(int ntx, int nty) {
     unsigned acc = 0;
+#pragma unroll
     for (int c = 0; c < 4; c++) {
       cx[c] = (ntx - (c & 1) + 1) / 2;
       const unsigned cy = (nty - (c >> 1) + 1) / 2;
@@ -1568,8 +1569,14 @@ struct ColourOrder {
   }
   __device__ __forceinline__ unsigned tile(unsigned i, int ntx) const {
     const int c = (i >= base[1]) + (i >= base[2]) + (i >= base[3]);
-    const unsigned r = i - base[c];
-    const unsigned ry = (unsigned)((r * m[c]) >> 40), rx = r - ry * cx[c];
+    // (selects, not dynamic indices: the tables stay in registers)
+    unsigned b = base[0], x = cx[0];
+    unsigned long long mm = m[0];
+#pragma unroll
+    for (int k = 1; k < 4; k++)
+      if (c == k) b = base[k], x = cx[k], mm = m[k];
+    const unsigned r = i - b;
+    const unsigned ry = (unsigned)((r * mm) >> 40), rx = r - ry * x;
     return (2 * ry + (c >> 1)) * (unsigned)ntx + 2 * rx + (c & 1);
   }
 };
@@ -1608,7 +1615,7 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
   }
   __syncwarp();
   const CUtensorMap *tmJ = &maps.m[0], *tmI = &maps.m[1];
-  unsigned phase[2] = {0, 0};
+  unsigned phase = 0;  // bit b: the parity of staging buffer b
   const bool l0 = lane == 0;
   unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0;
   const ColourOrder corder(a.ntx, a.nty);
@@ -1651,8 +1658,8 @@ __global__ void __launch_bounds__(kCtaThreads, kRegCtaMinBlocks)
       __syncwarp();  // the other buffer's previous tile is done (WAR)
       if (i2 < n) issue(tn, bi ^ 1);
       TmaWarpSmem &ts = tsm[wib][bi];
-      mbar_wait(&ts.bar, phase[bi]);
-      phase[bi] ^= 1u;
+      mbar_wait(&ts.bar, (phase >> bi) & 1u);
+      phase ^= 1u << bi;
       int tx, ty;
       tile_xy(a, t, tx, ty);
       const int x0 = tx * TS, y0 = ty * TS;
