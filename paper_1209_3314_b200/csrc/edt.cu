@@ -432,6 +432,128 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows_kernel(cons
   }
 }
 
+// The same init with 4 consecutive cells per lane, for W % 128 == 0 (every
+// segment full, rows 16-byte aligned) and planar keys: one 32-bit mask word
+// per row and lane, the neighbours across lanes by one shuffle of a 4-bit
+// mask per row, 16-byte key stores, and the next segment's words loaded
+// before this one is processed.  Same keys, same seeds (listed in another
+// order: the rounds' results do not depend on it).
+__device__ __forceinline__ unsigned nz4(unsigned w) {  // bit b: byte b of w is nonzero
+  const unsigned m = __vcmpne4(w, 0u);
+  return ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
+}
+template <int CONN, bool ROUND0 = false>
+__global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows4_kernel(const uint8_t *__restrict__ mask,
+                                                                             int W, int H, EdtState s) {
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+  __shared__ uint32_t buf[kInitWarps][kInitBuf];
+  unsigned nbuf = 0;
+  unsigned long long nseed = 0;
+  const int li = ROUND0 ? 1 : 0;
+  const long long segs_per_row = W / 128, nseg = segs_per_row * H;
+  const size_t NN = (size_t)W * H;
+  auto flush = [&]() {
+    unsigned base = 0;
+    if (lane == 0 && nbuf) base = atomicAdd(&s.cnt[li], nbuf);
+    base = __shfl_sync(FULL, base, 0);
+    for (unsigned i = lane; i < nbuf; i += 32) s.F[li][base + i] = buf[wib][i];
+    __syncwarp();
+    nbuf = 0;
+  };
+  // rows y-1, y, y+1 of segment g: this lane's word, and (lanes 0 / 31) the
+  // byte just left / right of the segment; kOff outside the image
+  auto load = [&](long long g, unsigned (&w)[3], unsigned (&e)[3]) {
+    const int y = (int)(g / segs_per_row), x0 = (int)(g - (long long)y * segs_per_row) * 128;
+#pragma unroll
+    for (int rr = 0; rr < 3; rr++) {
+      const int yy = y + rr - 1;
+      const bool rin = yy >= 0 && yy < H;
+      const uint8_t *row = mask + (size_t)(rin ? yy : 0) * W + x0;
+      w[rr] = rin ? __ldg(reinterpret_cast<const unsigned *>(row) + lane) : 0u;
+      const int ex = lane == 0 ? -1 : 128;
+      e[rr] = (rin && (lane == 0 || lane == 31) && x0 + ex >= 0 && x0 + ex < W) ? (unsigned)__ldg(row + ex) : kOff;
+    }
+  };
+  const long long stride = (long long)gridDim.x * kInitWarps;
+  long long g = (long long)blockIdx.x * kInitWarps + wib;
+  unsigned nw[3], ne[3];
+  if (g < nseg) load(g, nw, ne);
+  for (; g < nseg; g += stride) {
+    unsigned w[3] = {nw[0], nw[1], nw[2]}, e[3] = {ne[0], ne[1], ne[2]};
+    if (g + stride < nseg) load(g + stride, nw, ne);
+    const int y = (int)(g / segs_per_row), x0 = (int)(g - (long long)y * segs_per_row) * 128;
+    // 6-bit masks per row: bit 0 the cell left of my 4, bits 1-4 mine, bit 5
+    // the one right of them (fg = a nonzero sample inside the image, bg = a
+    // zero sample inside it; outside the image: neither)
+    unsigned fg[3], bg[3];
+#pragma unroll
+    for (int rr = 0; rr < 3; rr++) {
+      const int yy = y + rr - 1;
+      const bool rin = yy >= 0 && yy < H;
+      const unsigned f4 = rin ? nz4(w[rr]) : 0u, b4 = rin ? (~nz4(w[rr]) & 0xfu) : 0u;
+      unsigned fl = (__shfl_up_sync(FULL, f4, 1) >> 3) & 1u, bl = (__shfl_up_sync(FULL, b4, 1) >> 3) & 1u;
+      unsigned fr = __shfl_down_sync(FULL, f4, 1) & 1u, br = __shfl_down_sync(FULL, b4, 1) & 1u;
+      if (lane == 0) fl = e[rr] != kOff && e[rr] != 0u, bl = e[rr] == 0u;
+      if (lane == 31) fr = e[rr] != kOff && e[rr] != 0u, br = e[rr] == 0u;
+      fg[rr] = fl | (f4 << 1) | (fr << 5);
+      bg[rr] = bl | (b4 << 1) | (br << 5);
+    }
+    unsigned long long k[4];
+    unsigned seeds = 0;
+    const uint32_t yu = (uint32_t)(y - 1) << 16, yc = (uint32_t)y << 16, yd = (uint32_t)(y + 1) << 16;
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      const int c = b + 1;
+      const uint32_t x = (uint32_t)(x0 + 4 * (int)lane + b);
+      const bool isbg = (bg[1] >> c) & 1u;
+      const unsigned n3 = 7u << (c - 1);  // cells c-1, c, c+1
+      const bool near = CONN == 8 ? ((fg[0] & n3) | (fg[1] & (5u << (c - 1))) | (fg[2] & n3)) != 0u
+                                  : (((fg[0] >> c) | (fg[2] >> c)) & 1u) || (fg[1] & (5u << (c - 1))) != 0u;
+      unsigned long long kk = isbg ? (unsigned long long)(yc | x) : KINF;
+      if (ROUND0) {
+        if (isbg && near) nseed += 1;
+        if (!isbg) {  // round 0's offers: up, left, right, down; then the diagonals
+          if ((bg[0] >> c) & 1u) kk = (1ull << 32) | (yu | x);
+          else if ((bg[1] >> (c - 1)) & 1u) kk = (1ull << 32) | (yc | (x - 1));
+          else if ((bg[1] >> (c + 1)) & 1u) kk = (1ull << 32) | (yc | (x + 1));
+          else if ((bg[2] >> c) & 1u) kk = (1ull << 32) | (yd | x);
+          else if (CONN == 8) {
+            if ((bg[0] >> (c - 1)) & 1u) kk = (2ull << 32) | (yu | (x - 1));
+            else if ((bg[0] >> (c + 1)) & 1u) kk = (2ull << 32) | (yu | (x + 1));
+            else if ((bg[2] >> (c - 1)) & 1u) kk = (2ull << 32) | (yd | (x - 1));
+            else if ((bg[2] >> (c + 1)) & 1u) kk = (2ull << 32) | (yd | (x + 1));
+          }
+          if (kk != KINF) seeds |= 1u << b;
+        }
+      } else if (isbg && near) {
+        seeds |= 1u << b;
+      }
+      k[b] = kk;
+    }
+    const size_t p = (size_t)y * W + x0 + 4 * lane;
+    ulonglong2 *k0 = reinterpret_cast<ulonglong2 *>(s.keys + p), *k1 = reinterpret_cast<ulonglong2 *>(s.keys + NN + p);
+    k0[0] = make_ulonglong2(k[0], k[1]);
+    k0[1] = make_ulonglong2(k[2], k[3]);
+    k1[0] = make_ulonglong2(k[0], k[1]);
+    k1[1] = make_ulonglong2(k[2], k[3]);
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+      const bool q = (seeds >> b) & 1u;
+      const unsigned bal = __ballot_sync(FULL, q);
+      if (q) buf[wib][nbuf + __popc(bal & lanemask_lt())] = ((uint32_t)y << 16) | (uint32_t)(x0 + 4 * lane + b);
+      nbuf += __popc(bal);
+    }
+    __syncwarp();
+    if (nbuf > kInitBuf - 128) flush();
+  }
+  flush();
+  if (ROUND0) {
+    for (int o = 16; o; o >>= 1) nseed += __shfl_xor_sync(FULL, nseed, o);
+    if (lane == 0 && nseed) atomicAdd(&s.counters[EC_VISITS], nseed);
+  }
+}
+
 __global__ void edt_import_key_kernel(const int64_t *__restrict__ vr, int W, int H, EdtState s) {
   size_t n = (size_t)W * H;
   for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
@@ -986,12 +1108,24 @@ int launch_init(const uint8_t *mask, int W, int H, int conn, const EdtState &s, 
     if (round0_env < 0) round0_env = getenv("IWPP_EDT_ROUND0") ? atoi(getenv("IWPP_EDT_ROUND0")) : 1;
     const bool round0 = s.raster && round0_env && r0;
     if (round0) *r0 = 1;
-    if (conn == 8)
-      round0 ? edt_init_key_rows_kernel<8, true><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s)
-             : edt_init_key_rows_kernel<8><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s);
+    // 4 cells per lane when every segment is full (IWPP_EDT_INIT4=0: off)
+    static int init4_env = -1;
+    if (init4_env < 0) init4_env = getenv("IWPP_EDT_INIT4") ? atoi(getenv("IWPP_EDT_INIT4")) : 1;
+    const bool four = init4_env && IWPP_KEY_PLANAR && W % 128 == 0 && ((uintptr_t)mask % 16) == 0;
+    const dim3 gd((unsigned)gb), bd(32 * kInitWarps);
+    if (four) {
+      if (conn == 8)
+        round0 ? edt_init_key_rows4_kernel<8, true><<<gd, bd, 0, st>>>(mask, W, H, s)
+               : edt_init_key_rows4_kernel<8><<<gd, bd, 0, st>>>(mask, W, H, s);
+      else
+        round0 ? edt_init_key_rows4_kernel<4, true><<<gd, bd, 0, st>>>(mask, W, H, s)
+               : edt_init_key_rows4_kernel<4><<<gd, bd, 0, st>>>(mask, W, H, s);
+    } else if (conn == 8)
+      round0 ? edt_init_key_rows_kernel<8, true><<<gd, bd, 0, st>>>(mask, W, H, s)
+             : edt_init_key_rows_kernel<8><<<gd, bd, 0, st>>>(mask, W, H, s);
     else
-      round0 ? edt_init_key_rows_kernel<4, true><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s)
-             : edt_init_key_rows_kernel<4><<<(int)gb, 32 * kInitWarps, 0, st>>>(mask, W, H, s);
+      round0 ? edt_init_key_rows_kernel<4, true><<<gd, bd, 0, st>>>(mask, W, H, s)
+             : edt_init_key_rows_kernel<4><<<gd, bd, 0, st>>>(mask, W, H, s);
   } else {
     if (conn == 8)
       edt_init_kernel<8><<<g, 256, 0, st>>>(mask, W, H, s);
