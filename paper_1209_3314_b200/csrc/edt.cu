@@ -439,8 +439,10 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows_kernel(cons
 // before this one is processed.  Same keys, same seeds (listed in another
 // order: the rounds' results do not depend on it).
 __device__ __forceinline__ unsigned nz4(unsigned w) {  // bit b: byte b of w is nonzero
-  const unsigned m = __vcmpne4(w, 0u);
-  return ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
+  // high bit of each byte = (low 7 bits nonzero) | top bit; then one multiply
+  // gathers bits 0 / 8 / 16 / 24 into bits 28-31 (the cross terms land below)
+  const unsigned m = (((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) & 0x80808080u;
+  return ((m >> 7) * 0x10204080u) >> 28;
 }
 template <int CONN, bool ROUND0 = false>
 __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows4_kernel(const uint8_t *__restrict__ mask,
@@ -451,7 +453,10 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows4_kernel(con
   unsigned nbuf = 0;
   unsigned long long nseed = 0;
   const int li = ROUND0 ? 1 : 0;
-  const long long segs_per_row = W / 128, nseg = segs_per_row * H;
+  // segments as 32-bit indices (W / 128 * H < 2^24 here), row = g >> shift
+  // when W / 128 is a power of two (64-bit division is ~60 instructions)
+  const unsigned spr = (unsigned)W / 128u, nseg = spr * (unsigned)H;
+  const int sh = (spr & (spr - 1u)) == 0u ? __ffs(spr) - 1 : -1;
   const size_t NN = (size_t)W * H;
   auto flush = [&]() {
     unsigned base = 0;
@@ -463,8 +468,14 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows4_kernel(con
   };
   // rows y-1, y, y+1 of segment g: this lane's word, and (lanes 0 / 31) the
   // byte just left / right of the segment; kOff outside the image
-  auto load = [&](long long g, unsigned (&w)[3], unsigned (&e)[3]) {
-    const int y = (int)(g / segs_per_row), x0 = (int)(g - (long long)y * segs_per_row) * 128;
+  auto seg_yx = [&](unsigned g, int &y, int &x0) {
+    const unsigned yy = sh >= 0 ? g >> sh : g / spr;
+    y = (int)yy;
+    x0 = (int)(g - yy * spr) * 128;
+  };
+  auto load = [&](unsigned g, unsigned (&w)[3], unsigned (&e)[3]) {
+    int y, x0;
+    seg_yx(g, y, x0);
 #pragma unroll
     for (int rr = 0; rr < 3; rr++) {
       const int yy = y + rr - 1;
@@ -475,14 +486,15 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows4_kernel(con
       e[rr] = (rin && (lane == 0 || lane == 31) && x0 + ex >= 0 && x0 + ex < W) ? (unsigned)__ldg(row + ex) : kOff;
     }
   };
-  const long long stride = (long long)gridDim.x * kInitWarps;
-  long long g = (long long)blockIdx.x * kInitWarps + wib;
+  const unsigned stride = gridDim.x * kInitWarps;
+  unsigned g = blockIdx.x * kInitWarps + wib;
   unsigned nw[3], ne[3];
   if (g < nseg) load(g, nw, ne);
   for (; g < nseg; g += stride) {
     unsigned w[3] = {nw[0], nw[1], nw[2]}, e[3] = {ne[0], ne[1], ne[2]};
     if (g + stride < nseg) load(g + stride, nw, ne);
-    const int y = (int)(g / segs_per_row), x0 = (int)(g - (long long)y * segs_per_row) * 128;
+    int y, x0;
+    seg_yx(g, y, x0);
     // 6-bit masks per row: bit 0 the cell left of my 4, bits 1-4 mine, bit 5
     // the one right of them (fg = a nonzero sample inside the image, bg = a
     // zero sample inside it; outside the image: neither)
@@ -499,9 +511,22 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows4_kernel(con
       fg[rr] = fl | (f4 << 1) | (fr << 5);
       bg[rr] = bl | (b4 << 1) | (br << 5);
     }
+    const size_t p = (size_t)y * W + x0 + 4 * lane;
+    ulonglong2 *k0 = reinterpret_cast<ulonglong2 *>(s.keys + p), *k1 = reinterpret_cast<ulonglong2 *>(s.keys + NN + p);
+    // the common case, warp-wide: no foreground near any of my cells (all
+    // background, own source, no seed) or no background near any (all
+    // foreground, INF, no offer, no seed)
+    const bool far_bg = (fg[0] | fg[1] | fg[2]) == 0u, far_fg = (bg[0] | bg[1] | bg[2]) == 0u;
+    if (__all_sync(FULL, far_bg || far_fg)) {
+      const uint32_t yx = ((uint32_t)y << 16) | (uint32_t)(x0 + 4 * lane);
+      const ulonglong2 a = far_bg ? make_ulonglong2(yx, yx + 1) : make_ulonglong2(KINF, KINF);
+      const ulonglong2 b = far_bg ? make_ulonglong2(yx + 2, yx + 3) : make_ulonglong2(KINF, KINF);
+      k0[0] = a, k0[1] = b, k1[0] = a, k1[1] = b;
+      continue;
+    }
     unsigned long long k[4];
     unsigned seeds = 0;
-    const uint32_t yu = (uint32_t)(y - 1) << 16, yc = (uint32_t)y << 16, yd = (uint32_t)(y + 1) << 16;
+    const uint32_t yc = (uint32_t)y << 16;
 #pragma unroll
     for (int b = 0; b < 4; b++) {
       const int c = b + 1;
@@ -513,26 +538,29 @@ __global__ void __launch_bounds__(32 * kInitWarps) edt_init_key_rows4_kernel(con
       unsigned long long kk = isbg ? (unsigned long long)(yc | x) : KINF;
       if (ROUND0) {
         if (isbg && near) nseed += 1;
-        if (!isbg) {  // round 0's offers: up, left, right, down; then the diagonals
-          if ((bg[0] >> c) & 1u) kk = (1ull << 32) | (yu | x);
-          else if ((bg[1] >> (c - 1)) & 1u) kk = (1ull << 32) | (yc | (x - 1));
-          else if ((bg[1] >> (c + 1)) & 1u) kk = (1ull << 32) | (yc | (x + 1));
-          else if ((bg[2] >> c) & 1u) kk = (1ull << 32) | (yd | x);
-          else if (CONN == 8) {
-            if ((bg[0] >> (c - 1)) & 1u) kk = (2ull << 32) | (yu | (x - 1));
-            else if ((bg[0] >> (c + 1)) & 1u) kk = (2ull << 32) | (yu | (x + 1));
-            else if ((bg[2] >> (c - 1)) & 1u) kk = (2ull << 32) | (yd | (x - 1));
-            else if ((bg[2] >> (c + 1)) & 1u) kk = (2ull << 32) | (yd | (x + 1));
+        if (!isbg) {
+          // round 0's offers in the order that breaks their ties: up, left,
+          // right, down; then up-left, up-right, down-left, down-right
+          // (branch-free: the first background neighbour in that order)
+          unsigned cand = ((bg[0] >> c) & 1u) | (((bg[1] >> (c - 1)) & 1u) << 1) |
+                          (((bg[1] >> (c + 1)) & 1u) << 2) | (((bg[2] >> c) & 1u) << 3);
+          if (CONN == 8)
+            cand |= (((bg[0] >> (c - 1)) & 1u) << 4) | (((bg[0] >> (c + 1)) & 1u) << 5) |
+                    (((bg[2] >> (c - 1)) & 1u) << 6) | (((bg[2] >> (c + 1)) & 1u) << 7);
+          if (cand) {
+            const unsigned i = (unsigned)__ffs(cand) - 1u;
+            // 2-bit fields per candidate: dy + 1, dx + 1
+            const unsigned dy = (0xA094u >> (2 * i)) & 3u, dx = (0x8861u >> (2 * i)) & 3u;
+            const uint32_t src = (((uint32_t)(y + (int)dy - 1)) << 16) | (x + dx - 1u);
+            kk = ((unsigned long long)(i < 4 ? 1u : 2u) << 32) | src;
+            seeds |= 1u << b;
           }
-          if (kk != KINF) seeds |= 1u << b;
         }
       } else if (isbg && near) {
         seeds |= 1u << b;
       }
       k[b] = kk;
     }
-    const size_t p = (size_t)y * W + x0 + 4 * lane;
-    ulonglong2 *k0 = reinterpret_cast<ulonglong2 *>(s.keys + p), *k1 = reinterpret_cast<ulonglong2 *>(s.keys + NN + p);
     k0[0] = make_ulonglong2(k[0], k[1]);
     k0[1] = make_ulonglong2(k[2], k[3]);
     k1[0] = make_ulonglong2(k[0], k[1]);
