@@ -46,7 +46,7 @@ SUMMARY_KEYS = {
     "imfill_16k": [("recon_tile_engine_bin_c8_16k", "tile_engine_bin_kernel", 3 * 16384 * 16384)],
     "edt_blob4k": [("edt_rounds_blob4k_c8", "edt_rounds_raster_kernel", None)],
     "edt_nuclei4k": [("edt_rounds_nuclei4k_c8", "edt_rounds_raster_kernel", None)],
-    "edt_nuclei64k": [("edt_init_nuclei64k", "edt_init_key_rows_kernel", 17 * 65536 * 65536),
+    "edt_nuclei64k": [("edt_init_nuclei64k", "edt_init_key_rows", 17 * 65536 * 65536),
                       ("edt_finalize_nuclei64k", "edt_finalize_key_kernel", 20 * 65536 * 65536)],
     "edt_mg_blob4k": [("edt_mg_rounds_blob4k_4slabs", "mg_rounds_kernel", None)],
 }
@@ -159,7 +159,7 @@ def main():
                f"{'kernel':72s} {'launches':>8s} {'total_us':>10s} {'avg_us':>9s} {'share':>7s}"]
         for k, (n, ns) in sorted(agg.items(), key=lambda x: -x[1][1]):
             out.append(f"{k[:72]:72s} {n:8d} {ns / 1e3:10.1f} {ns / 1e3 / n:9.2f} {ns / tot * 100:6.1f}%")
-        open(os.path.join(PROF, "r02_launches.txt"), "w").write("\n".join(out) + "\n")
+        open(os.path.join(PROF, f"{TAG}_launches.txt"), "w").write("\n".join(out) + "\n")
     print("ok")
 
 
