@@ -54,3 +54,32 @@ def test_sm100a_cubin_present():
         pytest.skip("cuobjdump not available")
     out = subprocess.run(["cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The ctypes mirrors in _lib.py have the C layout of the header's structs
+    (size and every field offset, as gcc lays them out)."""
+    import shutil
+    import subprocess
+    from paper_1209_3314_b200 import _lib
+    if not shutil.which("gcc"):
+        pytest.skip("gcc not available")
+    pairs = [("iwpp_recon_opts", _lib.ReconOpts), ("iwpp_stats", _lib.Stats),
+             ("iwpp_edt_mg_slab", _lib.MgSlab)]
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "iwpp_b200.h"', "int main(void) {"]
+    for cname, py in pairs:
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)],
+                   check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                        check=True).stdout.splitlines())
+    for cname, py in pairs:
+        assert int(got[f"{cname} size"]) == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(got[f"{cname} {fname}"]) == getattr(py, fname).offset, (cname, fname)

@@ -535,3 +535,13 @@ def test_host_pipeline_pinned_output(gw, conn):
         I2[row, 7] = 0
         with pytest.raises(Exception):
             _recon_host_pinned(bad, I2, conn, 64)
+
+
+@pytest.mark.parametrize("dt,code,h", [(np.uint16, 1, 9000), (np.int32, 2, 1 << 27)])
+def test_host_pipeline_pinned_output_wide(gw, dt, code, h):
+    """The mapped last transfer for the 16/32-bit kinds (row bytes 2 / 4 x W)."""
+    for shape, rows in [((1000, 300), 64), ((1024, 512), 0), ((777, 130), 128)]:
+        M, I = oracle.gray_pair(shape, 21, h=h, dtype=dt)
+        want = oracle.recon_fh(M, I, 8)
+        got, st = _recon_host_pinned(M, I, 8, rows, code=code)
+        assert np.array_equal(got, want), (shape, rows, dt)
