@@ -2170,6 +2170,24 @@ __device__ __forceinline__ void bin_hdil(unsigned w0, unsigned w1, unsigned hl, 
   d1 = w1 | (w1 << 1) | (w0 >> 31) | (w1 >> 1) | (hr << 31);
 }
 
+// Row run fill: every mask bit joined to a set bit by a run of mask bits,
+// in one step.  For seeds s within mask m, m + s carries from a run's
+// lowest seed to the run's top (and one bit past it, outside m), so
+// ((m + s) ^ m) | s, masked by m, is the run above each lowest seed; the
+// other direction is the same on the bit-reversed row.
+#ifndef IWPP_BIN_RUNFILL
+#define IWPP_BIN_RUNFILL 1
+#endif
+__device__ __forceinline__ unsigned long long up_fill(unsigned long long s, unsigned long long m) {
+  return (((m + s) ^ m) | s) & m;
+}
+__device__ __forceinline__ void row_fill(unsigned &w0, unsigned &w1, unsigned m0, unsigned m1) {
+  const unsigned long long s = ((unsigned long long)w1 << 32) | w0, m = ((unsigned long long)m1 << 32) | m0;
+  const unsigned long long f = up_fill(s, m) | __brevll(up_fill(__brevll(s), __brevll(m)));
+  w0 = (unsigned)f;
+  w1 = (unsigned)(f >> 32);
+}
+
 template <int CONN>
 __device__ __forceinline__ int bin_fixpoint(unsigned &a0, unsigned &a1, unsigned &b0, unsigned &b1,
                                             unsigned ma0, unsigned ma1, unsigned mb0, unsigned mb1,
@@ -2214,7 +2232,11 @@ __device__ __forceinline__ int bin_fixpoint(unsigned &a0, unsigned &a1, unsigned
       Db0 |= ub0 | db0;
       Db1 |= ub1 | db1;
     }
-    const unsigned na0 = ma0 & Da0, na1 = ma1 & Da1, nb0 = mb0 & Db0, nb1 = mb1 & Db1;
+    unsigned na0 = ma0 & Da0, na1 = ma1 & Da1, nb0 = mb0 & Db0, nb1 = mb1 & Db1;
+    if (IWPP_BIN_RUNFILL) {  // whole row runs in one step
+      row_fill(na0, na1, ma0, ma1);
+      row_fill(nb0, nb1, mb0, mb1);
+    }
     const bool ch = ((na0 ^ a0) | (na1 ^ a1) | (nb0 ^ b0) | (nb1 ^ b1)) != 0;
     a0 = na0;
     a1 = na1;

@@ -38,4 +38,8 @@ for conn in (4, 8):
             torch.cuda.synchronize()
             if r >= 2:
                 ts.append(a.elapsed_time(b))
-        print(f"imfill 16K c{conn} {form}: {np.median(ts):.3f} ms (min {min(ts):.3f})", flush=True)
+        cnt = (_lib.ctypes.c_uint64 * 16)()
+        L.iwpp_recon_engine_counters(_lib.ptr(ws), W, H, cnt, 16, _lib.stream_ptr())
+        ntiles = ((W + 63) // 64) * ((H + 63) // 64)
+        print(f"imfill 16K c{conn} {form}: {np.median(ts):.3f} ms (min {min(ts):.3f}); activations {cnt[0]} "
+              f"({cnt[0] / ntiles:.2f}/tile) reruns {cnt[1]} steps/act {cnt[6] / max(cnt[0], 1):.2f}", flush=True)
