@@ -2188,6 +2188,24 @@ __device__ __forceinline__ void row_fill(unsigned &w0, unsigned &w1, unsigned m0
   w1 = (unsigned)(f >> 32);
 }
 
+// Column run fill across the warp's 32 rows (one word of columns per lane):
+// a Kogge-Stone segmented scan down and up the lanes, g |= p & g[lane - d],
+// p &= p[lane - d] (p: the mask all along the span).
+#ifndef IWPP_BIN_COLFILL
+#define IWPP_BIN_COLFILL 1
+#endif
+__device__ __forceinline__ unsigned col_fill(unsigned x, unsigned m, int lane) {
+  unsigned g = x, p = m, h = x, q = m;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned gu = __shfl_up_sync(FULL, g, d), pu = __shfl_up_sync(FULL, p, d);
+    const unsigned hd = __shfl_down_sync(FULL, h, d), qd = __shfl_down_sync(FULL, q, d);
+    if (lane >= d) g |= p & gu, p &= pu;
+    if (lane + d < 32) h |= q & hd, q &= qd;
+  }
+  return g | h;
+}
+
 template <int CONN>
 __device__ __forceinline__ int bin_fixpoint(unsigned &a0, unsigned &a1, unsigned &b0, unsigned &b1,
                                             unsigned ma0, unsigned ma1, unsigned mb0, unsigned mb1,
@@ -2236,6 +2254,12 @@ __device__ __forceinline__ int bin_fixpoint(unsigned &a0, unsigned &a1, unsigned
     if (IWPP_BIN_RUNFILL) {  // whole row runs in one step
       row_fill(na0, na1, ma0, ma1);
       row_fill(nb0, nb1, mb0, mb1);
+    }
+    if (IWPP_BIN_COLFILL) {  // and whole column runs within each 32-row half
+      na0 = col_fill(na0, ma0, lane);
+      na1 = col_fill(na1, ma1, lane);
+      nb0 = col_fill(nb0, mb0, lane);
+      nb1 = col_fill(nb1, mb1, lane);
     }
     const bool ch = ((na0 ^ a0) | (na1 ^ a1) | (nb0 ^ b0) | (nb1 ^ b1)) != 0;
     a0 = na0;
