@@ -60,6 +60,15 @@ check("recon smem engine, forced overflow", np.array_equal(got, oracle.recon_fh(
 J, I = oracle.gray_pair((1024, 512), 4, h=40)
 got = gw.reconstruct(J, I, 8, pipeline_rows=128)
 check("recon host pipeline", np.array_equal(got, oracle.recon_fh(J, I, 8)))
+# host pipeline into a page-locked output (the mapped last transfer)
+J, I = oracle.gray_pair((1024, 512), 8, h=40)
+pm, pi = torch.from_numpy(J).pin_memory(), torch.from_numpy(I).pin_memory()
+po = torch.empty_like(pm).pin_memory()
+wsh = _lib.workspace(L.iwpp_recon_host_workspace_bytes(512, 1024, 0, 8))
+o = gw.recon._opts(None, pipeline_rows=128)
+_lib.check(L.iwpp_recon_host(_lib.ptr(po.numpy()), _lib.ptr(pm.numpy()), _lib.ptr(pi.numpy()), 512, 1024, 0, 8,
+                             _lib.ptr(wsh), wsh.numel(), _lib.ctypes.byref(o), None, _lib.stream_ptr()))
+check("recon host pipeline, pinned output", np.array_equal(po.numpy(), oracle.recon_fh(J, I, 8)))
 # stage kernels: sweeps, seed scan, passes
 from paper_1209_3314_b200.recon import seed_scan  # noqa: E402
 J, I = oracle.gray_pair((160, 200), 6, h=40)
@@ -78,6 +87,12 @@ for mode in (0, 3, 4, 1):
     check(f"edt engine {mode}", np.array_equal(vm.vr.cpu().numpy(), vr_ref)
           and dist.data.cpu().numpy().tobytes() == d_ref.tobytes())
 _lib.check(L.iwpp_edt_set_engine(0), "set_engine")
+# the 4-cells-per-lane init (W % 128 == 0), both connectivities
+m2 = oracle.gen_synthetic_mask(256, 96, 50, 7)
+for conn in (4, 8):
+    vr2, d2 = oracle.edt(m2, conn)
+    vm, dist = gw.edt(gw.Image2D(m2.shape[1], m2.shape[0], "binary", dev(m2)), gw.StructuringElement(conn))
+    check(f"edt init4 c{conn}", np.array_equal(vm.vr.cpu().numpy(), vr2) and dist.data.cpu().numpy().tobytes() == d2.tobytes())
 from paper_1209_3314_b200.distributed import edt_slabs_local_device  # noqa: E402
 vr, d, _ = edt_slabs_local_device(m, 3, 8)
 check("edt multi-slab device protocol (3 slabs)", np.array_equal(vr, vr_ref) and d.tobytes() == d_ref.tobytes())
