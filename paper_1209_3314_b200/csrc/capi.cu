@@ -155,7 +155,8 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
   // a separate marker: the plain u8 path hands it to the engine (copied in
   // the fused kernel's prologue); everything else starts from a copy in J
   const void *msrc = opts && opts->marker != J ? opts->marker : nullptr;
-  if (msrc && !(dtype == IWPP_U8 && (!opts || (opts->sweeps <= 0 && !opts->slab_rows)))) {
+  // (binary: the bit planes are packed straight from the marker)
+  if (msrc && !((dtype == IWPP_U8 || dtype == IWPP_BIN) && (!opts || (opts->sweeps <= 0 && !opts->slab_rows)))) {
     IWPP_CUDA_TRY(cudaMemcpyAsync(J, msrc, (size_t)W * H * elem_size(dtype), cudaMemcpyDeviceToDevice, st));
     msrc = nullptr;
   }
@@ -212,8 +213,9 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
   if (dtype == IWPP_BIN) {  // the bit-plane engine: pack, propagate, unpack
     const size_t nw = recon::bin_plane_words(W, H);
     uint32_t *Jb = c.take<uint32_t>(nw), *Ib = c.take<uint32_t>(nw);
-    if ((rc = recon::bin_pack(J, (int)W, (int)H, Jb, st))) return rc;
+    if ((rc = recon::bin_pack(msrc ? msrc : J, (int)W, (int)H, Jb, st))) return rc;
     if ((rc = recon::bin_pack(I, (int)W, (int)H, Ib, st))) return rc;
+    eo.src = nullptr;  // (J is written whole by the unpack)
     if ((rc = recon::run_tile_engine(Jb, Ib, (int)W, (int)H, IWPP_BIN, conn, w.q, w.counters, eo, st)))
       return rc;
     if ((rc = recon::bin_unpack(Jb, (int)W, (int)H, J, st))) return rc;

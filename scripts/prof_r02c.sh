@@ -16,12 +16,15 @@ full() {
   python scripts/ncu_sass_stalls.py $OUT/$1.ncu-rep 20 > $OUT/$1.sass.txt 2>/dev/null
   rm -f $OUT/$1.ncu-rep
 }
+if [ $# -gt 0 ]; then  # only the named cases: prof_r02c.sh CASE REGEX COUNT
+  full "$1" "$2" "$3"; exit 0
+fi
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-extras --no-cpu > $OUT/launches.log 2>&1
 echo "launches rc=$?"
 full recon_u8_4k 'tile_engine_reg_kernel' 1
 full recon_u8_64k 'tile_engine_reg_kernel' 1
-full imfill_16k 'tile_engine_bin_kernel|bin_pack_kernel|bin_unpack_kernel' 3
+full imfill_16k 'tile_engine_bin_kernel|bin_pack_kernel|bin_unpack_kernel' 4
 full edt_nuclei4k 'edt_rounds_raster_kernel|edt_init_key_rows|edt_finalize_key_kernel' 3
 full edt_nuclei64k 'edt_init_key_rows|edt_finalize_key_kernel' 2
 du -sh $OUT
