@@ -2110,12 +2110,14 @@ __global__ void __launch_bounds__(kCtaThreads, kReg32CtaMinBlocks)
 // The "binary" element kind (grid.py binary, imfill).  iwpp_recon packs the
 // 0 / 255 marker and mask into bit planes (one bit per pixel, ceil(W/32)
 // words per row) and unpacks the result afterwards, so the engine moves
-// 1/8 of the bytes and does no byte arithmetic.  A warp owns a 64 x 64 tile
-// -- lane = rows lane and lane + 32, two words per row -- and a Jacobi step
+// 1/8 of the bytes and does no byte arithmetic.  A warp owns a 128 x 128
+// tile -- lane = rows lane + 32 q (q = 0..3), four words per row -- and a
+// Jacobi step
 //     J <- I & (J | J_up | J_down | the same shifted by one column)
-// is a few dozen instructions for 4096 pixels.  Binary fills are long narrow
-// fronts crossing the image tile by tile; 64-pixel tiles halve the tile hops
-// on that critical path.  Same queue protocol, on a 64-pixel tile grid.
+// plus whole row and column run fills is a few hundred instructions for
+// 16384 pixels.  Binary fills are long narrow fronts crossing the image tile
+// by tile; 128-pixel tiles quarter the tile hops of 32-pixel tiles on that
+// critical path.  Same queue protocol, on a 128-pixel tile grid.
 
 __device__ __forceinline__ unsigned bitw(const uint32_t *P, int WW, int H, int wx, int gy, bool cg) {
   if (gy < 0 || gy >= H || wx < 0 || wx >= WW) return 0u;
@@ -2123,150 +2125,226 @@ __device__ __forceinline__ unsigned bitw(const uint32_t *P, int WW, int H, int w
   return cg ? __ldcg(p) : __ldg(p);
 }
 
+constexpr int BNR = TSB / 32;  // rows per lane: lane + 32 q, q = 0 .. BNR - 1
+constexpr int BNW = TSB / 32;  // 32-bit words per tile row
+static_assert(BNR == 4 && BNW == 4, "the binary engine's masks assume 128 x 128 tiles");
+
 struct BinHalo {
-  unsigned row0, row1, rowI0, rowI1;  // lane 0: the row above; lane 31: the row below
-  unsigned la, ra, lIa, rIa;          // bits left / right of row lane (J, I)
-  unsigned lb, rb, lIb, rIb;          // ... of row lane + 32
-  unsigned cl, cr, clI, crI;          // lane 0: corners above; lane 31: corners below
+  unsigned row[BNW], rowI[BNW];  // lane 0: the row above; lane 31: the row below
+  unsigned l, r, lI, rI;         // bit q: the cell left / right of row lane + 32 q (J, I)
+  unsigned cl, cr, clI, crI;     // lane 0: corners above; lane 31: corners below
 };
 
-// the tile (rows lane, lane + 32; words wx0, wx0 + 1) and its halo: every
-// load issued before any is used
+// the tile (rows lane + 32 q, words wx .. wx + 3) and its halo: every load
+// issued before any is used (16-byte loads when the plane's rows allow)
 __device__ __forceinline__ void bin_load(const EngineArgs &a, int x0, int y0, int lane, bool tile,
-                                         unsigned *jt, unsigned *mt, BinHalo &h) {
+                                         unsigned (&jt)[BNR][BNW], unsigned (&mt)[BNR][BNW],
+                                         BinHalo &h) {
   const uint32_t *J = (const uint32_t *)a.J, *I = (const uint32_t *)a.I;
-  const int WW = a.WW, wx = x0 >> 5, ya = y0 + lane, yb = ya + 32;
+  const int WW = a.WW, wx = x0 >> 5;
+  const bool vec = (WW & 3) == 0 && wx + BNW <= WW;
   const int hy = lane == 0 ? y0 - 1 : (lane == 31 ? y0 + TSB : -1);
   if (tile) {
-    jt[0] = bitw(J, WW, a.H, wx, ya, true);
-    jt[1] = bitw(J, WW, a.H, wx + 1, ya, true);
-    jt[2] = bitw(J, WW, a.H, wx, yb, true);
-    jt[3] = bitw(J, WW, a.H, wx + 1, yb, true);
-    mt[0] = bitw(I, WW, a.H, wx, ya, false);
-    mt[1] = bitw(I, WW, a.H, wx + 1, ya, false);
-    mt[2] = bitw(I, WW, a.H, wx, yb, false);
-    mt[3] = bitw(I, WW, a.H, wx + 1, yb, false);
+#pragma unroll
+    for (int q = 0; q < BNR; q++) {
+      const int gy = y0 + lane + 32 * q;
+      if (vec && gy < a.H) {
+        const uint4 vj = __ldcg(reinterpret_cast<const uint4 *>(J + (size_t)gy * WW + wx));
+        const uint4 vi = __ldg(reinterpret_cast<const uint4 *>(I + (size_t)gy * WW + wx));
+        jt[q][0] = vj.x; jt[q][1] = vj.y; jt[q][2] = vj.z; jt[q][3] = vj.w;
+        mt[q][0] = vi.x; mt[q][1] = vi.y; mt[q][2] = vi.z; mt[q][3] = vi.w;
+      } else {
+#pragma unroll
+        for (int w = 0; w < BNW; w++) {
+          jt[q][w] = bitw(J, WW, a.H, wx + w, gy, true);
+          mt[q][w] = bitw(I, WW, a.H, wx + w, gy, false);
+        }
+      }
+    }
   }
-  const unsigned jla = bitw(J, WW, a.H, wx - 1, ya, true), jra = bitw(J, WW, a.H, wx + 2, ya, true);
-  const unsigned jlb = bitw(J, WW, a.H, wx - 1, yb, true), jrb = bitw(J, WW, a.H, wx + 2, yb, true);
-  const unsigned ila = bitw(I, WW, a.H, wx - 1, ya, false), ira = bitw(I, WW, a.H, wx + 2, ya, false);
-  const unsigned ilb = bitw(I, WW, a.H, wx - 1, yb, false), irb = bitw(I, WW, a.H, wx + 2, yb, false);
-  const unsigned jhl = bitw(J, WW, a.H, wx - 1, hy, true), jhr = bitw(J, WW, a.H, wx + 2, hy, true);
-  const unsigned ihl = bitw(I, WW, a.H, wx - 1, hy, false), ihr = bitw(I, WW, a.H, wx + 2, hy, false);
-  h.row0 = bitw(J, WW, a.H, wx, hy, true);
-  h.row1 = bitw(J, WW, a.H, wx + 1, hy, true);
-  h.rowI0 = bitw(I, WW, a.H, wx, hy, false);
-  h.rowI1 = bitw(I, WW, a.H, wx + 1, hy, false);
-  h.la = jla >> 31; h.ra = jra & 1u; h.lIa = ila >> 31; h.rIa = ira & 1u;
-  h.lb = jlb >> 31; h.rb = jrb & 1u; h.lIb = ilb >> 31; h.rIb = irb & 1u;
+  unsigned jl[BNR], jr[BNR], il[BNR], ir[BNR];
+#pragma unroll
+  for (int q = 0; q < BNR; q++) {
+    const int gy = y0 + lane + 32 * q;
+    jl[q] = bitw(J, WW, a.H, wx - 1, gy, true);
+    jr[q] = bitw(J, WW, a.H, wx + BNW, gy, true);
+    il[q] = bitw(I, WW, a.H, wx - 1, gy, false);
+    ir[q] = bitw(I, WW, a.H, wx + BNW, gy, false);
+  }
+#pragma unroll
+  for (int w = 0; w < BNW; w++) {
+    h.row[w] = bitw(J, WW, a.H, wx + w, hy, true);
+    h.rowI[w] = bitw(I, WW, a.H, wx + w, hy, false);
+  }
+  const unsigned jhl = bitw(J, WW, a.H, wx - 1, hy, true), jhr = bitw(J, WW, a.H, wx + BNW, hy, true);
+  const unsigned ihl = bitw(I, WW, a.H, wx - 1, hy, false), ihr = bitw(I, WW, a.H, wx + BNW, hy, false);
+  h.l = h.r = h.lI = h.rI = 0;
+#pragma unroll
+  for (int q = 0; q < BNR; q++) {
+    h.l |= (jl[q] >> 31) << q;
+    h.r |= (jr[q] & 1u) << q;
+    h.lI |= (il[q] >> 31) << q;
+    h.rI |= (ir[q] & 1u) << q;
+  }
   h.cl = jhl >> 31; h.cr = jhr & 1u; h.clI = ihl >> 31; h.crI = ihr & 1u;
 }
 
-// 3x3 (8-conn) / cross (4-conn) dilation of a 64-bit row (w0, w1) with the
-// halo bits at its ends
-__device__ __forceinline__ void bin_hdil(unsigned w0, unsigned w1, unsigned hl, unsigned hr,
-                                         unsigned &d0, unsigned &d1) {
-  d0 = w0 | (w0 << 1) | hl | (w0 >> 1) | (w1 << 31);
-  d1 = w1 | (w1 << 1) | (w0 >> 31) | (w1 >> 1) | (hr << 31);
+// Vertical neighbours of a column of per-row bits packed as bit q = row
+// lane + 32 q (the rows above / below within the tile; `in_up` / `in_dn`:
+// lane 0's bit 0 above / lane 31's bit BNR-1 below come from outside).
+__device__ __forceinline__ unsigned bits_up(unsigned b, int lane, unsigned in_up) {
+  const unsigned R = __shfl_sync(FULL, b, (lane + 31) & 31);  // lane - 1 (lane 0: lane 31)
+  return lane == 0 ? (((R << 1) & ((1u << BNR) - 2u)) | in_up) : R;
+}
+__device__ __forceinline__ unsigned bits_dn(unsigned b, int lane, unsigned in_dn) {
+  const unsigned S = __shfl_sync(FULL, b, (lane + 1) & 31);  // lane + 1 (lane 31: lane 0)
+  return lane == 31 ? ((S >> 1) | (in_dn << (BNR - 1))) : S;
+}
+
+// 3x3 (8-conn) / cross (4-conn) horizontal dilation of a 128-bit row with
+// the halo bits at its ends
+__device__ __forceinline__ void bin_hdil(const unsigned (&v)[BNW], unsigned hl, unsigned hr,
+                                         unsigned (&d)[BNW]) {
+#pragma unroll
+  for (int w = 0; w < BNW; w++)
+    d[w] = v[w] | (v[w] << 1) | (v[w] >> 1) | (w ? v[w - 1] >> 31 : hl) |
+           (w < BNW - 1 ? v[w + 1] << 31 : hr << 31);
 }
 
 // Row run fill: every mask bit joined to a set bit by a run of mask bits,
 // in one step.  For seeds s within mask m, m + s carries from a run's
 // lowest seed to the run's top (and one bit past it, outside m), so
 // ((m + s) ^ m) | s, masked by m, is the run above each lowest seed; the
-// other direction is the same on the bit-reversed row.
+// other direction is the same on the bit-reversed row.  Rows are 128 bits:
+// one add-with-carry chain.
 #ifndef IWPP_BIN_RUNFILL
 #define IWPP_BIN_RUNFILL 1
 #endif
-__device__ __forceinline__ unsigned long long up_fill(unsigned long long s, unsigned long long m) {
-  return (((m + s) ^ m) | s) & m;
+__device__ __forceinline__ void up_fill128(const unsigned (&s)[BNW], const unsigned (&m)[BNW],
+                                           unsigned (&f)[BNW]) {
+  unsigned t0, t1, t2, t3;
+  asm("add.cc.u32 %0, %4, %8;\n\t"
+      "addc.cc.u32 %1, %5, %9;\n\t"
+      "addc.cc.u32 %2, %6, %10;\n\t"
+      "addc.u32 %3, %7, %11;"
+      : "=r"(t0), "=r"(t1), "=r"(t2), "=r"(t3)
+      : "r"(m[0]), "r"(m[1]), "r"(m[2]), "r"(m[3]), "r"(s[0]), "r"(s[1]), "r"(s[2]), "r"(s[3]));
+  f[0] = ((t0 ^ m[0]) | s[0]) & m[0];
+  f[1] = ((t1 ^ m[1]) | s[1]) & m[1];
+  f[2] = ((t2 ^ m[2]) | s[2]) & m[2];
+  f[3] = ((t3 ^ m[3]) | s[3]) & m[3];
 }
-__device__ __forceinline__ void row_fill(unsigned &w0, unsigned &w1, unsigned m0, unsigned m1) {
-  const unsigned long long s = ((unsigned long long)w1 << 32) | w0, m = ((unsigned long long)m1 << 32) | m0;
-  const unsigned long long f = up_fill(s, m) | __brevll(up_fill(__brevll(s), __brevll(m)));
-  w0 = (unsigned)f;
-  w1 = (unsigned)(f >> 32);
+__device__ __forceinline__ void row_fill(unsigned (&x)[BNW], const unsigned (&m)[BNW]) {
+  unsigned f[BNW], rs[BNW], rm[BNW], g[BNW];
+  up_fill128(x, m, f);
+#pragma unroll
+  for (int w = 0; w < BNW; w++) {
+    rs[w] = __brev(x[BNW - 1 - w]);
+    rm[w] = __brev(m[BNW - 1 - w]);
+  }
+  up_fill128(rs, rm, g);
+#pragma unroll
+  for (int w = 0; w < BNW; w++) x[w] = f[w] | __brev(g[BNW - 1 - w]);
 }
 
-// Column run fill across the warp's 32 rows (one word of columns per lane):
-// a Kogge-Stone segmented scan down and up the lanes, g |= p & g[lane - d],
-// p &= p[lane - d] (p: the mask all along the span).
+// Column run fill over the tile's 128 rows, one word of columns: a
+// Kogge-Stone segmented scan down and up the lanes inside each 32-row
+// quarter (g |= p & g[lane - d], p &= p[lane - d]; p: the mask all along
+// the span), then the carries across the quarters (a quarter's top rows
+// take the fill of the row above it where the mask runs unbroken from
+// there; the same upwards).
 #ifndef IWPP_BIN_COLFILL
 #define IWPP_BIN_COLFILL 1
 #endif
-__device__ __forceinline__ unsigned col_fill(unsigned x, unsigned m, int lane) {
-  unsigned g = x, p = m, h = x, q = m;
+__device__ __forceinline__ void col_fill(unsigned (&x)[BNR], const unsigned (&m)[BNR], int lane) {
+  unsigned g[BNR], p[BNR], h[BNR], r[BNR];
+#pragma unroll
+  for (int q = 0; q < BNR; q++) {
+    g[q] = h[q] = x[q];
+    p[q] = r[q] = m[q];
+  }
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    const unsigned gu = __shfl_up_sync(FULL, g, d), pu = __shfl_up_sync(FULL, p, d);
-    const unsigned hd = __shfl_down_sync(FULL, h, d), qd = __shfl_down_sync(FULL, q, d);
-    if (lane >= d) g |= p & gu, p &= pu;
-    if (lane + d < 32) h |= q & hd, q &= qd;
+#pragma unroll
+    for (int q = 0; q < BNR; q++) {
+      const unsigned gu = __shfl_up_sync(FULL, g[q], d), pu = __shfl_up_sync(FULL, p[q], d);
+      const unsigned hd = __shfl_down_sync(FULL, h[q], d), rd = __shfl_down_sync(FULL, r[q], d);
+      if (lane >= d) g[q] |= p[q] & gu, p[q] &= pu;
+      if (lane + d < 32) h[q] |= r[q] & hd, r[q] &= rd;
+    }
   }
-  return g | h;
+#pragma unroll
+  for (int q = 1; q < BNR; q++) g[q] |= p[q] & __shfl_sync(FULL, g[q - 1], 31);
+#pragma unroll
+  for (int q = BNR - 2; q >= 0; q--) h[q] |= r[q] & __shfl_sync(FULL, h[q + 1], 0);
+#pragma unroll
+  for (int q = 0; q < BNR; q++) x[q] = g[q] | h[q];
 }
 
 template <int CONN>
-__device__ __forceinline__ int bin_fixpoint(unsigned &a0, unsigned &a1, unsigned &b0, unsigned &b1,
-                                            unsigned ma0, unsigned ma1, unsigned mb0, unsigned mb1,
+__device__ __forceinline__ int bin_fixpoint(unsigned (&A)[BNR][BNW], const unsigned (&M)[BNR][BNW],
                                             const BinHalo &h, int lane, bool &changed) {
-  // halo column bits, vertically dilated for 8-conn (rows lane, lane + 32)
-  unsigned hla = h.la, hra = h.ra, hlb = h.lb, hrb = h.rb;
+  // halo column bits (bit q: row lane + 32 q), vertically dilated for 8-conn
+  unsigned hl = h.l, hr = h.r;
   if (CONN == 8) {
-    unsigned lau = __shfl_up_sync(FULL, h.la, 1), lad = __shfl_down_sync(FULL, h.la, 1);
-    unsigned rau = __shfl_up_sync(FULL, h.ra, 1), rad = __shfl_down_sync(FULL, h.ra, 1);
-    unsigned lbu = __shfl_up_sync(FULL, h.lb, 1), lbd = __shfl_down_sync(FULL, h.lb, 1);
-    unsigned rbu = __shfl_up_sync(FULL, h.rb, 1), rbd = __shfl_down_sync(FULL, h.rb, 1);
-    const unsigned lb0 = __shfl_sync(FULL, h.lb, 0), rb0 = __shfl_sync(FULL, h.rb, 0);
-    const unsigned la31 = __shfl_sync(FULL, h.la, 31), ra31 = __shfl_sync(FULL, h.ra, 31);
-    if (lane == 0) { lau = h.cl; rau = h.cr; lbu = la31; rbu = ra31; }
-    if (lane == 31) { lad = lb0; rad = rb0; lbd = h.cl; rbd = h.cr; }
-    hla = h.la | lau | lad;
-    hra = h.ra | rau | rad;
-    hlb = h.lb | lbu | lbd;
-    hrb = h.rb | rbu | rbd;
+    hl = h.l | bits_up(h.l, lane, h.cl) | bits_dn(h.l, lane, h.cl);
+    hr = h.r | bits_up(h.r, lane, h.cr) | bits_dn(h.r, lane, h.cr);
   }
   int steps = 0;
   for (;;) {
     steps++;
-    // rows above / below: row lane +- 1 and row lane + 32 +- 1
-    unsigned ua0 = __shfl_up_sync(FULL, a0, 1), ua1 = __shfl_up_sync(FULL, a1, 1);
-    unsigned da0 = __shfl_down_sync(FULL, a0, 1), da1 = __shfl_down_sync(FULL, a1, 1);
-    unsigned ub0 = __shfl_up_sync(FULL, b0, 1), ub1 = __shfl_up_sync(FULL, b1, 1);
-    unsigned db0 = __shfl_down_sync(FULL, b0, 1), db1 = __shfl_down_sync(FULL, b1, 1);
-    const unsigned b00 = __shfl_sync(FULL, b0, 0), b10 = __shfl_sync(FULL, b1, 0);
-    const unsigned a031 = __shfl_sync(FULL, a0, 31), a131 = __shfl_sync(FULL, a1, 31);
-    if (lane == 0) { ua0 = h.row0; ua1 = h.row1; ub0 = a031; ub1 = a131; }
-    if (lane == 31) { da0 = b00; da1 = b10; db0 = h.row0; db1 = h.row1; }
-    unsigned Da0, Da1, Db0, Db1;
-    if (CONN == 8) {
-      bin_hdil(a0 | ua0 | da0, a1 | ua1 | da1, hla, hra, Da0, Da1);
-      bin_hdil(b0 | ub0 | db0, b1 | ub1 | db1, hlb, hrb, Db0, Db1);
-    } else {
-      bin_hdil(a0, a1, h.la, h.ra, Da0, Da1);
-      bin_hdil(b0, b1, h.lb, h.rb, Db0, Db1);
-      Da0 |= ua0 | da0;
-      Da1 |= ua1 | da1;
-      Db0 |= ub0 | db0;
-      Db1 |= ub1 | db1;
+    unsigned N[BNR][BNW];
+    // rows above / below: the neighbouring lane, across quarters through
+    // lanes 0 / 31, and the halo rows at the tile's top / bottom
+#pragma unroll
+    for (int w = 0; w < BNW; w++) {
+      unsigned R[BNR], S[BNR];
+#pragma unroll
+      for (int q = 0; q < BNR; q++) {
+        R[q] = __shfl_sync(FULL, A[q][w], (lane + 31) & 31);
+        S[q] = __shfl_sync(FULL, A[q][w], (lane + 1) & 31);
+      }
+#pragma unroll
+      for (int q = 0; q < BNR; q++) {
+        const unsigned up = lane == 0 ? (q ? R[q - 1] : h.row[w]) : R[q];
+        const unsigned dn = lane == 31 ? (q < BNR - 1 ? S[q + 1] : h.row[w]) : S[q];
+        N[q][w] = CONN == 8 ? (A[q][w] | up | dn) : (up | dn);
+      }
     }
-    unsigned na0 = ma0 & Da0, na1 = ma1 & Da1, nb0 = mb0 & Db0, nb1 = mb1 & Db1;
-    if (IWPP_BIN_RUNFILL) {  // whole row runs in one step
-      row_fill(na0, na1, ma0, ma1);
-      row_fill(nb0, nb1, mb0, mb1);
+#pragma unroll
+    for (int q = 0; q < BNR; q++) {
+      unsigned D[BNW];
+      if (CONN == 8) {
+        bin_hdil(N[q], (hl >> q) & 1u, (hr >> q) & 1u, D);
+      } else {
+        bin_hdil(A[q], (h.l >> q) & 1u, (h.r >> q) & 1u, D);
+#pragma unroll
+        for (int w = 0; w < BNW; w++) D[w] |= N[q][w];
+      }
+#pragma unroll
+      for (int w = 0; w < BNW; w++) N[q][w] = M[q][w] & D[w];
+      if (IWPP_BIN_RUNFILL) row_fill(N[q], M[q]);  // whole row runs in one step
     }
-    if (IWPP_BIN_COLFILL) {  // and whole column runs within each 32-row half
-      na0 = col_fill(na0, ma0, lane);
-      na1 = col_fill(na1, ma1, lane);
-      nb0 = col_fill(nb0, mb0, lane);
-      nb1 = col_fill(nb1, mb1, lane);
+    if (IWPP_BIN_COLFILL) {  // and whole column runs of the tile
+#pragma unroll
+      for (int w = 0; w < BNW; w++) {
+        unsigned x[BNR], m[BNR];
+#pragma unroll
+        for (int q = 0; q < BNR; q++) x[q] = N[q][w], m[q] = M[q][w];
+        col_fill(x, m, lane);
+#pragma unroll
+        for (int q = 0; q < BNR; q++) N[q][w] = x[q];
+      }
     }
-    const bool ch = ((na0 ^ a0) | (na1 ^ a1) | (nb0 ^ b0) | (nb1 ^ b1)) != 0;
-    a0 = na0;
-    a1 = na1;
-    b0 = nb0;
-    b1 = nb1;
-    if (!__any_sync(FULL, ch)) break;
+    unsigned ch = 0;
+#pragma unroll
+    for (int q = 0; q < BNR; q++)
+#pragma unroll
+      for (int w = 0; w < BNW; w++) {
+        ch |= N[q][w] ^ A[q][w];
+        A[q][w] = N[q][w];
+      }
+    if (!__any_sync(FULL, ch != 0)) break;
     changed = true;
   }
   return steps;
@@ -2297,11 +2375,13 @@ __global__ void __launch_bounds__(kCtaThreads)
     const int x0 = tx * TSB, y0 = ty * TSB;
     long long c_load = pclock(l0);
     if (kPhases && l0) ph[0] += c_load - c_pop;
-    unsigned jt[4], mt[4];
+    unsigned A[BNR][BNW], M[BNR][BNW], O[BNR][BNW];  // O: as last published
     BinHalo h;
-    bin_load(a, x0, y0, lane, true, jt, mt, h);
-    unsigned a0 = jt[0], a1 = jt[1], b0 = jt[2], b1 = jt[3];
-    unsigned oa0 = a0, oa1 = a1, ob0 = b0, ob1 = b1;  // as last published
+    bin_load(a, x0, y0, lane, true, A, M, h);
+#pragma unroll
+    for (int q = 0; q < BNR; q++)
+#pragma unroll
+      for (int w = 0; w < BNW; w++) O[q][w] = A[q][w];
     if (kPhases && l0) ph[1] += clock64() - c_load;
     bool rerun = false;
     for (;;) {
@@ -2309,75 +2389,68 @@ __global__ void __launch_bounds__(kCtaThreads)
       n_reruns += l0 && rerun;
       long long c_fix = pclock(l0);
       bool changed = false;
-      const int steps = bin_fixpoint<CONN>(a0, a1, b0, b1, mt[0], mt[1], mt[2], mt[3], h, lane, changed);
+      const int steps = bin_fixpoint<CONN>(A, M, h, lane, changed);
       if (l0) n_steps += steps;
       changed = __any_sync(FULL, changed);
       long long c_st = pclock(l0);
       if (kPhases && l0) ph[2] += c_st - c_fix;
       if (changed) {
         uint32_t *Jw = (uint32_t *)a.J;
-        const int wx = x0 >> 5, ya = y0 + lane, yb = ya + 32;
-        if (ya < a.H) {
-          if (a0 != oa0) Jw[(size_t)ya * a.WW + wx] = a0;
-          if (a1 != oa1) Jw[(size_t)ya * a.WW + wx + 1] = a1;
-        }
-        if (yb < a.H) {
-          if (b0 != ob0) Jw[(size_t)yb * a.WW + wx] = b0;
-          if (b1 != ob1) Jw[(size_t)yb * a.WW + wx + 1] = b1;
+        const int wx = x0 >> 5;
+#pragma unroll
+        for (int q = 0; q < BNR; q++) {
+          const int gy = y0 + lane + 32 * q;
+          if (gy < a.H) {
+#pragma unroll
+            for (int w = 0; w < BNW; w++)
+              if (A[q][w] != O[q][w]) Jw[(size_t)gy * a.WW + wx + w] = A[q][w];
+          }
         }
         if (a.dirty && l0) a.dirty[ty] = 1;
         // newly set border cells; a neighbour needs a re-run where such a
         // cell (dilated along the border for 8-conn) meets a halo cell with
         // J = 0, I = 1
-        const unsigned ca0 = a0 & ~oa0, ca1 = a1 & ~oa1, cb0 = b0 & ~ob0, cb1 = b1 & ~ob1;
-        unsigned need_row = 0;
+        unsigned need_row = 0;  // lane 0: top row vs the row above; lane 31: bottom vs below
         {
-          const unsigned c0 = l0 ? ca0 : cb0, c1 = l0 ? ca1 : cb1;  // lane 0: top, 31: bottom
-          unsigned d0 = c0, d1 = c1;
-          if (CONN == 8) {
-            d0 = c0 | (c0 << 1) | (c0 >> 1) | (c1 << 31);
-            d1 = c1 | (c1 << 1) | (c0 >> 31) | (c1 >> 1);
+          const int qe = l0 ? 0 : BNR - 1;
+          unsigned c[BNW];
+#pragma unroll
+          for (int w = 0; w < BNW; w++) c[w] = (qe == 0 ? A[0][w] & ~O[0][w] : A[BNR - 1][w] & ~O[BNR - 1][w]);
+#pragma unroll
+          for (int w = 0; w < BNW; w++) {
+            unsigned d = c[w];
+            if (CONN == 8)
+              d |= (c[w] << 1) | (c[w] >> 1) | (w ? c[w - 1] >> 31 : 0u) | (w < BNW - 1 ? c[w + 1] << 31 : 0u);
+            need_row |= d & h.rowI[w] & ~h.row[w];
           }
-          need_row = (d0 & h.rowI0 & ~h.row0) | (d1 & h.rowI1 & ~h.row1);
         }
-        const unsigned cla = ca0 & 1u, clb = cb0 & 1u, cra = ca1 >> 31, crb = cb1 >> 31;
-        unsigned dla = cla, dlb = clb, dra = cra, drb = crb;
+        unsigned cl = 0, cr = 0;  // bit q: row lane + 32 q's left / right cell newly set
+#pragma unroll
+        for (int q = 0; q < BNR; q++) {
+          cl |= ((A[q][0] & ~O[q][0]) & 1u) << q;
+          cr |= ((A[q][BNW - 1] & ~O[q][BNW - 1]) >> 31) << q;
+        }
+        unsigned dl = cl, dr = cr;
         if (CONN == 8) {
-          unsigned u, d;
-          const unsigned clb0 = __shfl_sync(FULL, clb, 0), crb0 = __shfl_sync(FULL, crb, 0);
-          const unsigned cla31 = __shfl_sync(FULL, cla, 31), cra31 = __shfl_sync(FULL, cra, 31);
-          u = __shfl_up_sync(FULL, cla, 1); d = __shfl_down_sync(FULL, cla, 1);
-          if (l0) u = 0;
-          if (l31) d = clb0;
-          dla |= u | d;
-          u = __shfl_up_sync(FULL, clb, 1); d = __shfl_down_sync(FULL, clb, 1);
-          if (l0) u = cla31;
-          if (l31) d = 0;
-          dlb |= u | d;
-          u = __shfl_up_sync(FULL, cra, 1); d = __shfl_down_sync(FULL, cra, 1);
-          if (l0) u = 0;
-          if (l31) d = crb0;
-          dra |= u | d;
-          u = __shfl_up_sync(FULL, crb, 1); d = __shfl_down_sync(FULL, crb, 1);
-          if (l0) u = cra31;
-          if (l31) d = 0;
-          drb |= u | d;
+          dl |= bits_up(cl, lane, 0u) | bits_dn(cl, lane, 0u);
+          dr |= bits_up(cr, lane, 0u) | bits_dn(cr, lane, 0u);
         }
         unsigned dirs = 0;
         if (__any_sync(FULL, l0 && need_row)) dirs |= 1u << 1;   // N
         if (__any_sync(FULL, l31 && need_row)) dirs |= 1u << 7;  // S
-        if (__any_sync(FULL, (dla & h.lIa & ~h.la) | (dlb & h.lIb & ~h.lb))) dirs |= 1u << 3;  // W
-        if (__any_sync(FULL, (dra & h.rIa & ~h.ra) | (drb & h.rIb & ~h.rb))) dirs |= 1u << 5;  // E
-        if (CONN == 8) {
-          if (__any_sync(FULL, l0 && (cla & h.clI & ~h.cl))) dirs |= 1u << 0;
-          if (__any_sync(FULL, l0 && (cra & h.crI & ~h.cr))) dirs |= 1u << 2;
-          if (__any_sync(FULL, l31 && (clb & h.clI & ~h.cl))) dirs |= 1u << 6;
-          if (__any_sync(FULL, l31 && (crb & h.crI & ~h.cr))) dirs |= 1u << 8;
+        if (__any_sync(FULL, dl & h.lI & ~h.l)) dirs |= 1u << 3;  // W
+        if (__any_sync(FULL, dr & h.rI & ~h.r)) dirs |= 1u << 5;  // E
+        if (CONN == 8) {  // corners: one interior cell each
+          const unsigned c0l = cl & 1u, c0r = cr & 1u, c3l = (cl >> (BNR - 1)) & 1u, c3r = (cr >> (BNR - 1)) & 1u;
+          if (__any_sync(FULL, l0 && (c0l & h.clI & ~h.cl))) dirs |= 1u << 0;
+          if (__any_sync(FULL, l0 && (c0r & h.crI & ~h.cr))) dirs |= 1u << 2;
+          if (__any_sync(FULL, l31 && (c3l & h.clI & ~h.cl))) dirs |= 1u << 6;
+          if (__any_sync(FULL, l31 && (c3r & h.crI & ~h.cr))) dirs |= 1u << 8;
         }
-        oa0 = a0;
-        oa1 = a1;
-        ob0 = b0;
-        ob1 = b1;
+#pragma unroll
+        for (int q = 0; q < BNR; q++)
+#pragma unroll
+          for (int w = 0; w < BNW; w++) O[q][w] = A[q][w];
         // publish the tile before any neighbour is (re)queued, and before
         // this tile's finish: the finish CAS is what lets a later activation
         // pop the tile again, and its next owner must load these values (a
@@ -2416,7 +2489,7 @@ __global__ void __launch_bounds__(kCtaThreads)
       done = __shfl_sync(FULL, done, 0);
       if (kPhases && l0) ph[5] += clock64() - c_st;
       if (done) break;
-      bin_load(a, x0, y0, lane, false, jt, mt, h);  // the tile is ours: halo only
+      bin_load(a, x0, y0, lane, false, A, M, h);  // the tile is ours: halo only
       rerun = true;
     }
   }

@@ -7,7 +7,7 @@ namespace recon {
 
 // One warp owns one TS x TS tile at a time (plus a 1-pixel halo).
 constexpr int TS = 32;                   // tile side
-constexpr int TSB = 64;                  // the binary engine's tile side (the largest)
+constexpr int TSB = 128;                 // the binary engine's tile side (the largest)
 constexpr int PW = TS + 2;               // logical tile side with the halo
 constexpr int PS = PW + 1;               // shared-memory row stride (odd: conflict-free)
 constexpr int PN = PW * PW;              // logical cells
