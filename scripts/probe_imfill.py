@@ -40,6 +40,10 @@ for conn in (4, 8):
                 ts.append(a.elapsed_time(b))
         cnt = (_lib.ctypes.c_uint64 * 16)()
         L.iwpp_recon_engine_counters(_lib.ptr(ws), W, H, cnt, 16, _lib.stream_ptr())
-        ntiles = ((W + 63) // 64) * ((H + 63) // 64)
+        ntiles = ((W + 127) // 128) * ((H + 127) // 128)  # the binary engine's 128 x 128 tiles
         print(f"imfill 16K c{conn} {form}: {np.median(ts):.3f} ms (min {min(ts):.3f}); activations {cnt[0]} "
               f"({cnt[0] / ntiles:.2f}/tile) reruns {cnt[1]} steps/act {cnt[6] / max(cnt[0], 1):.2f}", flush=True)
+        if cnt[8] or cnt[13]:  # -DIWPP_PHASES build: cycles per activation (lane 0)
+            na = max(cnt[0], 1)
+            print("   phases (cycles/activation): pop %.0f load %.0f fix %.0f publish %.0f"
+                  % (cnt[8] / na, cnt[9] / na, cnt[10] / na, cnt[13] / na), flush=True)
