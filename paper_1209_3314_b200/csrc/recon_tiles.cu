@@ -2189,6 +2189,62 @@ __device__ __forceinline__ void bin_load(const EngineArgs &a, int x0, int y0, in
   h.cl = jhl >> 31; h.cr = jhr & 1u; h.clI = ihl >> 31; h.crI = ihr & 1u;
 }
 
+// TMA staging of a binary tile (bit planes with W % 128 == 0): one box per
+// plane of 12 words x 130 rows -- image words wx - 4 .. wx + 7 (16-byte
+// aligned start; the tile is words 4..7, its halo words 3 and 8) and rows
+// y0 - 1 .. y0 + 128 -- instead of ~60 scattered per-lane loads; cells
+// outside the image arrive as 0, the plane's own outside value.
+constexpr int kBinBoxW = 12, kBinBoxH = TSB + 2, kBinBoxX = 4;
+struct alignas(128) BinBoxSmem {  // (TMA destinations 128-byte aligned)
+  uint32_t J[kBinBoxH][kBinBoxW];
+  uint8_t pad0[(128 - kBinBoxH * kBinBoxW * 4 % 128) % 128];
+  uint32_t I[kBinBoxH][kBinBoxW];
+  uint8_t pad1[(128 - kBinBoxH * kBinBoxW * 4 % 128) % 128];
+  unsigned long long bar;
+};
+static_assert(offsetof(BinBoxSmem, I) % 128 == 0, "TMA destination alignment");
+
+__device__ __forceinline__ void bin_load_box(const CUtensorMap *maps, BinBoxSmem &b, int x0, int y0,
+                                             int lane, bool tile, unsigned &phase,
+                                             unsigned (&jt)[BNR][BNW], unsigned (&mt)[BNR][BNW],
+                                             BinHalo &h) {
+  constexpr unsigned BYTES = kBinBoxH * kBinBoxW * 4;
+  __syncwarp();  // the previous boxes have been read
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mbar_expect_tx(&b.bar, tile ? 2u * BYTES : BYTES);
+    tma_load_box(maps, &b.J[0][0], &b.bar, (x0 >> 5) - kBinBoxX, y0 - 1);
+    if (tile) tma_load_box(maps + 1, &b.I[0][0], &b.bar, (x0 >> 5) - kBinBoxX, y0 - 1);
+  }
+  mbar_wait(&b.bar, phase);
+  phase ^= 1u;
+  h.l = h.r = h.lI = h.rI = 0;
+#pragma unroll
+  for (int q = 0; q < BNR; q++) {
+    const int r = lane + 32 * q + 1;
+    if (tile) {
+      const uint4 vj = *reinterpret_cast<const uint4 *>(&b.J[r][kBinBoxX]);
+      const uint4 vi = *reinterpret_cast<const uint4 *>(&b.I[r][kBinBoxX]);
+      jt[q][0] = vj.x; jt[q][1] = vj.y; jt[q][2] = vj.z; jt[q][3] = vj.w;
+      mt[q][0] = vi.x; mt[q][1] = vi.y; mt[q][2] = vi.z; mt[q][3] = vi.w;
+    }
+    h.l |= (b.J[r][kBinBoxX - 1] >> 31) << q;
+    h.r |= (b.J[r][kBinBoxX + BNW] & 1u) << q;
+    h.lI |= (b.I[r][kBinBoxX - 1] >> 31) << q;
+    h.rI |= (b.I[r][kBinBoxX + BNW] & 1u) << q;
+  }
+  const int hr = lane == 0 ? 0 : kBinBoxH - 1;  // halo row (lanes 0 / 31)
+#pragma unroll
+  for (int w = 0; w < BNW; w++) {
+    h.row[w] = b.J[hr][kBinBoxX + w];
+    h.rowI[w] = b.I[hr][kBinBoxX + w];
+  }
+  h.cl = b.J[hr][kBinBoxX - 1] >> 31;
+  h.cr = b.J[hr][kBinBoxX + BNW] & 1u;
+  h.clI = b.I[hr][kBinBoxX - 1] >> 31;
+  h.crI = b.I[hr][kBinBoxX + BNW] & 1u;
+}
+
 // Vertical neighbours of a column of per-row bits packed as bit q = row
 // lane + 32 q (the rows above / below within the tile; `in_up` / `in_dn`:
 // lane 0's bit 0 above / lane 31's bit BNR-1 below come from outside).
@@ -2351,10 +2407,19 @@ __device__ __forceinline__ int bin_fixpoint(unsigned (&A)[BNR][BNW], const unsig
 }
 
 template <int CONN>
-__global__ void __launch_bounds__(kCtaThreads)
-    tile_engine_bin_kernel(EngineArgs a, unsigned long long *counters) {
+__global__ void __launch_bounds__(kCtaThreads, 3)
+    tile_engine_bin_kernel(EngineArgs a, unsigned long long *counters,
+                           const __grid_constant__ BoxMaps maps, int use_tma) {
+  extern __shared__ __align__(128) unsigned char bin_dsmem[];  // use_tma: one BinBoxSmem per warp
   const int lane = threadIdx.x & 31;
   const bool l0 = lane == 0, l31 = lane == 31;
+  BinBoxSmem &bx = reinterpret_cast<BinBoxSmem *>(bin_dsmem)[threadIdx.x >> 5];
+  unsigned tphase = 0;
+  if (use_tma && l0) {
+    mbar_init(&bx.bar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
   unsigned long long n_tiles = 0, n_reruns = 0, n_steps = 0;
   unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
   int next_tile = -1;
@@ -2377,7 +2442,10 @@ __global__ void __launch_bounds__(kCtaThreads)
     if (kPhases && l0) ph[0] += c_load - c_pop;
     unsigned A[BNR][BNW], M[BNR][BNW], O[BNR][BNW];  // O: as last published
     BinHalo h;
-    bin_load(a, x0, y0, lane, true, A, M, h);
+    if (use_tma)
+      bin_load_box(&maps.m[0], bx, x0, y0, lane, true, tphase, A, M, h);
+    else
+      bin_load(a, x0, y0, lane, true, A, M, h);
 #pragma unroll
     for (int q = 0; q < BNR; q++)
 #pragma unroll
@@ -2489,7 +2557,10 @@ __global__ void __launch_bounds__(kCtaThreads)
       done = __shfl_sync(FULL, done, 0);
       if (kPhases && l0) ph[5] += clock64() - c_st;
       if (done) break;
-      bin_load(a, x0, y0, lane, false, A, M, h);  // the tile is ours: halo only
+      if (use_tma)  // the tile is ours: halo only
+        bin_load_box(&maps.m[0], bx, x0, y0, lane, false, tphase, A, M, h);
+      else
+        bin_load(a, x0, y0, lane, false, A, M, h);
       rerun = true;
     }
   }
@@ -2748,7 +2819,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static bool make_box_map(CUtensorMap *map, const void *base, int W, int H, int esize, int boxW) {
+static bool make_box_map(CUtensorMap *map, const void *base, int W, int H, int esize, int boxW,
+                         int boxH = kBoxH) {
   static EncodeTiledFn encode = nullptr;
   static int tried = 0;
   if (!tried) {
@@ -2764,7 +2836,7 @@ static bool make_box_map(CUtensorMap *map, const void *base, int W, int H, int e
   if (!encode || ((size_t)W * esize) % 16 != 0 || (uintptr_t)base % 16 != 0) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)H};
   const cuuint64_t strides[1] = {(cuuint64_t)W * esize};
-  const cuuint32_t box[2] = {(cuuint32_t)boxW, (cuuint32_t)kBoxH};
+  const cuuint32_t box[2] = {(cuuint32_t)boxW, (cuuint32_t)boxH};
   const cuuint32_t estr[2] = {1, 1};
   const CUtensorMapDataType dt = esize == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                  : esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
@@ -2940,11 +3012,20 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
   EngineArgs a{J, I, W, H, ntx, nty, qlimit, hth, o.sweeps, vec ? 1 : 0, o.dirty, (W + 31) / 32, q, ntx_m};
   if (o.ev_begin) IWPP_CUDA_TRY(cudaEventRecord((cudaEvent_t)o.ev_begin, st));
   if (use_bin_engine(binary, o)) {
+    // TMA boxes when the plane's rows are 16-byte multiples (W % 128 == 0)
+    BoxMaps maps;
+    const int WW = (W + 31) / 32;
+    int use_tma = (WW % 4 == 0) && !getenv("IWPP_BIN_NO_TMA") &&
+                  make_box_map(&maps.m[0], J, WW, H, 4, kBinBoxW, kBinBoxH) &&
+                  make_box_map(&maps.m[1], I, WW, H, 4, kBinBoxW, kBinBoxH);
+    const size_t dsm = use_tma ? kWarpsPerCta * sizeof(BinBoxSmem) : 0;
     static int bin_blocks = 0;
     if (bin_blocks == 0) {
       int per_sm = 0;
+      IWPP_CUDA_TRY(cudaFuncSetAttribute(tile_engine_bin_kernel<CONN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kWarpsPerCta * sizeof(BinBoxSmem))));
       IWPP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_engine_bin_kernel<CONN>,
-                                                                  kCtaThreads, 0));
+                                                                  kCtaThreads, kWarpsPerCta * sizeof(BinBoxSmem)));
       // more resident warps than this only adds idle pollers on the tile
       // ring (binary fills are narrow fronts): measured best at 4 CTAs/SM
       int cap = kBinCtasPerSm;
@@ -2955,7 +3036,7 @@ static int launch_engine(void *J, const void *I, int W, int H, TileQueue q,
     int bb = bin_blocks;
     if (o.max_blocks > 0 && bb > o.max_blocks) bb = o.max_blocks;
     if ((unsigned)bb > max_b) bb = (int)max_b;
-    tile_engine_bin_kernel<CONN><<<bb, kCtaThreads, 0, st>>>(a, counters);
+    tile_engine_bin_kernel<CONN><<<bb, kCtaThreads, dsm, st>>>(a, counters, maps, use_tma);
   } else if (sizeof(T) > 1 && use_reg_engine<T>(o)) {  // 16 / 32-bit register engine
     const int rc = launch_reg32<T, CONN>(a, counters, q, J, I, W, H, o, max_b, fused_init, st, f32);
     if (rc) return rc;
