@@ -2379,7 +2379,19 @@ __device__ __forceinline__ int bin_fixpoint(unsigned (&A)[BNR][BNW], const unsig
       }
 #pragma unroll
       for (int w = 0; w < BNW; w++) N[q][w] = M[q][w] & D[w];
-      if (IWPP_BIN_RUNFILL) row_fill(N[q], M[q]);  // whole row runs in one step
+    }
+    // The plain step is the fixed-point test: if it adds nothing, no mask
+    // cell touches a set cell, so the run fills below cannot add anything
+    // either.  Only a step that changes something pays for the fills.
+    unsigned ch = 0;
+#pragma unroll
+    for (int q = 0; q < BNR; q++)
+#pragma unroll
+      for (int w = 0; w < BNW; w++) ch |= N[q][w] ^ A[q][w];
+    if (!__any_sync(FULL, ch != 0)) break;
+    if (IWPP_BIN_RUNFILL) {  // whole row runs in one step
+#pragma unroll
+      for (int q = 0; q < BNR; q++) row_fill(N[q], M[q]);
     }
     if (IWPP_BIN_COLFILL) {  // and whole column runs of the tile
 #pragma unroll
@@ -2392,15 +2404,10 @@ __device__ __forceinline__ int bin_fixpoint(unsigned (&A)[BNR][BNW], const unsig
         for (int q = 0; q < BNR; q++) N[q][w] = x[q];
       }
     }
-    unsigned ch = 0;
 #pragma unroll
     for (int q = 0; q < BNR; q++)
 #pragma unroll
-      for (int w = 0; w < BNW; w++) {
-        ch |= N[q][w] ^ A[q][w];
-        A[q][w] = N[q][w];
-      }
-    if (!__any_sync(FULL, ch != 0)) break;
+      for (int w = 0; w < BNW; w++) A[q][w] = N[q][w];
     changed = true;
   }
   return steps;
