@@ -1,10 +1,10 @@
 #!/bin/bash
-# Round-2 (session 5) re-captures after the 128x128 binary engine: both bench
+# Round-2 (session 5) re-captures after the binary engine changes (128x128 tiles, TMA staging, cheap fixed-point test): both bench
 # arms, the launch list of the headline bench command and one `--set full`
 # capture of the imfill kernels (same format as prof_r02.sh; summarised by
-# `scripts/summarize_r02.py gpurun_out/r02d r02d`).
+# `scripts/summarize_r02.py gpurun_out/r02e r02e`).
 set -u
-OUT=gpurun_out/r02d
+OUT=gpurun_out/r02e
 mkdir -p $OUT
 ATOM=lts__t_requests_op_atom.sum,lts__t_requests_op_red.sum,lts__t_sectors_op_atom.sum,lts__t_sectors_op_red.sum,lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,dram__bytes_write.sum
 full() {
