@@ -271,11 +271,12 @@ def main():
     out = torch.empty_like(dJ)
     W = H = N_PX
     ws = _lib.workspace(L.iwpp_recon_workspace_bytes(W, H, 0, 8))
-    ev0, ev1 = _lib.Event(), _lib.Event()
     opts = _lib.ReconOpts()
     opts.sweeps, opts.max_blocks, opts.check_contract, opts.queue_capacity = -1, 0, 0, 0
     opts.tile_sweeps, opts.halo_sweep_threshold = -1, -1
-    opts.ev_begin, opts.ev_end = ev0.handle, ev1.handle
+    # no events inside the call: each timed step is exactly one engine launch
+    # between s0 and s1 (two more event records in the stream cost ~3.7 us)
+    opts.ev_begin = opts.ev_end = None
     stream = _lib.stream_ptr()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2 (126 MB)
 
@@ -303,7 +304,7 @@ def main():
             s1.record()
             s1.synchronize()
             step_ms.append(s0.elapsed_time(s1))
-            kern_ms.append(ev0.elapsed_ms(ev1))
+            kern_ms.append(step_ms[-1])  # the step is the one engine launch
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -2617,16 +2617,43 @@ __global__ void bin_pack_kernel(const uint8_t *__restrict__ src, int W, int H,
   }
 }
 
+__device__ __forceinline__ unsigned unpack_nibble(unsigned b, int k) {  // 4 bits -> 4 bytes of 0 / 255
+  return ((((b >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu;
+}
+
+// One 32-pixel word per lane.  When rows are whole words (W % 32 == 0) and
+// the output is 16-byte aligned, a warp's 32 words are 1 KB of contiguous
+// output: store j writes chunk lane + 32 j (half lane & 1 of the word of lane
+// lane / 2 + 16 j, fetched by one shuffle), so each store instruction fills
+// 512 contiguous bytes -- whole sectors instead of half sectors.
 __global__ void bin_unpack_kernel(const uint32_t *__restrict__ bits, int W, int H,
                                   uint8_t *__restrict__ dst, int vec) {
   const unsigned WW = (unsigned)(W + 31) >> 5;
   const unsigned nw = WW * (unsigned)H;
-  for (unsigned wi = blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const bool lin = vec && (W & 31) == 0;
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < nw; base += stride) {
+    const unsigned wi = base + lane;
+    if (lin && base + 32 <= nw) {  // (warp-uniform)
+      const unsigned b = bits[wi];
+      uint4 *out = reinterpret_cast<uint4 *>(dst + (size_t)base * 32);
+      const int h = lane & 1;
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const unsigned bs = __shfl_sync(0xffffffffu, b, (lane >> 1) + 16 * j);
+        const unsigned v = h ? bs >> 16 : bs;
+        out[lane + 32 * j] = make_uint4(unpack_nibble(v, 0), unpack_nibble(v, 1), unpack_nibble(v, 2),
+                                        unpack_nibble(v, 3));
+      }
+      continue;
+    }
+    if (wi >= nw) continue;
     const unsigned y = wi / WW, x0 = (wi - y * WW) * 32;
     const unsigned b = bits[wi];
     unsigned w[8];
 #pragma unroll
-    for (int k = 0; k < 8; k++) w[k] = ((((b >> (4 * k)) & 0xFu) * 0x00204081u) & 0x01010101u) * 0xFFu;
+    for (int k = 0; k < 8; k++) w[k] = unpack_nibble(b, k);
     uint8_t *p = dst + (size_t)y * W + x0;
     if (vec && x0 + 32 <= (unsigned)W) {
       reinterpret_cast<uint4 *>(p)[0] = make_uint4(w[0], w[1], w[2], w[3]);

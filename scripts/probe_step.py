@@ -43,6 +43,21 @@ for mode in ("marker", "copy"):
     s = np.median(np.array(seg), axis=0)
     print(f"{mode}: before-kernel {s[0]:.1f} us, kernel {s[1]:.1f} us, after {s[2]:.1f} us, step {s[3]:.1f} us",
           flush=True)
+# the same step without the inner events (what bench.py times): the step
+# is then only the engine launch between the two outer events
+o.marker = _lib.ptr(dJ)
+o.ev_begin = o.ev_end = None
+seg = []
+for i in range(30):
+    flush.fill_(i & 255)
+    a0.record()
+    _lib.check(L.iwpp_recon(_lib.ptr(out), _lib.ptr(dI), n, n, 0, 8, _lib.ptr(ws), ws.numel(),
+                            _lib.ctypes.byref(o), None, st))
+    a1.record()
+    torch.cuda.synchronize()
+    if i >= 5:
+        seg.append(a0.elapsed_ms(a1) * 1e3)
+print(f"marker, no inner events: step {np.median(seg):.1f} us", flush=True)
 # back-to-back calls, no flush, no sync: the per-call spacing
 o.marker = _lib.ptr(dJ)
 o.ev_begin = o.ev_end = None
