@@ -213,8 +213,7 @@ int iwpp_recon(void *J, const void *I, int64_t W, int64_t H, int dtype, int conn
   if (dtype == IWPP_BIN) {  // the bit-plane engine: pack, propagate, unpack
     const size_t nw = recon::bin_plane_words(W, H);
     uint32_t *Jb = c.take<uint32_t>(nw), *Ib = c.take<uint32_t>(nw);
-    if ((rc = recon::bin_pack(msrc ? msrc : J, (int)W, (int)H, Jb, st))) return rc;
-    if ((rc = recon::bin_pack(I, (int)W, (int)H, Ib, st))) return rc;
+    if ((rc = recon::bin_pack(msrc ? msrc : J, (int)W, (int)H, Jb, st, I, Ib))) return rc;
     eo.src = nullptr;  // (J is written whole by the unpack)
     if ((rc = recon::run_tile_engine(Jb, Ib, (int)W, (int)H, IWPP_BIN, conn, w.q, w.counters, eo, st)))
       return rc;

@@ -2593,8 +2593,14 @@ __device__ __forceinline__ unsigned pack_bits(const unsigned *w) {
   return b;
 }
 
-__global__ void bin_pack_kernel(const uint8_t *__restrict__ src, int W, int H,
-                                uint32_t *__restrict__ bits, int vec) {
+// blockIdx.y selects the plane: (src, bits) or (src2, bits2) -- the marker
+// and the mask are packed by one launch
+__global__ void bin_pack_kernel(const uint8_t *__restrict__ src0, int W, int H,
+                                uint32_t *__restrict__ bits0, int vec0,
+                                const uint8_t *__restrict__ src2, uint32_t *__restrict__ bits2, int vec2) {
+  const uint8_t *__restrict__ src = blockIdx.y ? src2 : src0;
+  uint32_t *__restrict__ bits = blockIdx.y ? bits2 : bits0;
+  const int vec = blockIdx.y ? vec2 : vec0;
   const unsigned WW = (unsigned)(W + 31) >> 5;
   const unsigned nw = WW * (unsigned)H;
   for (unsigned wi = blockIdx.x * blockDim.x + threadIdx.x; wi < nw; wi += gridDim.x * blockDim.x) {
@@ -2666,12 +2672,15 @@ __global__ void bin_unpack_kernel(const uint32_t *__restrict__ bits, int W, int 
 
 size_t bin_plane_words(int64_t W, int64_t H) { return (size_t)((W + 31) / 32) * (size_t)H; }
 
-int bin_pack(const void *src, int W, int H, uint32_t *bits, cudaStream_t st) {
+int bin_pack(const void *src, int W, int H, uint32_t *bits, cudaStream_t st, const void *src2,
+             uint32_t *bits2) {
   size_t threads = bin_plane_words(W, H);
-  size_t blocks = (threads + 255) / 256, cap = (size_t)device_sm_count() * 16;
+  size_t blocks = (threads + 255) / 256, cap = (size_t)device_sm_count() * (src2 ? 8 : 16);
   const int vec = W % 16 == 0 && (uintptr_t)src % 16 == 0;
-  bin_pack_kernel<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, st>>>((const uint8_t *)src, W, H,
-                                                                           bits, vec);
+  const int vec2 = W % 16 == 0 && (uintptr_t)src2 % 16 == 0;
+  const dim3 grid((unsigned)(blocks < cap ? blocks : cap), src2 ? 2u : 1u);
+  bin_pack_kernel<<<grid, 256, 0, st>>>((const uint8_t *)src, W, H, bits, vec, (const uint8_t *)src2,
+                                        bits2, vec2);
   IWPP_CUDA_TRY(cudaGetLastError());
   return IWPP_OK;
 }

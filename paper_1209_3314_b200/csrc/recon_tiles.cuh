@@ -108,7 +108,9 @@ int tile_side(int dtype, const EngineOpts &o);
 int atrace_control(void *buf, unsigned cap, unsigned *n_out);
 // binary kind: J / I as bit planes (ceil(W/32) words per row) for the engine
 size_t bin_plane_words(int64_t W, int64_t H);
-int bin_pack(const void *src, int W, int H, uint32_t *bits, cudaStream_t st);
+// (src2 / bits2: a second plane packed by the same launch)
+int bin_pack(const void *src, int W, int H, uint32_t *bits, cudaStream_t st,
+             const void *src2 = nullptr, uint32_t *bits2 = nullptr);
 int bin_unpack(const uint32_t *bits, int W, int H, void *dst, cudaStream_t st);
 
 inline unsigned num_tiles(int64_t W, int64_t H) {
