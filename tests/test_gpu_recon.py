@@ -412,6 +412,52 @@ def test_binary_engine_vs_oracle(gw, conn):
         assert np.array_equal(_np(out.data), want)
 
 
+def _serpentine(H, W, pitch=3):
+    """A one-pixel-wide corridor snaking down the image (rows every `pitch`,
+    joined alternately at the right and left ends) and its far-end marker:
+    the fill must cross every 128 x 128 bit tile many times."""
+    mask = np.zeros((H, W), np.uint8)
+    rows = list(range(1, H - 1, pitch))
+    for k, y in enumerate(rows):
+        mask[y, 1:W - 1] = 255
+        if k + 1 < len(rows):
+            x = W - 2 if k % 2 == 0 else 1
+            mask[y:rows[k + 1] + 1, x] = 255
+    marker = np.zeros_like(mask)
+    marker[rows[0], 1] = 255
+    return marker, mask
+
+
+@pytest.mark.parametrize("conn", [4, 8])
+def test_binary_engine_long_paths(gw, conn):
+    """The 128 x 128 bit-tile engine on inputs whose propagation crosses
+    tiles, words and 32-row quarters many times: a serpentine corridor on a
+    TMA-staged width (W % 128 == 0) and on a per-lane width, a diagonal
+    staircase (8-conn corner hops), and near-percolation random masks in
+    wide and tall shapes -- all against the oracle."""
+    t = _torch()
+    rng = np.random.default_rng(77 + conn)
+    cases = [_serpentine(389, 640), _serpentine(389, 600, pitch=4)]
+    st = np.zeros((700, 768), np.uint8)  # a staircase: diagonal steps of 1 px
+    for i in range(0, 690):
+        st[i, i % 768] = 255
+        st[i, (i + 1) % 768] = 255
+    m0 = np.zeros_like(st)
+    m0[0, 0] = 255
+    cases.append((m0, st))
+    for shape in [(130, 2048), (2048, 130), (384, 640)]:
+        mask = (rng.random(shape) < 0.6).astype(np.uint8) * 255
+        marker = np.where((rng.random(shape) < 0.001) & (mask == 255), 255, 0).astype(np.uint8)
+        cases.append((marker, mask))
+    for marker, mask in cases:
+        want = oracle.recon_fh(marker, mask, conn)
+        got = gw.reconstruct(t.from_numpy(marker).cuda(), t.from_numpy(mask).cuda(), conn,
+                             kind="binary")
+        assert np.array_equal(got.cpu().numpy(), want), marker.shape
+        got = gw.reconstruct(marker, mask, conn, kind="binary", pipeline_rows=128)
+        assert np.array_equal(got, want), (marker.shape, "host")
+
+
 def test_reconstruct_validates_raw_inputs(gw):
     """reconstruct() on raw arrays checks shape, dtype and residency before
     any kernel reads the buffers (an int32 marker with a u8 mask, or a
