@@ -973,7 +973,62 @@ __global__ void __launch_bounds__(kRoundThreads) edt_rounds_raster_kernel(int W,
       }
       __syncthreads();
       unsigned o = blk_base + wsum[warp] + incl - c;
-      if (c) {
+      if (CONN == 8) {
+        // 8-conn: the warp writes its items together, 32 consecutive list
+        // entries per store -- item j goes to lane j % 32, which finds the
+        // owning lane (the last with exclusive count <= j) by a binary
+        // search over the lanes, then the word and the bit (__fns) in that
+        // lane's words.  Same order as the per-thread walk below; coalesced
+        // stores, no divergent per-bit loops.  Blob 4K^2 c8 5.59 -> 5.28 ms
+        // (compaction 11.2 -> 8.3 us per raster round); the 4-conn kernel
+        // measured 2-4% slower with it, so it keeps the walk.
+        if (c) {
+          if (full) {
+            *reinterpret_cast<uint4 *>(Fb + wi) = make_uint4(0u, 0u, 0u, 0u);
+          } else {
+            for (unsigned k = 0; k < kRasterWpt; k++)
+              if (w4[k]) Fb[wi + k] = 0u;
+          }
+        }
+        const unsigned excl = incl - c;
+        const unsigned wtot = __shfl_sync(FULL, incl, 31);
+        const unsigned obase = blk_base + wsum[warp];
+        const unsigned wbase = wb + warp * 32u * kRasterWpt;  // this warp's first word
+        for (unsigned j0 = 0; j0 < wtot; j0 += 32) {
+          const unsigned j = j0 + lane;
+          unsigned lo = 0;
+#pragma unroll
+          for (unsigned step = 16; step; step >>= 1) {
+            const unsigned e = __shfl_sync(FULL, excl, lo + step);
+            if (e <= j) lo += step;
+          }
+          unsigned r = j - __shfl_sync(FULL, excl, lo);
+          unsigned ow[kRasterWpt];
+#pragma unroll
+          for (unsigned k = 0; k < kRasterWpt; k++) ow[k] = __shfl_sync(FULL, w4[k], lo);
+          unsigned kk = 0, word = ow[0];
+          bool found = false;
+#pragma unroll
+          for (unsigned k = 0; k < kRasterWpt; k++) {
+            const unsigned pc = __popc(ow[k]);
+            if (!found) {
+              if (r < pc) {
+                kk = k;
+                word = ow[k];
+                found = true;
+              } else {
+                r -= pc;
+              }
+            }
+          }
+          if (j < wtot) {
+            const unsigned bb = __fns(word, 0, (int)r + 1);
+            const unsigned wi2 = wbase + lo * kRasterWpt + kk;
+            const unsigned y = wi2 / (unsigned)WW, x0 = (wi2 - y * (unsigned)WW) * 32;
+            nxt[obase + j] = (y << 16) | (x0 + bb);
+          }
+        }
+      } else if (c) {
         if (full) {
           *reinterpret_cast<uint4 *>(Fb + wi) = make_uint4(0u, 0u, 0u, 0u);
         } else {
